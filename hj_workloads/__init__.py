@@ -203,10 +203,10 @@ def _scaled(n: int, scale: float, ratio: int) -> int:
     return cells + 1
 
 
-def config1(seed: int = 0, scale: float = 1.0) -> Config:
+def config1(seed: int = 0, scale: float = 1.0, ratio=None) -> Config:
     """2D eikonal minimum time, 32 unit controls, [-1,1]^2, 101^2, 4 balls r=0.05
     at (+-0.5,+-0.5), Kruzkov, h = dx, tol 1e-10, 4 sub-domains."""
-    ratio = 5
+    ratio = 5 if ratio is None else int(ratio)
     n = _scaled(101, scale, ratio)
     g = Grid((n, n), (-1.0, -1.0), (1.0, 1.0), (False, False))
     centres = [(-0.5, -0.5), (0.5, -0.5), (-0.5, 0.5), (0.5, 0.5)]
@@ -223,10 +223,10 @@ def config1(seed: int = 0, scale: float = 1.0) -> Config:
                   note="closed form T(x)=min_k |x-c_k|-r_k; Voronoi labels")
 
 
-def config2(seed: int = 2, scale: float = 1.0) -> Config:
+def config2(seed: int = 2, scale: float = 1.0, ratio=None) -> Config:
     """2D variable-speed eikonal, c = 1+0.5 sin sin, 64 controls, 1025^2 fp32,
     8 balls r=0.03 seeded in [-0.9,0.9]^2, tol 1e-7, coarse 129^2."""
-    ratio = 8
+    ratio = 8 if ratio is None else int(ratio)
     n = _scaled(1025, scale, ratio)
     g = Grid((n, n), (-1.0, -1.0), (1.0, 1.0), (False, False))
     centres = seeded_centres(seed, 8, 0.9)
@@ -242,10 +242,10 @@ def config2(seed: int = 2, scale: float = 1.0) -> Config:
                   dtype="f32", n_max_steps=8 * cg.n[0])
 
 
-def config3(seed: int = 3, scale: float = 1.0) -> Config:
+def config3(seed: int = 3, scale: float = 1.0, ratio=None) -> Config:
     """2D Zermelo: f = a + (0.5 y, 0), 64 controls, [-2,2]^2, 4097^2 fp32,
     16 balls r=0.04 seeded, coarse 257^2, overlap band 4 cells."""
-    ratio = 16
+    ratio = 16 if ratio is None else int(ratio)
     n = _scaled(4097, scale, ratio)
     g = Grid((n, n), (-2.0, -2.0), (2.0, 2.0), (False, False))
     centres = seeded_centres(seed, 16, 1.8)
@@ -263,10 +263,10 @@ def config3(seed: int = 3, scale: float = 1.0) -> Config:
                   dtype="f32", n_max_steps=8 * cg.n[0])
 
 
-def config4(seed: int = 4, scale: float = 1.0) -> Config:
+def config4(seed: int = 4, scale: float = 1.0, ratio=None) -> Config:
     """3D Dubins car: (cos th, sin th, a), a in 11 values in [-1,1], (x,y) in
     [-3,3]^2, th periodic, 257x257x128 fp32, 8 disks r=0.2 seeded."""
-    ratio = (4, 4, 4)
+    ratio = (4, 4, 4) if ratio is None else (int(ratio),) * 3
     nxy = _scaled(257, scale, ratio[0])
     nth = max(ratio[2] * 2, int(round(128 * scale / ratio[2])) * ratio[2])
     g = Grid((nxy, nxy, nth), (-3.0, -3.0, 0.0), (3.0, 3.0, 2 * np.pi), (False, False, True))
@@ -283,12 +283,12 @@ def config4(seed: int = 4, scale: float = 1.0) -> Config:
                   n_max_steps=8 * cg.n[0])
 
 
-def config5(seed: int = 5, scale: float = 1.0) -> Config:
+def config5(seed: int = 5, scale: float = 1.0, ratio=None) -> Config:
     """2D discounted regulator: f = (x2, a - 0.5 x1), 33 controls in [-1,1],
     l = |x|^2 + 0.1 a^2, lambda = 1, [-2,2]^2, 16385^2 fp32, 32 sub-domains from
     a 513^2 coarse feedback, tol 1e-6.  Reading R12: target B(0,0.2) cut in 32
     sectors (paper §4.1 "slices of a cake"); reading R5b: h = dx^(2/3)."""
-    ratio = 32
+    ratio = 32 if ratio is None else int(ratio)
     n = _scaled(16385, scale, ratio)
     g = Grid((n, n), (-2.0, -2.0), (2.0, 2.0), (False, False))
     A = np.zeros((3, 3))
@@ -312,9 +312,15 @@ def config5(seed: int = 5, scale: float = 1.0) -> Config:
 CONFIGS = {1: config1, 2: config2, 3: config3, 4: config4, 5: config5}
 
 
-def make(idx: int, scale: float = 1.0, seed: Optional[int] = None) -> Config:
+def make(idx: int, scale: float = 1.0, seed: Optional[int] = None, ratio=None) -> Config:
+    """BASELINE config `idx` (1..5); scale < 1 shrinks the fine grid, `ratio`
+    overrides the fine/coarse nesting ratio (small test grids need a finer coarse
+    grid to resolve the target balls)."""
     fn = CONFIGS[idx]
-    return fn(scale=scale) if seed is None else fn(seed=seed, scale=scale)
+    kw = dict(scale=scale, ratio=ratio)
+    if seed is not None:
+        kw["seed"] = seed
+    return fn(**kw)
 
 
 def random_field(problem: Problem, seed: int, lo=0.0, hi=1.0) -> np.ndarray:

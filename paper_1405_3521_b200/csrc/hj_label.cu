@@ -1,0 +1,296 @@
+// hj_label.cu — discrete optimal feedback, trajectory labelling of the coarse
+// nodes and prolongation of the labels to the fine grid with an overlap band
+// (north_star "reconstruction of independent sub-domains"; PAPER.md Definition
+// 2.2 line 150-152, Proposition 2.3, ISA steps 1-2 line 396-418;
+// readings R7, R8, R9).  Decisions are taken in fp64 whatever the V dtype.
+#include <algorithm>
+
+#include "hj_host.cuh"
+
+namespace hj {
+
+// min over controls of the Tdef bracket at index-space point g (fp64), lowest
+// index argmin, second-best gap.
+template <typename Ts, int DIM>
+__device__ double min_bracket(const DevProblem<double, Ts> &P, const Ts *__restrict__ V,
+                              const int64_t o[3], const int64_t vn[3], const double g[3],
+                              int *arg, double *margin) {
+    double x[3] = {0, 0, 0};
+#pragma unroll
+    for (int d = 0; d < DIM; ++d) x[d] = fma(g[d], P.dx[d], P.lo[d]);
+    double cs = 1.0;
+    if (P.speed && P.dyn == HJ_DYN_AFFINE)
+        cs = interp<double, Ts, DIM>(P.speed, o, vn, P.n, P.periodic, g, 1.0);
+    double base = (P.cost == HJ_COST_KRUZKOV) ? P.kcost : P.h * cost_state(P, x);
+    double best = INFINITY, second = INFINITY;
+    int a = -1;
+    for (int k = 0; k < P.K; ++k) {
+        double f[3];
+        dynamics(P, x, cs, k, f);
+        double foot[3] = {0, 0, 0};
+#pragma unroll
+        for (int d = 0; d < DIM; ++d) foot[d] = fma(P.hdx[d], f[d], g[d]);
+        double I = interp<double, Ts, DIM>(V, o, vn, P.n, P.periodic, foot, P.v_out);
+        double ck = (P.cost == HJ_COST_KRUZKOV) ? base : fma(P.h * P.lr, P.csq[k], base);
+        double v = fma(P.beta, I, ck);
+        if (v < best) {
+            second = best;
+            best = v;
+            a = k;
+        } else if (v < second) {
+            second = v;
+        }
+    }
+    *arg = a;
+    *margin = second - best;
+    return best;
+}
+
+template <typename Ts, int DIM>
+__global__ void k_feedback(const DevProblem<double, Ts> P, const Ts *__restrict__ V,
+                           const int8_t *__restrict__ piece, int64_t N, int32_t *astar,
+                           double *margin) {
+    const int64_t o[3] = {0, 0, 0};
+    const int64_t vn[3] = {P.n[0], P.n[1], P.n[2]};
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < N;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        if (piece[t] >= 0) {
+            astar[t] = -1;
+            if (margin) margin[t] = INFINITY;
+            continue;
+        }
+        double g[3] = {(double)(t % P.n[0]), (double)((t / P.n[0]) % P.n[1]),
+                       (double)(t / (P.n[0] * P.n[1]))};
+        int a;
+        double m;
+        min_bracket<Ts, DIM>(P, V, o, vn, g, &a, &m);
+        astar[t] = a;
+        if (margin) margin[t] = m;
+    }
+}
+
+// One thread follows the discrete optimal feedback trajectory of one coarse node.
+template <typename Ts, int DIM>
+__global__ void k_label(const DevProblem<double, Ts> P, const Ts *__restrict__ V,
+                        const int8_t *__restrict__ piece, int64_t N, int64_t n_max,
+                        int32_t *label, double *margin_out, double *geo_out, int32_t *steps_out) {
+    const int64_t o[3] = {0, 0, 0};
+    const int64_t vn[3] = {P.n[0], P.n[1], P.n[2]};
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < N;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        double g[3] = {(double)(t % P.n[0]), (double)((t / P.n[0]) % P.n[1]),
+                       (double)(t / (P.n[0] * P.n[1]))};
+        double mm = INFINITY, mg = INFINITY;
+        int lab = -1;
+        int64_t s = 0;
+        for (;; ++s) {
+            int64_t r[3] = {0, 0, 0};
+#pragma unroll
+            for (int d = 0; d < DIM; ++d) {
+                double q = g[d] + 0.5;
+                double fl = floor(q);
+                double dist = q - fl;
+                dist = fmin(dist, 1.0 - dist);
+                mg = fmin(mg, dist);
+                int64_t c = (int64_t)fl;
+                if (P.periodic[d]) {
+                    c %= P.n[d];
+                    if (c < 0) c += P.n[d];
+                } else if (c > P.n[d] - 1) {
+                    c = P.n[d] - 1;
+                }
+                r[d] = c;
+            }
+            int pc = piece[r[0] + P.n[0] * (r[1] + P.n[1] * r[2])];
+            if (pc >= 0) {
+                lab = pc;
+                break;
+            }
+            if (s >= n_max) break;
+            int a;
+            double margin;
+            min_bracket<Ts, DIM>(P, V, o, vn, g, &a, &margin);
+            mm = fmin(mm, margin);
+            double x[3] = {0, 0, 0};
+#pragma unroll
+            for (int d = 0; d < DIM; ++d) x[d] = fma(g[d], P.dx[d], P.lo[d]);
+            double cs = 1.0;
+            if (P.speed && P.dyn == HJ_DYN_AFFINE)
+                cs = interp<double, Ts, DIM>(P.speed, o, vn, P.n, P.periodic, g, 1.0);
+            double f[3];
+            dynamics(P, x, cs, a, f);
+            bool out = false;
+#pragma unroll
+            for (int d = 0; d < DIM; ++d) {
+                g[d] = fma(P.hdx[d], f[d], g[d]);
+                if (P.periodic[d]) {
+                    double n = (double)P.n[d];
+                    g[d] = g[d] - n * floor(g[d] / n);
+                } else {
+                    double hi = (double)(P.n[d] - 1);
+                    mg = fmin(mg, fmin(fabs(g[d]), fabs(hi - g[d])));
+                    if (g[d] < 0.0 || g[d] > hi) out = true;
+                }
+            }
+            if (out) {
+                ++s;
+                break;
+            }
+        }
+        label[t] = lab;
+        if (margin_out) margin_out[t] = mm;
+        if (geo_out) geo_out[t] = mg;
+        if (steps_out) steps_out[t] = (int32_t)s;
+    }
+}
+
+struct ProlongArgs {
+    int dim;
+    int64_t nc[3], nf[3], R[3];
+    int periodic[3];
+    int64_t band;
+    uint32_t all;
+};
+
+__device__ __forceinline__ int64_t floordiv(int64_t a, int64_t b) {
+    int64_t q = a / b;
+    return (a % b != 0 && ((a < 0) != (b < 0))) ? q - 1 : q;
+}
+
+__global__ void k_prolong(const ProlongArgs A, const int32_t *__restrict__ lab,
+                          const int8_t *__restrict__ fine_piece, int64_t Nf, uint32_t *mask) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < Nf;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        int64_t ii[3] = {t % A.nf[0], (t / A.nf[0]) % A.nf[1], t / (A.nf[0] * A.nf[1])};
+        int64_t lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
+        for (int d = 0; d < A.dim; ++d) {
+            int64_t reach = A.R[d] + A.band;
+            lo[d] = -floordiv(-(ii[d] - reach), A.R[d]);  // ceil
+            hi[d] = floordiv(ii[d] + reach, A.R[d]);
+        }
+        uint32_t bits = 0;
+        for (int64_t I2 = lo[2]; I2 <= hi[2]; ++I2)
+            for (int64_t I1 = lo[1]; I1 <= hi[1]; ++I1)
+                for (int64_t I0 = lo[0]; I0 <= hi[0]; ++I0) {
+                    int64_t I[3] = {I0, I1, I2}, J[3] = {0, 0, 0};
+                    bool ok = true;
+                    for (int d = 0; d < A.dim; ++d) {
+                        int64_t c = I[d];
+                        if (A.periodic[d]) {
+                            c %= A.nc[d];
+                            if (c < 0) c += A.nc[d];
+                        } else if (c < 0 || c > A.nc[d] - 1) {
+                            ok = false;
+                        }
+                        J[d] = c;
+                    }
+                    if (!ok) continue;
+                    int32_t l = lab[J[0] + A.nc[0] * (J[1] + A.nc[1] * J[2])];
+                    bits |= (l < 0) ? A.all : (1u << l);
+                }
+        int8_t p = fine_piece[t];
+        if (p >= 0) bits |= 1u << p;
+        mask[t] = bits & A.all;
+    }
+}
+
+template <typename Ts>
+static hj_status feedback_impl(const hj_grid &g, const hj_problem &p, const hj_fields &f,
+                               const Ts *V, int32_t *astar, double *margin, cudaStream_t s) {
+    auto P = make_dev_problem<double, Ts>(g, p, f);
+    int64_t N = grid_nodes(g);
+    int blocks = (int)std::min<int64_t>((N + 127) / 128, 148 * 16);
+    if (g.dim == 2)
+        k_feedback<Ts, 2><<<blocks, 128, 0, s>>>(P, V, f.piece, N, astar, margin);
+    else
+        k_feedback<Ts, 3><<<blocks, 128, 0, s>>>(P, V, f.piece, N, astar, margin);
+    HJ_CUDA(cudaGetLastError());
+    return HJ_OK;
+}
+
+template <typename Ts>
+static hj_status label_impl(const hj_grid &g, const hj_problem &p, const hj_fields &f,
+                            const Ts *V, int64_t n_max, int32_t *label, double *margin,
+                            double *geo, int32_t *steps, cudaStream_t s) {
+    auto P = make_dev_problem<double, Ts>(g, p, f);
+    int64_t N = grid_nodes(g);
+    int blocks = (int)std::min<int64_t>((N + 63) / 64, 148 * 32);
+    if (g.dim == 2)
+        k_label<Ts, 2><<<blocks, 64, 0, s>>>(P, V, f.piece, N, n_max, label, margin, geo, steps);
+    else
+        k_label<Ts, 3><<<blocks, 64, 0, s>>>(P, V, f.piece, N, n_max, label, margin, geo, steps);
+    HJ_CUDA(cudaGetLastError());
+    return HJ_OK;
+}
+
+}  // namespace hj
+
+using namespace hj;
+
+extern "C" {
+
+hj_status hj_coarse_feedback(const hj_grid *grid, const hj_problem *prob,
+                             const hj_fields *fields, int32_t dtype, const void *V,
+                             int32_t *astar, double *margin, void *stream) {
+    clear_error();
+    hj_status st;
+    if ((st = validate_grid(grid)) != HJ_OK) return st;
+    if ((st = validate_problem(grid, prob)) != HJ_OK) return st;
+    HJ_CHECK(fields && fields->piece, "fields.piece is required");
+    HJ_CHECK(V && astar, "V / astar is NULL");
+    HJ_CHECK(dtype == HJ_F32 || dtype == HJ_F64, "dtype must be HJ_F32 or HJ_F64");
+    cudaStream_t s = (cudaStream_t)stream;
+    if (dtype == HJ_F64)
+        return feedback_impl<double>(*grid, *prob, *fields, (const double *)V, astar, margin, s);
+    return feedback_impl<float>(*grid, *prob, *fields, (const float *)V, astar, margin, s);
+}
+
+hj_status hj_label_subdomains(const hj_grid *cg, const hj_problem *cp, const hj_fields *cf,
+                              int32_t dtype, const void *Vc, int64_t n_max, const hj_grid *fg,
+                              const int32_t ratio[3], int32_t band, int32_t m,
+                              const int8_t *fine_piece, int32_t *label, double *margin,
+                              double *geo, int32_t *steps, uint32_t *fine_mask, void *stream) {
+    clear_error();
+    hj_status st;
+    if ((st = validate_grid(cg)) != HJ_OK) return st;
+    if ((st = validate_grid(fg)) != HJ_OK) return st;
+    if ((st = validate_problem(cg, cp)) != HJ_OK) return st;
+    HJ_CHECK(cf && cf->piece, "coarse fields.piece is required");
+    HJ_CHECK(Vc && label && fine_mask && fine_piece && ratio, "NULL argument");
+    HJ_CHECK(m >= 1 && m <= HJ_MAX_SUBDOMAINS, "m must be in [1, %d]", HJ_MAX_SUBDOMAINS);
+    HJ_CHECK(band >= 0 && n_max >= 0, "band and n_max must be >= 0");
+    HJ_CHECK(cg->dim == fg->dim, "coarse and fine grids differ in dim");
+    HJ_CHECK(dtype == HJ_F32 || dtype == HJ_F64, "dtype must be HJ_F32 or HJ_F64");
+    for (int d = 0; d < cg->dim; ++d) {
+        HJ_CHECK(ratio[d] >= 1, "ratio[%d] must be >= 1", d);
+        HJ_CHECK(cg->periodic[d] == fg->periodic[d], "periodicity differs on axis %d", d);
+        if (fg->periodic[d])
+            HJ_CHECK(fg->n[d] == ratio[d] * cg->n[d], "periodic axis %d not nested", d);
+        else
+            HJ_CHECK(fg->n[d] - 1 == ratio[d] * (cg->n[d] - 1), "axis %d not nested", d);
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    st = dtype == HJ_F64 ? label_impl<double>(*cg, *cp, *cf, (const double *)Vc, n_max, label,
+                                              margin, geo, steps, s)
+                         : label_impl<float>(*cg, *cp, *cf, (const float *)Vc, n_max, label,
+                                             margin, geo, steps, s);
+    if (st != HJ_OK) return st;
+    ProlongArgs A;
+    memset(&A, 0, sizeof(A));
+    A.dim = fg->dim;
+    for (int d = 0; d < 3; ++d) {
+        A.nc[d] = d < cg->dim ? cg->n[d] : 1;
+        A.nf[d] = d < fg->dim ? fg->n[d] : 1;
+        A.R[d] = d < fg->dim ? ratio[d] : 1;
+        A.periodic[d] = d < fg->dim ? fg->periodic[d] : 0;
+    }
+    A.band = band;
+    A.all = m >= 32 ? 0xffffffffu : ((1u << m) - 1u);
+    int64_t Nf = grid_nodes(*fg);
+    int blocks = (int)std::min<int64_t>((Nf + 255) / 256, 148 * 16);
+    k_prolong<<<blocks, 256, 0, s>>>(A, label, fine_piece, Nf, fine_mask);
+    HJ_CUDA(cudaGetLastError());
+    return HJ_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,562 @@
+// hj_solve.cu — the value-iteration sweep of the SL Bellman operator
+// (PAPER.md eq. (SL), (Tdef) line 238-245), the device-side stopping
+// rule (line 341-345, reading R6) and the ISA fine stage (steps 3-4, line 400-407).
+#include <algorithm>
+#include <deque>
+#include <vector>
+
+#include "hj_host.cuh"
+#include "hj_sweep.cuh"
+
+namespace hj {
+
+// ---------------------------------------------------------------------------
+// small kernels
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void k_init_view(const SweepView<T> *views, T v_out, const T *g, const int64_t n0,
+                            const int64_t n1) {
+    const SweepView<T> &vw = views[blockIdx.y];
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < vw.nodes;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        int8_t c = vw.cls[t];
+        T v = v_out;
+        if (c >= 0) {
+            if (g) {
+                int64_t li = t % vw.vn[0], r = t / vw.vn[0];
+                int64_t lj = r % vw.vn[1], lk = r / vw.vn[1];
+                int64_t gi = (li + vw.o[0]) + n0 * ((lj + vw.o[1]) + n1 * (lk + vw.o[2]));
+                v = g[gi];
+            } else {
+                v = T(0);
+            }
+        }
+        vw.V[0][t] = v;
+        vw.V[1][t] = v;
+    }
+}
+
+template <typename T>
+__global__ void k_count_interior(const SweepView<T> *views, unsigned long long *counts) {
+    const SweepView<T> &vw = views[blockIdx.y];
+    unsigned long long c = 0;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < vw.nodes;
+         t += (int64_t)gridDim.x * blockDim.x)
+        c += (vw.cls[t] == -1);
+    for (int s = 16; s > 0; s >>= 1) c += __shfl_down_sync(0xffffffffu, c, s);
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(&counts[blockIdx.y], c);
+}
+
+// class array of sub-domain k over its box: piece inside S_k, -2 (ghost) outside
+__global__ void k_subdomain_classes(const uint32_t *__restrict__ mask,
+                                    const int8_t *__restrict__ piece, int k, int64_t o0,
+                                    int64_t o1, int64_t o2, int64_t vn0, int64_t vn1,
+                                    int64_t nodes, int64_t n0, int64_t n1, int8_t *cls) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nodes;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        int64_t li = t % vn0, r = t / vn0;
+        int64_t lj = r % vn1, lk = r / vn1;
+        int64_t gi = (li + o0) + n0 * ((lj + o1) + n1 * (lk + o2));
+        cls[t] = ((mask[gi] >> k) & 1u) ? piece[gi] : (int8_t)-2;
+    }
+}
+
+template <typename T>
+struct AsmView {
+    int64_t o[3], vn[3];
+    const T *V;
+    int32_t sub;
+};
+
+template <typename T>
+__global__ void k_assemble(const AsmView<T> *__restrict__ av, int nv,
+                           const uint32_t *__restrict__ mask, int64_t n0, int64_t n1,
+                           int64_t N, T v_out, T *Vbar) {
+    for (int64_t gi = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; gi < N;
+         gi += (int64_t)gridDim.x * blockDim.x) {
+        uint32_t bits = mask[gi];
+        int64_t i = gi % n0, r = gi / n0;
+        int64_t j = r % n1, k = r / n1;
+        T v = v_out;
+        for (int q = 0; q < nv; ++q) {
+            const AsmView<T> &a = av[q];
+            if (!((bits >> a.sub) & 1u)) continue;
+            int64_t li = i - a.o[0], lj = j - a.o[1], lk = k - a.o[2];
+            if (li < 0 || lj < 0 || lk < 0 || li >= a.vn[0] || lj >= a.vn[1] || lk >= a.vn[2])
+                continue;
+            T x = a.V[li + a.vn[0] * (lj + a.vn[1] * lk)];
+            v = x < v ? x : v;
+        }
+        Vbar[gi] = v;
+    }
+}
+
+__global__ void k_plan(const uint32_t *__restrict__ mask, int64_t N, int64_t n0, int64_t n1,
+                       int m, int *bb /* [m][6]: lo0..2, hi0..2 */,
+                       unsigned long long *cnt) {
+    __shared__ int s_lo[HJ_MAX_SUBDOMAINS][3], s_hi[HJ_MAX_SUBDOMAINS][3];
+    __shared__ unsigned long long s_cnt[HJ_MAX_SUBDOMAINS];
+    for (int t = threadIdx.x; t < HJ_MAX_SUBDOMAINS; t += blockDim.x) {
+        for (int d = 0; d < 3; ++d) {
+            s_lo[t][d] = 0x7fffffff;
+            s_hi[t][d] = -1;
+        }
+        s_cnt[t] = 0;
+    }
+    __syncthreads();
+    for (int64_t gi = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; gi < N;
+         gi += (int64_t)gridDim.x * blockDim.x) {
+        uint32_t bits = mask[gi];
+        if (!bits) continue;
+        int c[3];
+        c[0] = (int)(gi % n0);
+        int64_t r = gi / n0;
+        c[1] = (int)(r % n1);
+        c[2] = (int)(r / n1);
+        while (bits) {
+            int k = __ffs(bits) - 1;
+            bits &= bits - 1;
+            if (k >= m) break;
+            for (int d = 0; d < 3; ++d) {
+                atomicMin(&s_lo[k][d], c[d]);
+                atomicMax(&s_hi[k][d], c[d]);
+            }
+            atomicAdd(&s_cnt[k], 1ull);
+        }
+    }
+    __syncthreads();
+    for (int k = threadIdx.x; k < m; k += blockDim.x) {
+        if (!s_cnt[k]) continue;
+        for (int d = 0; d < 3; ++d) {
+            atomicMin(&bb[6 * k + d], s_lo[k][d]);
+            atomicMax(&bb[6 * k + 3 + d], s_hi[k][d]);
+        }
+        atomicAdd(&cnt[k], s_cnt[k]);
+    }
+}
+
+__global__ void k_fill_int(int *p, int n, int v_lo, int v_hi) {
+    int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < n) p[t] = ((t % 6) < 3) ? v_lo : v_hi;
+}
+
+// ---------------------------------------------------------------------------
+// the iteration driver: sweeps in batches, residuals read back one batch
+// behind so the device never waits for the host; every view stops at its own
+// first n with res[n] < tol (the sweep kernel itself skips converged views).
+// ---------------------------------------------------------------------------
+struct IterResult {
+    std::vector<int64_t> iters;
+    std::vector<double> resid;
+    std::vector<int> converged;
+    float ms = 0.f;
+    int64_t launches = 0;
+};
+
+template <typename T>
+static hj_status iterate(const hj_grid &grid, const hj_problem &prob, const DevProblem<T, T> &P,
+                         SweepView<T> *d_views, const std::vector<SweepView<T>> &h_views,
+                         double *res_base, int64_t res_stride, double tol, int64_t max_iter,
+                         cudaStream_t s, IterResult &out) {
+    const int nv = (int)h_views.size();
+    const int B = 16;
+    double *pin = pinned_scratch((size_t)2 * nv * B);
+    HJ_CHECK(pin != nullptr, "cudaMallocHost failed for the residual staging buffer");
+    cudaEvent_t ev[2], t0, t1;
+    for (auto &e : ev) HJ_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    HJ_CUDA(cudaEventCreate(&t0));
+    HJ_CUDA(cudaEventCreate(&t1));
+    out.iters.assign(nv, max_iter);
+    out.resid.assign(nv, INFINITY);
+    out.converged.assign(nv, 0);
+    int n_done = 0;
+
+    SweepLaunch<T> L;
+    if (sweep_prepare(grid, prob, h_views, L) != HJ_OK) return HJ_ERR_INVALID;
+
+    struct Batch {
+        int64_t start, count;
+        int slot;
+    };
+    std::deque<Batch> inflight;
+    int64_t next = 0;
+    int slot = 0;
+    HJ_CUDA(cudaEventRecord(t0, s));
+    while (true) {
+        while (inflight.size() < 2 && next < max_iter && n_done < nv) {
+            int64_t cnt = std::min<int64_t>(B, max_iter - next);
+            for (int64_t it = next; it < next + cnt; ++it) {
+                hj_status st = sweep_launch(P, d_views, L, it, tol, s);
+                if (st != HJ_OK) return st;
+                ++out.launches;
+            }
+            for (int v = 0; v < nv; ++v)
+                HJ_CUDA(cudaMemcpyAsync(pin + ((size_t)slot * nv + v) * B,
+                                        res_base + v * res_stride + next, cnt * sizeof(double),
+                                        cudaMemcpyDeviceToHost, s));
+            HJ_CUDA(cudaEventRecord(ev[slot], s));
+            inflight.push_back({next, cnt, slot});
+            next += cnt;
+            slot ^= 1;
+        }
+        if (inflight.empty()) break;
+        Batch b = inflight.front();
+        inflight.pop_front();
+        HJ_CUDA(cudaEventSynchronize(ev[b.slot]));
+        for (int v = 0; v < nv; ++v) {
+            if (out.converged[v]) continue;
+            for (int64_t i = 0; i < b.count; ++i) {
+                double r = pin[((size_t)b.slot * nv + v) * B + i];
+                out.resid[v] = r;
+                if (r < tol) {
+                    out.converged[v] = 1;
+                    out.iters[v] = b.start + i + 1;
+                    ++n_done;
+                    break;
+                }
+            }
+        }
+        if (n_done == nv) break;
+    }
+    HJ_CUDA(cudaEventRecord(t1, s));
+    HJ_CUDA(cudaStreamSynchronize(s));
+    HJ_CUDA(cudaGetLastError());
+    HJ_CUDA(cudaEventElapsedTime(&out.ms, t0, t1));
+    for (auto &e : ev) cudaEventDestroy(e);
+    cudaEventDestroy(t0);
+    cudaEventDestroy(t1);
+    sweep_release(L);
+    return HJ_OK;
+}
+
+static hj_status validate_fields(const hj_fields *f) {
+    HJ_CHECK(f != nullptr, "fields is NULL");
+    HJ_CHECK(f->piece != nullptr, "fields.piece is required");
+    return HJ_OK;
+}
+
+// ---------------------------------------------------------------------------
+// hj_solve
+// ---------------------------------------------------------------------------
+template <typename T>
+static size_t solve_ws(int64_t N, int64_t max_iter) {
+    Carver c(nullptr, 0);
+    c.take(N * sizeof(T));
+    c.take(max_iter * sizeof(double));
+    c.take(sizeof(SweepView<T>));
+    c.take(64);
+    return c.off;
+}
+
+template <typename T>
+static hj_status solve_impl(const hj_grid &grid, const hj_problem &prob, const hj_fields &f,
+                            T *V, double tol, int64_t max_iter, void *ws, size_t ws_bytes,
+                            cudaStream_t s, hj_report *rep) {
+    int64_t N = grid_nodes(grid);
+    Carver c(ws, ws_bytes);
+    T *V1 = (T *)c.take(N * sizeof(T));
+    double *res = (double *)c.take(max_iter * sizeof(double));
+    SweepView<T> *d_view = (SweepView<T> *)c.take(sizeof(SweepView<T>));
+    unsigned long long *cnt = (unsigned long long *)c.take(64);
+    if (!c.ok()) {
+        set_error("workspace too small: need %zu bytes, got %zu", c.off, ws_bytes);
+        return HJ_ERR_WORKSPACE;
+    }
+    SweepView<T> hv;
+    memset(&hv, 0, sizeof(hv));
+    for (int d = 0; d < 3; ++d) {
+        hv.o[d] = 0;
+        hv.vn[d] = d < grid.dim ? grid.n[d] : 1;
+    }
+    hv.nodes = N;
+    hv.V[0] = V;
+    hv.V[1] = V1;
+    hv.cls = f.piece;
+    hv.res = res;
+    auto P = make_dev_problem<T, T>(grid, prob, f);
+    HJ_CUDA(cudaMemsetAsync(res, 0, max_iter * sizeof(double), s));
+    HJ_CUDA(cudaMemsetAsync(cnt, 0, 64, s));
+    HJ_CUDA(cudaMemcpyAsync(d_view, &hv, sizeof(hv), cudaMemcpyHostToDevice, s));
+    int blocks = (int)std::min<int64_t>((N + 255) / 256, 148 * 16);
+    k_init_view<T><<<dim3(blocks, 1), 256, 0, s>>>(d_view, (T)prob.v_out, (const T *)f.g,
+                                                   hv.vn[0], hv.vn[1]);
+    k_count_interior<T><<<dim3(blocks, 1), 256, 0, s>>>(d_view, cnt);
+    HJ_CUDA(cudaGetLastError());
+    IterResult r;
+    std::vector<SweepView<T>> hvs{hv};
+    hj_status st = iterate<T>(grid, prob, P, d_view, hvs, res, 0, tol, max_iter, s, r);
+    if (st != HJ_OK) return st;
+    int64_t it = r.iters[0];
+    if (it & 1) HJ_CUDA(cudaMemcpyAsync(V, V1, N * sizeof(T), cudaMemcpyDeviceToDevice, s));
+    unsigned long long interior = 0;
+    HJ_CUDA(cudaMemcpyAsync(&interior, cnt, sizeof(interior), cudaMemcpyDeviceToHost, s));
+    HJ_CUDA(cudaStreamSynchronize(s));
+    if (rep) {
+        rep->iterations = it;
+        rep->residual = r.resid[0];
+        rep->converged = r.converged[0];
+        rep->node_updates = (int64_t)interior * prob.n_controls * it;
+        rep->device_ms = r.ms;
+        rep->launches = r.launches + 2;
+    }
+    if (!r.converged[0]) {
+        set_error("not converged after %lld iterations (residual %g)", (long long)it, r.resid[0]);
+        return HJ_ERR_NOT_CONVERGED;
+    }
+    return HJ_OK;
+}
+
+// ---------------------------------------------------------------------------
+// partitioned solve (ISA steps 3-4)
+// ---------------------------------------------------------------------------
+struct PartLayout {
+    std::vector<size_t> off_v0, off_v1, off_cls;
+    size_t off_res, off_views, off_asm, off_cnt, total;
+};
+
+template <typename T>
+static PartLayout part_layout(int m, const hj_subdomain *plan, int64_t max_iter) {
+    PartLayout L;
+    Carver c(nullptr, 0);
+    for (int k = 0; k < m; ++k) {
+        int64_t bn = plan[k].n_nodes > 0 ? plan[k].box_nodes : 0;
+        L.off_v0.push_back(c.off);
+        c.take(bn * sizeof(T));
+        L.off_v1.push_back(c.off);
+        c.take(bn * sizeof(T));
+        L.off_cls.push_back(c.off);
+        c.take(bn);
+    }
+    L.off_res = c.off;
+    c.take((size_t)m * max_iter * sizeof(double));
+    L.off_views = c.off;
+    c.take((size_t)m * sizeof(SweepView<T>));
+    L.off_asm = c.off;
+    c.take((size_t)m * sizeof(AsmView<T>));
+    L.off_cnt = c.off;
+    c.take((size_t)m * sizeof(unsigned long long));
+    L.total = c.off;
+    return L;
+}
+
+template <typename T>
+static hj_status partitioned_impl(const hj_grid &grid, const hj_problem &prob,
+                                  const hj_fields &f, const uint32_t *mask, int m,
+                                  const hj_subdomain *plan, uint32_t solve_set, double tol,
+                                  int64_t max_iter, T *Vbar, void *ws, size_t ws_bytes,
+                                  cudaStream_t s, hj_report *reps) {
+    PartLayout L = part_layout<T>(m, plan, max_iter);
+    if (ws_bytes < L.total) {
+        set_error("workspace too small: need %zu bytes, got %zu", L.total, ws_bytes);
+        return HJ_ERR_WORKSPACE;
+    }
+    char *base = (char *)ws;
+    int64_t n0 = grid.n[0], n1 = grid.dim > 1 ? grid.n[1] : 1;
+    int64_t N = grid_nodes(grid);
+    double *res = (double *)(base + L.off_res);
+    SweepView<T> *d_views = (SweepView<T> *)(base + L.off_views);
+    AsmView<T> *d_asm = (AsmView<T> *)(base + L.off_asm);
+    unsigned long long *cnt = (unsigned long long *)(base + L.off_cnt);
+
+    std::vector<SweepView<T>> hv;
+    std::vector<int> subs;
+    int64_t max_nodes = 1;
+    for (int k = 0; k < m; ++k) {
+        if (!((solve_set >> k) & 1u) || plan[k].n_nodes == 0) continue;
+        SweepView<T> v;
+        memset(&v, 0, sizeof(v));
+        v.nodes = 1;
+        for (int d = 0; d < 3; ++d) {
+            v.o[d] = d < grid.dim ? plan[k].lo[d] : 0;
+            v.vn[d] = d < grid.dim ? plan[k].hi[d] - plan[k].lo[d] + 1 : 1;
+            v.nodes *= v.vn[d];
+        }
+        if (v.nodes != plan[k].box_nodes) {
+            set_error("plan[%d] inconsistent: box_nodes %lld vs box %lld", k,
+                      (long long)plan[k].box_nodes, (long long)v.nodes);
+            return HJ_ERR_INVALID;
+        }
+        v.V[0] = (T *)(base + L.off_v0[k]);
+        v.V[1] = (T *)(base + L.off_v1[k]);
+        v.cls = (const int8_t *)(base + L.off_cls[k]);
+        v.res = res + (size_t)hv.size() * max_iter;
+        int blocks = (int)std::min<int64_t>((v.nodes + 255) / 256, 148 * 16);
+        k_subdomain_classes<<<blocks, 256, 0, s>>>(mask, f.piece, k, v.o[0], v.o[1], v.o[2],
+                                                   v.vn[0], v.vn[1], v.nodes, n0, n1,
+                                                   (int8_t *)v.cls);
+        max_nodes = std::max(max_nodes, v.nodes);
+        hv.push_back(v);
+        subs.push_back(k);
+    }
+    int nv = (int)hv.size();
+    int gblocks = (int)std::min<int64_t>((N + 255) / 256, 148 * 16);
+    if (nv == 0) {
+        std::vector<AsmView<T>> none;
+        k_assemble<T><<<gblocks, 256, 0, s>>>(d_asm, 0, mask, n0, n1, N, (T)prob.v_out, Vbar);
+        HJ_CUDA(cudaGetLastError());
+        HJ_CUDA(cudaStreamSynchronize(s));
+        return HJ_OK;
+    }
+    HJ_CUDA(cudaMemsetAsync(res, 0, (size_t)nv * max_iter * sizeof(double), s));
+    HJ_CUDA(cudaMemsetAsync(cnt, 0, (size_t)m * sizeof(unsigned long long), s));
+    HJ_CUDA(cudaMemcpyAsync(d_views, hv.data(), nv * sizeof(SweepView<T>),
+                            cudaMemcpyHostToDevice, s));
+    int blocks = (int)std::min<int64_t>((max_nodes + 255) / 256, 148 * 16);
+    auto P = make_dev_problem<T, T>(grid, prob, f);
+    k_init_view<T><<<dim3(blocks, nv), 256, 0, s>>>(d_views, (T)prob.v_out, (const T *)f.g, n0,
+                                                    n1);
+    k_count_interior<T><<<dim3(blocks, nv), 256, 0, s>>>(d_views, cnt);
+    HJ_CUDA(cudaGetLastError());
+    IterResult r;
+    hj_status st = iterate<T>(grid, prob, P, d_views, hv, res, max_iter, tol, max_iter, s, r);
+    if (st != HJ_OK) return st;
+    std::vector<AsmView<T>> ha(nv);
+    for (int q = 0; q < nv; ++q) {
+        for (int d = 0; d < 3; ++d) {
+            ha[q].o[d] = hv[q].o[d];
+            ha[q].vn[d] = hv[q].vn[d];
+        }
+        ha[q].V = hv[q].V[r.iters[q] & 1];
+        ha[q].sub = subs[q];
+    }
+    HJ_CUDA(cudaMemcpyAsync(d_asm, ha.data(), nv * sizeof(AsmView<T>), cudaMemcpyHostToDevice, s));
+    k_assemble<T><<<gblocks, 256, 0, s>>>(d_asm, nv, mask, n0, n1, N, (T)prob.v_out, Vbar);
+    HJ_CUDA(cudaGetLastError());
+    std::vector<unsigned long long> interior(m, 0);
+    HJ_CUDA(cudaMemcpyAsync(interior.data(), cnt, nv * sizeof(unsigned long long),
+                            cudaMemcpyDeviceToHost, s));
+    HJ_CUDA(cudaStreamSynchronize(s));
+    bool all = true;
+    for (int q = 0; q < nv; ++q) {
+        all = all && r.converged[q];
+        if (reps) {
+            hj_report &rp = reps[subs[q]];
+            rp.iterations = r.iters[q];
+            rp.residual = r.resid[q];
+            rp.converged = r.converged[q];
+            rp.node_updates = (int64_t)interior[q] * prob.n_controls * r.iters[q];
+            rp.device_ms = r.ms;
+            rp.launches = q == 0 ? r.launches + nv + 3 : 0;  // shared launches, counted once
+        }
+    }
+    if (!all) {
+        set_error("a sub-domain did not converge within %lld iterations", (long long)max_iter);
+        return HJ_ERR_NOT_CONVERGED;
+    }
+    return HJ_OK;
+}
+
+}  // namespace hj
+
+using namespace hj;
+
+extern "C" {
+
+size_t hj_solve_workspace_bytes(const hj_grid *grid, int32_t dtype, int64_t max_iter) {
+    if (!grid || validate_grid(grid) != HJ_OK || max_iter < 1) return 0;
+    int64_t N = grid_nodes(*grid);
+    return dtype == HJ_F64 ? solve_ws<double>(N, max_iter) : solve_ws<float>(N, max_iter);
+}
+
+hj_status hj_solve(const hj_grid *grid, const hj_problem *prob, const hj_fields *fields,
+                   int32_t dtype, void *V, double tol, int64_t max_iter, void *workspace,
+                   size_t ws_bytes, void *stream, hj_report *report) {
+    clear_error();
+    hj_status st;
+    if ((st = validate_grid(grid)) != HJ_OK) return st;
+    if ((st = validate_problem(grid, prob)) != HJ_OK) return st;
+    if ((st = validate_fields(fields)) != HJ_OK) return st;
+    HJ_CHECK(V != nullptr && workspace != nullptr, "V / workspace is NULL");
+    HJ_CHECK(max_iter >= 1, "max_iter must be >= 1");
+    HJ_CHECK(tol > 0, "tol must be > 0");
+    HJ_CHECK(dtype == HJ_F32 || dtype == HJ_F64, "dtype must be HJ_F32 or HJ_F64");
+    cudaStream_t s = (cudaStream_t)stream;
+    if (dtype == HJ_F64)
+        return solve_impl<double>(*grid, *prob, *fields, (double *)V, tol, max_iter, workspace,
+                                  ws_bytes, s, report);
+    return solve_impl<float>(*grid, *prob, *fields, (float *)V, tol, max_iter, workspace,
+                             ws_bytes, s, report);
+}
+
+hj_status hj_partition_plan(const hj_grid *grid, const uint32_t *fine_mask, int32_t m,
+                            int32_t dtype, int64_t max_iter, hj_subdomain *plan,
+                            size_t *ws_bytes, void *stream) {
+    clear_error();
+    hj_status st;
+    if ((st = validate_grid(grid)) != HJ_OK) return st;
+    HJ_CHECK(m >= 1 && m <= HJ_MAX_SUBDOMAINS, "m must be in [1, %d]", HJ_MAX_SUBDOMAINS);
+    HJ_CHECK(fine_mask && plan && ws_bytes, "NULL argument");
+    HJ_CHECK(max_iter >= 1, "max_iter must be >= 1");
+    cudaStream_t s = (cudaStream_t)stream;
+    int64_t N = grid_nodes(*grid);
+    int *d_bb;
+    unsigned long long *d_cnt;
+    HJ_CUDA(cudaMallocAsync(&d_bb, sizeof(int) * 6 * HJ_MAX_SUBDOMAINS, s));
+    HJ_CUDA(cudaMallocAsync(&d_cnt, sizeof(unsigned long long) * HJ_MAX_SUBDOMAINS, s));
+    k_fill_int<<<1, 6 * HJ_MAX_SUBDOMAINS, 0, s>>>(d_bb, 6 * HJ_MAX_SUBDOMAINS, 0x7fffffff, -1);
+    HJ_CUDA(cudaMemsetAsync(d_cnt, 0, sizeof(unsigned long long) * HJ_MAX_SUBDOMAINS, s));
+    int blocks = (int)std::min<int64_t>((N + 255) / 256, 148 * 8);
+    int64_t n0 = grid->n[0], n1 = grid->dim > 1 ? grid->n[1] : 1;
+    k_plan<<<blocks, 256, 0, s>>>(fine_mask, N, n0, n1, m, d_bb, d_cnt);
+    int hbb[6 * HJ_MAX_SUBDOMAINS];
+    unsigned long long hcnt[HJ_MAX_SUBDOMAINS];
+    HJ_CUDA(cudaMemcpyAsync(hbb, d_bb, sizeof(hbb), cudaMemcpyDeviceToHost, s));
+    HJ_CUDA(cudaMemcpyAsync(hcnt, d_cnt, sizeof(hcnt), cudaMemcpyDeviceToHost, s));
+    HJ_CUDA(cudaFreeAsync(d_bb, s));
+    HJ_CUDA(cudaFreeAsync(d_cnt, s));
+    HJ_CUDA(cudaStreamSynchronize(s));
+    HJ_CUDA(cudaGetLastError());
+    for (int k = 0; k < m; ++k) {
+        hj_subdomain &p = plan[k];
+        memset(&p, 0, sizeof(p));
+        p.n_nodes = (int64_t)hcnt[k];
+        if (!p.n_nodes) continue;
+        p.box_nodes = 1;
+        int64_t extent = 1;
+        for (int d = 0; d < 3; ++d) {
+            if (d >= grid->dim) {
+                p.lo[d] = p.hi[d] = 0;
+                continue;
+            }
+            if (grid->periodic[d]) {
+                p.lo[d] = 0;
+                p.hi[d] = grid->n[d] - 1;
+            } else {
+                p.lo[d] = hbb[6 * k + d];
+                p.hi[d] = hbb[6 * k + 3 + d];
+            }
+            p.box_nodes *= p.hi[d] - p.lo[d] + 1;
+            extent = std::max<int64_t>(extent, p.hi[d] - p.lo[d] + 1);
+        }
+        // sweeps scale with the extent, work per sweep with the nodes
+        p.work = (double)p.n_nodes * (double)extent;
+    }
+    *ws_bytes = dtype == HJ_F64 ? part_layout<double>(m, plan, max_iter).total
+                                : part_layout<float>(m, plan, max_iter).total;
+    return HJ_OK;
+}
+
+hj_status hj_solve_partitioned(const hj_grid *grid, const hj_problem *prob,
+                               const hj_fields *fields, int32_t dtype, const uint32_t *fine_mask,
+                               int32_t m, const hj_subdomain *plan, uint32_t solve_set, double tol,
+                               int64_t max_iter, void *Vbar, void *workspace, size_t ws_bytes,
+                               void *stream, hj_report *reports) {
+    clear_error();
+    hj_status st;
+    if ((st = validate_grid(grid)) != HJ_OK) return st;
+    if ((st = validate_problem(grid, prob)) != HJ_OK) return st;
+    if ((st = validate_fields(fields)) != HJ_OK) return st;
+    HJ_CHECK(m >= 1 && m <= HJ_MAX_SUBDOMAINS, "m must be in [1, %d]", HJ_MAX_SUBDOMAINS);
+    HJ_CHECK(fine_mask && plan && Vbar && workspace, "NULL argument");
+    HJ_CHECK(max_iter >= 1 && tol > 0, "need max_iter >= 1 and tol > 0");
+    HJ_CHECK(dtype == HJ_F32 || dtype == HJ_F64, "dtype must be HJ_F32 or HJ_F64");
+    cudaStream_t s = (cudaStream_t)stream;
+    if (dtype == HJ_F64)
+        return partitioned_impl<double>(*grid, *prob, *fields, fine_mask, m, plan, solve_set,
+                                        tol, max_iter, (double *)Vbar, workspace, ws_bytes, s,
+                                        reports);
+    return partitioned_impl<float>(*grid, *prob, *fields, fine_mask, m, plan, solve_set, tol,
+                                   max_iter, (float *)Vbar, workspace, ws_bytes, s, reports);
+}
+
+}  // extern "C"

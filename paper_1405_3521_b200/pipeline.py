@@ -1,0 +1,54 @@
+"""The whole hot path as one call: coarse pre-solve -> coarse feedback labels ->
+prolongation -> partitioned fine solves -> min assembly (§4 ISA, with the
+north_star's trajectory labelling), optionally sharded over ranks.
+
+Every step is a libhj.so entry point; this module only sequences them and, for
+N > 1 ranks, does the one collective the method has: the final element-wise MIN
+of the ranks' assembled fields (NCCL through torch.distributed).
+"""
+from __future__ import annotations
+
+import time
+
+import torch
+
+from . import hj
+
+
+def solve_set_for_rank(owners, rank):
+    bits = 0
+    for k, r in enumerate(owners):
+        if r == rank:
+            bits |= 1 << k
+    return bits
+
+
+def run_isa(cfg, dtype="f32", device="cuda", rank=0, world=1, group=None, fine=None, coarse=None,
+            gather=True):
+    """Returns dict(V=assembled fine field (on every rank after the MIN all-reduce when
+    gather), labels, mask, plan, owners, reports, timings)."""
+    t = {}
+    fine = fine or hj.DeviceProblem(cfg.fine, dtype, device)
+    coarse = coarse or hj.DeviceProblem(cfg.coarse, dtype, device)
+    s = torch.cuda.current_stream()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+    ev[0].record(s)
+    Vc, rep_c = hj.hj_solve(coarse)
+    ev[1].record(s)
+    lab = hj.hj_label_subdomains(coarse, Vc, cfg.n_max_steps, fine, cfg.ratio, cfg.band, cfg.m)
+    ev[2].record(s)
+    plan, ws = hj.hj_partition_plan(fine, lab["mask"], cfg.m)
+    owners = hj.hj_assign_subdomains(plan, world)
+    solve_set = solve_set_for_rank(owners, rank)
+    Vbar, reps = hj.hj_solve_partitioned(fine, lab["mask"], cfg.m, plan, ws, solve_set=solve_set)
+    ev[3].record(s)
+    if world > 1 and gather:
+        torch.distributed.all_reduce(Vbar, op=torch.distributed.ReduceOp.MIN, group=group)
+    ev[4].record(s)
+    torch.cuda.synchronize()
+    t["coarse_ms"] = ev[0].elapsed_time(ev[1])
+    t["label_ms"] = ev[1].elapsed_time(ev[2])
+    t["fine_ms"] = ev[2].elapsed_time(ev[3])
+    t["gather_ms"] = ev[3].elapsed_time(ev[4])
+    return dict(V=Vbar, Vc=Vc, coarse_report=rep_c, labels=lab, mask=lab["mask"], plan=plan,
+                owners=owners, solve_set=solve_set, reports=reps, timings=t)
