@@ -23,6 +23,11 @@
 #define OR_COST_KRUZKOV 0
 #define OR_COST_DISCOUNTED 1
 
+/* Reading R3: a foot is outside the closed box when it lies more than OR_BOX_EPS
+ * cells beyond it; feet within OR_BOX_EPS are clamped onto the boundary (feet whose
+ * offset is zero in exact arithmetic, e.g. cos(pi/2), stay inside in any precision). */
+#define OR_BOX_EPS 1e-6
+
 #define OR_INTERIOR 0
 #define OR_TARGET 1
 #define OR_GHOST 2
@@ -93,7 +98,9 @@ double or_interp_field(const or_problem *p, const double *F, const double gi[3],
             i0[d] = c;
             i1[d] = (c + 1) % n;
         } else {
-            if (g < 0.0 || g > (double)(n - 1)) return outside_value;
+            if (g < -OR_BOX_EPS || g > (double)(n - 1) + OR_BOX_EPS) return outside_value;
+            if (g < 0.0) g = 0.0;
+            if (g > (double)(n - 1)) g = (double)(n - 1);
             long c = (long)floor(g);
             if (c > n - 2) c = n - 2;
             w[d] = g - (double)c;

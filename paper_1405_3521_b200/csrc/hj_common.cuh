@@ -60,30 +60,44 @@ __device__ __forceinline__ Ts view_fetch(const Ts *__restrict__ V, const int64_t
     return V[li + vn[0] * (lj + vn[1] * lk)];
 }
 
-// Multilinear interpolation I[V] at index-space point g (R4); v_out outside the
-// closed box on a non-periodic axis (R3).
+// Reading R3: feet more than BOX_EPS cells outside the closed box read v_out;
+// feet within BOX_EPS are clamped onto it (offsets that are zero in exact
+// arithmetic, e.g. cos(pi/2), then decide the same way in fp32 and fp64).
+constexpr double BOX_EPS = 1e-6;
+
+// Multilinear interpolation I[V] at the point base + delta (index space, R4).
+// The foot is kept as (integer node, small offset) so that the cell weights keep
+// full precision on large grids in fp32; v_out outside the box (R3).
 template <typename Tc, typename Ts, int DIM>
 __device__ __forceinline__ Tc interp(const Ts *__restrict__ V, const int64_t o[3],
                                      const int64_t vn[3], const int64_t n[3],
-                                     const int periodic[3], const Tc g[3], Tc v_out) {
+                                     const int periodic[3], const int64_t base[3],
+                                     const Tc delta[3], Tc v_out) {
     int64_t c0[3] = {0, 0, 0}, c1[3] = {0, 0, 0};
     Tc w[3] = {0, 0, 0};
 #pragma unroll
     for (int d = 0; d < DIM; ++d) {
-        Tc x = g[d];
-        int64_t nd = n[d];
+        Tc x = delta[d];
+        int64_t nd = n[d], b = base[d];
         if (periodic[d]) {
             Tc f = floor(x);
             w[d] = x - f;
-            int64_t c = ((int64_t)f) % nd;
+            int64_t c = (b + (int64_t)f) % nd;
             if (c < 0) c += nd;
             c0[d] = c;
             c1[d] = (c + 1 == nd) ? 0 : c + 1;
         } else {
-            if (!(x >= Tc(0) && x <= (Tc)(nd - 1))) return v_out;
-            int64_t c = (int64_t)floor(x);
-            if (c > nd - 2) c = nd - 2;
-            w[d] = x - (Tc)c;
+            const Tc lo = -(Tc)b, hi = (Tc)(nd - 1 - b);
+            if (!(x >= lo - (Tc)BOX_EPS && x <= hi + (Tc)BOX_EPS)) return v_out;
+            x = x < lo ? lo : (x > hi ? hi : x);
+            Tc f = floor(x);
+            int64_t c = b + (int64_t)f;
+            Tc ww = x - f;
+            if (c > nd - 2) {   // only when x == hi exactly: the last cell at weight 1
+                c = nd - 2;
+                ww = Tc(1);
+            }
+            w[d] = ww;
             c0[d] = c;
             c1[d] = c + 1;
         }

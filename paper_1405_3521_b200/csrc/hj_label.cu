@@ -18,9 +18,10 @@ __device__ double min_bracket(const DevProblem<double, Ts> &P, const Ts *__restr
     double x[3] = {0, 0, 0};
 #pragma unroll
     for (int d = 0; d < DIM; ++d) x[d] = fma(g[d], P.dx[d], P.lo[d]);
+    const int64_t zero[3] = {0, 0, 0};
     double cs = 1.0;
     if (P.speed && P.dyn == HJ_DYN_AFFINE)
-        cs = interp<double, Ts, DIM>(P.speed, o, vn, P.n, P.periodic, g, 1.0);
+        cs = interp<double, Ts, DIM>(P.speed, o, vn, P.n, P.periodic, zero, g, 1.0);
     double base = (P.cost == HJ_COST_KRUZKOV) ? P.kcost : P.h * cost_state(P, x);
     double best = INFINITY, second = INFINITY;
     int a = -1;
@@ -30,7 +31,7 @@ __device__ double min_bracket(const DevProblem<double, Ts> &P, const Ts *__restr
         double foot[3] = {0, 0, 0};
 #pragma unroll
         for (int d = 0; d < DIM; ++d) foot[d] = fma(P.hdx[d], f[d], g[d]);
-        double I = interp<double, Ts, DIM>(V, o, vn, P.n, P.periodic, foot, P.v_out);
+        double I = interp<double, Ts, DIM>(V, o, vn, P.n, P.periodic, zero, foot, P.v_out);
         double ck = (P.cost == HJ_COST_KRUZKOV) ? base : fma(P.h * P.lr, P.csq[k], base);
         double v = fma(P.beta, I, ck);
         if (v < best) {
@@ -114,9 +115,10 @@ __global__ void k_label(const DevProblem<double, Ts> P, const Ts *__restrict__ V
             double x[3] = {0, 0, 0};
 #pragma unroll
             for (int d = 0; d < DIM; ++d) x[d] = fma(g[d], P.dx[d], P.lo[d]);
+            const int64_t zero[3] = {0, 0, 0};
             double cs = 1.0;
             if (P.speed && P.dyn == HJ_DYN_AFFINE)
-                cs = interp<double, Ts, DIM>(P.speed, o, vn, P.n, P.periodic, g, 1.0);
+                cs = interp<double, Ts, DIM>(P.speed, o, vn, P.n, P.periodic, zero, g, 1.0);
             double f[3];
             dynamics(P, x, cs, a, f);
             bool out = false;

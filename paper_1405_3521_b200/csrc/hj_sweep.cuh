@@ -54,10 +54,10 @@ __global__ void __launch_bounds__(256)
             for (int k = 0; k < P.K; ++k) {
                 T f[3];
                 dynamics(P, x, cs, k, f);
-                T foot[3] = {0, 0, 0};
+                T delta[3] = {0, 0, 0};
 #pragma unroll
-                for (int d = 0; d < DIM; ++d) foot[d] = fma(P.hdx[d], f[d], (T)gi[d]);
-                T I = interp<T, T, DIM>(Vi, o, vn, P.n, P.periodic, foot, P.v_out);
+                for (int d = 0; d < DIM; ++d) delta[d] = P.hdx[d] * f[d];
+                T I = interp<T, T, DIM>(Vi, o, vn, P.n, P.periodic, gi, delta, P.v_out);
                 T ck = (P.cost == HJ_COST_KRUZKOV) ? base : fma(P.h * P.lr, P.csq[k], base);
                 T cand = fma(P.beta, I, ck);
                 best = cand < best ? cand : best;

@@ -229,9 +229,11 @@ def test_p10_interpolation():
     G.reshape(6, 5, 7)[0] = 4.0
     assert abs(o.interp(G, [3, 2, 5.5]) - 3.0) < 1e-14
     assert abs(o.interp(G, [3, 2, -0.5]) - 3.0) < 1e-14
-    # outside the box on a non-periodic axis -> v_out (R3)
-    assert o.interp(G, [6.0000001, 2, 1]) == p.v_out
-    assert o.interp(G, [-1e-9, 2, 1]) == p.v_out
+    # outside the box on a non-periodic axis -> v_out; within 1e-6 cells: clamped (R3)
+    assert o.interp(G, [6.000002, 2, 1]) == p.v_out
+    assert o.interp(G, [-2e-6, 2, 1]) == p.v_out
+    assert o.interp(G, [6.0000005, 2, 1]) == o.interp(G, [6.0, 2, 1])
+    assert o.interp(G, [-5e-7, 2, 1]) == o.interp(G, [0.0, 2, 1])
 
 
 # ---------------------------------------------------------------------------
