@@ -25,6 +25,7 @@ struct DevProblem {
     Tc dub_v, dub_w, vdp_mu;
     Tc l0, lq, ln, lr;
     Tc v_out;
+    int monotone;              // V^0 is a supersolution: iterates decrease (see hj_host.cuh)
     Tc ctrl[HJ_MAX_CONTROLS][3];
     Tc csq[HJ_MAX_CONTROLS];   // |a_k|^2
     const Ts *speed;           // node field or nullptr

@@ -48,6 +48,35 @@ inline double grid_spacing(const hj_grid &g, int d) {
 hj_status validate_grid(const hj_grid *g);
 hj_status validate_problem(const hj_grid *g, const hj_problem *p);
 
+// V^0 (g on targets, v_out elsewhere) is a supersolution, T(V^0) <= V^0, when v_out
+// bounds every bracket: Kruzkov with v_out >= 1 (brackets are beta I + 1 - beta <= 1
+// for I <= 1), or discounted with lambda > 0 and v_out >= h l_max / (1 - beta) over
+// the box.  T is monotone, so then V^{n+1} = T(V^n) <= V^n for every n in exact
+// arithmetic and the sweep may clamp V^{n+1} = min(T(V^n), V^n): the identity on
+// exact iterates, it removes upward rounding noise (no fp32 limit cycles; the
+// stopping rule is always reached).  Off when a g field is given (g <= v_out unknown).
+inline bool supersolution_start(const hj_grid &g, const hj_problem &p, const hj_fields &f) {
+    if (f.g) return false;
+    if (p.cost == HJ_COST_KRUZKOV) return p.v_out >= 1.0 && p.lambda > 0;
+    if (p.lambda <= 0) return false;
+    double x2 = 0, amax2 = 0;
+    for (int d = 0; d < g.dim; ++d)
+        if (!g.periodic[d]) {
+            double m = std::max(std::fabs(g.lo[d]), std::fabs(g.hi[d]));
+            x2 += m * m;
+        }
+    for (int k = 0; k < p.n_controls; ++k) {
+        double a2 = 0;
+        for (int c = 0; c < 3; ++c) a2 += p.controls[k][c] * p.controls[k][c];
+        amax2 = std::max(amax2, a2);
+    }
+    double lmax = std::fabs(p.l0) + std::fabs(p.lq) * x2 + std::fabs(p.ln) * std::sqrt(x2) +
+                  std::fabs(p.lr) * amax2;
+    if (p.l0 < 0 || p.lq < 0 || p.ln < 0 || p.lr < 0) return false;
+    double beta = 1.0 / (1.0 + p.lambda * p.h);
+    return p.v_out >= p.h * lmax / (1.0 - beta) * (1.0 - 1e-12);
+}
+
 template <typename Tc, typename Ts>
 DevProblem<Tc, Ts> make_dev_problem(const hj_grid &g, const hj_problem &p, const hj_fields &f) {
     DevProblem<Tc, Ts> P;
@@ -88,6 +117,7 @@ DevProblem<Tc, Ts> make_dev_problem(const hj_grid &g, const hj_problem &p, const
     }
     P.speed = (const Ts *)f.speed;
     P.g = (const Ts *)f.g;
+    P.monotone = supersolution_start(g, p, f) ? 1 : 0;
     return P;
 }
 

@@ -135,6 +135,34 @@ __global__ void k_plan(const uint32_t *__restrict__ mask, int64_t N, int64_t n0,
     }
 }
 
+template <typename T>
+__global__ void k_absmax(const T *__restrict__ x, int64_t N, unsigned long long *out) {
+    double m = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N;
+         i += (int64_t)gridDim.x * blockDim.x)
+        m = fmax(m, fabs((double)x[i]));
+    for (int s = 16; s > 0; s >>= 1) m = fmax(m, __shfl_down_sync(0xffffffffu, m, s));
+    if ((threadIdx.x & 31) == 0) atomicMax(out, (unsigned long long)__double_as_longlong(m));
+}
+
+hj_status speed_max(const void *speed, int dtype, int64_t N, cudaStream_t s, double *out) {
+    double *pin = pinned_scratch(1);
+    HJ_CHECK(pin != nullptr, "cudaMallocHost failed");
+    unsigned long long *d;
+    HJ_CUDA(cudaMallocAsync(&d, sizeof(*d), s));
+    HJ_CUDA(cudaMemsetAsync(d, 0, sizeof(*d), s));
+    int blocks = (int)std::min<int64_t>((N + 255) / 256, 148 * 8);
+    if (dtype == HJ_F64)
+        k_absmax<double><<<blocks, 256, 0, s>>>((const double *)speed, N, d);
+    else
+        k_absmax<float><<<blocks, 256, 0, s>>>((const float *)speed, N, d);
+    HJ_CUDA(cudaMemcpyAsync(pin, d, sizeof(double), cudaMemcpyDeviceToHost, s));
+    HJ_CUDA(cudaFreeAsync(d, s));
+    HJ_CUDA(cudaStreamSynchronize(s));
+    *out = pin[0];
+    return HJ_OK;
+}
+
 __global__ void k_fill_int(int *p, int n, int v_lo, int v_hi) {
     int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t < n) p[t] = ((t % 6) < 3) ? v_lo : v_hi;
@@ -154,11 +182,9 @@ struct IterResult {
 };
 
 template <typename T>
-static hj_status iterate(const hj_grid &grid, const hj_problem &prob, const DevProblem<T, T> &P,
-                         SweepView<T> *d_views, const std::vector<SweepView<T>> &h_views,
+static hj_status iterate(const DevProblem<T, T> &P, const SweepLaunch<T> &L, int nv,
                          double *res_base, int64_t res_stride, double tol, int64_t max_iter,
                          cudaStream_t s, IterResult &out) {
-    const int nv = (int)h_views.size();
     const int B = 16;
     double *pin = pinned_scratch((size_t)2 * nv * B);
     HJ_CHECK(pin != nullptr, "cudaMallocHost failed for the residual staging buffer");
@@ -170,9 +196,6 @@ static hj_status iterate(const hj_grid &grid, const hj_problem &prob, const DevP
     out.resid.assign(nv, INFINITY);
     out.converged.assign(nv, 0);
     int n_done = 0;
-
-    SweepLaunch<T> L;
-    if (sweep_prepare(grid, prob, h_views, L) != HJ_OK) return HJ_ERR_INVALID;
 
     struct Batch {
         int64_t start, count;
@@ -186,7 +209,7 @@ static hj_status iterate(const hj_grid &grid, const hj_problem &prob, const DevP
         while (inflight.size() < 2 && next < max_iter && n_done < nv) {
             int64_t cnt = std::min<int64_t>(B, max_iter - next);
             for (int64_t it = next; it < next + cnt; ++it) {
-                hj_status st = sweep_launch(P, d_views, L, it, tol, s);
+                hj_status st = sweep_launch(P, L, it, tol, s);
                 if (st != HJ_OK) return st;
                 ++out.launches;
             }
@@ -225,7 +248,6 @@ static hj_status iterate(const hj_grid &grid, const hj_problem &prob, const DevP
     for (auto &e : ev) cudaEventDestroy(e);
     cudaEventDestroy(t0);
     cudaEventDestroy(t1);
-    sweep_release(L);
     return HJ_OK;
 }
 
@@ -239,11 +261,14 @@ static hj_status validate_fields(const hj_fields *f) {
 // hj_solve
 // ---------------------------------------------------------------------------
 template <typename T>
-static size_t solve_ws(int64_t N, int64_t max_iter) {
+static size_t solve_ws(const hj_grid &g, int64_t max_iter) {
+    int64_t N = grid_nodes(g);
+    int64_t vn[3] = {g.n[0], g.dim > 1 ? g.n[1] : 1, g.dim > 2 ? g.n[2] : 1};
     Carver c(nullptr, 0);
     c.take(N * sizeof(T));
     c.take(max_iter * sizeof(double));
-    c.take(sizeof(SweepView<T>));
+    c.take(chg_bytes_for(vn));
+    c.take(sizeof(SweepGroup<T>));
     c.take(64);
     return c.off;
 }
@@ -253,20 +278,21 @@ static hj_status solve_impl(const hj_grid &grid, const hj_problem &prob, const h
                             T *V, double tol, int64_t max_iter, void *ws, size_t ws_bytes,
                             cudaStream_t s, hj_report *rep) {
     int64_t N = grid_nodes(grid);
-    Carver c(ws, ws_bytes);
-    T *V1 = (T *)c.take(N * sizeof(T));
-    double *res = (double *)c.take(max_iter * sizeof(double));
-    SweepView<T> *d_view = (SweepView<T> *)c.take(sizeof(SweepView<T>));
-    unsigned long long *cnt = (unsigned long long *)c.take(64);
-    if (!c.ok()) {
-        set_error("workspace too small: need %zu bytes, got %zu", c.off, ws_bytes);
-        return HJ_ERR_WORKSPACE;
-    }
     SweepView<T> hv;
     memset(&hv, 0, sizeof(hv));
     for (int d = 0; d < 3; ++d) {
         hv.o[d] = 0;
         hv.vn[d] = d < grid.dim ? grid.n[d] : 1;
+    }
+    Carver c(ws, ws_bytes);
+    T *V1 = (T *)c.take(N * sizeof(T));
+    double *res = (double *)c.take(max_iter * sizeof(double));
+    uint8_t *chg = (uint8_t *)c.take(chg_bytes_for(hv.vn));
+    void *group = c.take(sizeof(SweepGroup<T>));
+    unsigned long long *cnt = (unsigned long long *)c.take(64);
+    if (!c.ok()) {
+        set_error("workspace too small: need %zu bytes, got %zu", c.off, ws_bytes);
+        return HJ_ERR_WORKSPACE;
     }
     hv.nodes = N;
     hv.V[0] = V;
@@ -276,15 +302,19 @@ static hj_status solve_impl(const hj_grid &grid, const hj_problem &prob, const h
     auto P = make_dev_problem<T, T>(grid, prob, f);
     HJ_CUDA(cudaMemsetAsync(res, 0, max_iter * sizeof(double), s));
     HJ_CUDA(cudaMemsetAsync(cnt, 0, 64, s));
-    HJ_CUDA(cudaMemcpyAsync(d_view, &hv, sizeof(hv), cudaMemcpyHostToDevice, s));
+    std::vector<SweepView<T>> hvs{hv};
+    std::vector<uint8_t *> chgs{chg};
+    SweepLaunch<T> L;
+    hj_status st = sweep_prepare(grid, prob, f, hvs, chgs, group, s, L);
+    if (st != HJ_OK) return st;
+    const SweepView<T> *d_view = &L.d_group->v[0];
     int blocks = (int)std::min<int64_t>((N + 255) / 256, 148 * 16);
     k_init_view<T><<<dim3(blocks, 1), 256, 0, s>>>(d_view, (T)prob.v_out, (const T *)f.g,
                                                    hv.vn[0], hv.vn[1]);
     k_count_interior<T><<<dim3(blocks, 1), 256, 0, s>>>(d_view, cnt);
     HJ_CUDA(cudaGetLastError());
     IterResult r;
-    std::vector<SweepView<T>> hvs{hv};
-    hj_status st = iterate<T>(grid, prob, P, d_view, hvs, res, 0, tol, max_iter, s, r);
+    st = iterate<T>(P, L, 1, res, 0, tol, max_iter, s, r);
     if (st != HJ_OK) return st;
     int64_t it = r.iters[0];
     if (it & 1) HJ_CUDA(cudaMemcpyAsync(V, V1, N * sizeof(T), cudaMemcpyDeviceToDevice, s));
@@ -297,7 +327,7 @@ static hj_status solve_impl(const hj_grid &grid, const hj_problem &prob, const h
         rep->converged = r.converged[0];
         rep->node_updates = (int64_t)interior * prob.n_controls * it;
         rep->device_ms = r.ms;
-        rep->launches = r.launches + 2;
+        rep->launches = r.launches + 3 + (f.speed ? 1 : 0);
     }
     if (!r.converged[0]) {
         set_error("not converged after %lld iterations (residual %g)", (long long)it, r.resid[0]);
@@ -310,7 +340,7 @@ static hj_status solve_impl(const hj_grid &grid, const hj_problem &prob, const h
 // partitioned solve (ISA steps 3-4)
 // ---------------------------------------------------------------------------
 struct PartLayout {
-    std::vector<size_t> off_v0, off_v1, off_cls;
+    std::vector<size_t> off_v0, off_v1, off_cls, off_chg;
     size_t off_res, off_views, off_asm, off_cnt, total;
 };
 
@@ -326,11 +356,16 @@ static PartLayout part_layout(int m, const hj_subdomain *plan, int64_t max_iter)
         c.take(bn * sizeof(T));
         L.off_cls.push_back(c.off);
         c.take(bn);
+        int64_t vn[3] = {1, 1, 1};
+        for (int d = 0; d < 3; ++d)
+            if (plan[k].n_nodes > 0) vn[d] = plan[k].hi[d] - plan[k].lo[d] + 1;
+        L.off_chg.push_back(c.off);
+        c.take(plan[k].n_nodes > 0 ? chg_bytes_for(vn) : 0);
     }
     L.off_res = c.off;
     c.take((size_t)m * max_iter * sizeof(double));
     L.off_views = c.off;
-    c.take((size_t)m * sizeof(SweepView<T>));
+    c.take(sizeof(SweepGroup<T>));
     L.off_asm = c.off;
     c.take((size_t)m * sizeof(AsmView<T>));
     L.off_cnt = c.off;
@@ -354,11 +389,12 @@ static hj_status partitioned_impl(const hj_grid &grid, const hj_problem &prob,
     int64_t n0 = grid.n[0], n1 = grid.dim > 1 ? grid.n[1] : 1;
     int64_t N = grid_nodes(grid);
     double *res = (double *)(base + L.off_res);
-    SweepView<T> *d_views = (SweepView<T> *)(base + L.off_views);
+    void *group = base + L.off_views;
     AsmView<T> *d_asm = (AsmView<T> *)(base + L.off_asm);
     unsigned long long *cnt = (unsigned long long *)(base + L.off_cnt);
 
     std::vector<SweepView<T>> hv;
+    std::vector<uint8_t *> chgs;
     std::vector<int> subs;
     int64_t max_nodes = 1;
     for (int k = 0; k < m; ++k) {
@@ -386,6 +422,7 @@ static hj_status partitioned_impl(const hj_grid &grid, const hj_problem &prob,
                                                    (int8_t *)v.cls);
         max_nodes = std::max(max_nodes, v.nodes);
         hv.push_back(v);
+        chgs.push_back((uint8_t *)(base + L.off_chg[k]));
         subs.push_back(k);
     }
     int nv = (int)hv.size();
@@ -399,8 +436,10 @@ static hj_status partitioned_impl(const hj_grid &grid, const hj_problem &prob,
     }
     HJ_CUDA(cudaMemsetAsync(res, 0, (size_t)nv * max_iter * sizeof(double), s));
     HJ_CUDA(cudaMemsetAsync(cnt, 0, (size_t)m * sizeof(unsigned long long), s));
-    HJ_CUDA(cudaMemcpyAsync(d_views, hv.data(), nv * sizeof(SweepView<T>),
-                            cudaMemcpyHostToDevice, s));
+    SweepLaunch<T> SL;
+    hj_status st = sweep_prepare(grid, prob, f, hv, chgs, group, s, SL);
+    if (st != HJ_OK) return st;
+    const SweepView<T> *d_views = &SL.d_group->v[0];
     int blocks = (int)std::min<int64_t>((max_nodes + 255) / 256, 148 * 16);
     auto P = make_dev_problem<T, T>(grid, prob, f);
     k_init_view<T><<<dim3(blocks, nv), 256, 0, s>>>(d_views, (T)prob.v_out, (const T *)f.g, n0,
@@ -408,7 +447,7 @@ static hj_status partitioned_impl(const hj_grid &grid, const hj_problem &prob,
     k_count_interior<T><<<dim3(blocks, nv), 256, 0, s>>>(d_views, cnt);
     HJ_CUDA(cudaGetLastError());
     IterResult r;
-    hj_status st = iterate<T>(grid, prob, P, d_views, hv, res, max_iter, tol, max_iter, s, r);
+    st = iterate<T>(P, SL, nv, res, max_iter, tol, max_iter, s, r);
     if (st != HJ_OK) return st;
     std::vector<AsmView<T>> ha(nv);
     for (int q = 0; q < nv; ++q) {
@@ -436,7 +475,7 @@ static hj_status partitioned_impl(const hj_grid &grid, const hj_problem &prob,
             rp.converged = r.converged[q];
             rp.node_updates = (int64_t)interior[q] * prob.n_controls * r.iters[q];
             rp.device_ms = r.ms;
-            rp.launches = q == 0 ? r.launches + nv + 3 : 0;  // shared launches, counted once
+            rp.launches = q == 0 ? r.launches + nv + 3 + (f.speed ? 1 : 0) : 0;  // counted once
         }
     }
     if (!all) {
@@ -455,7 +494,7 @@ extern "C" {
 size_t hj_solve_workspace_bytes(const hj_grid *grid, int32_t dtype, int64_t max_iter) {
     if (!grid || validate_grid(grid) != HJ_OK || max_iter < 1) return 0;
     int64_t N = grid_nodes(*grid);
-    return dtype == HJ_F64 ? solve_ws<double>(N, max_iter) : solve_ws<float>(N, max_iter);
+    return dtype == HJ_F64 ? solve_ws<double>(*grid, max_iter) : solve_ws<float>(*grid, max_iter);
 }
 
 hj_status hj_solve(const hj_grid *grid, const hj_problem *prob, const hj_fields *fields,

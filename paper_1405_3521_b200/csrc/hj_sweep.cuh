@@ -1,114 +1,515 @@
 // hj_sweep.cuh — one Jacobi sweep V^{n+1} = T(V^n) over a set of views
 // (PAPER.md eq. (SL), operator (Tdef) line 238-245, readings R1-R4).
 //
-// Kernel family:
-//   k_sweep_generic<T, DIM>   any dynamics / cost / h: per node, per control, the
-//                             foot, the multilinear interpolation and the min of the
-//                             bracket, corners read through L1/L2.
-// Every sweep kernel:
-//   - exits at once if its view already stopped (res[n-1] < tol), so launching a
-//     few sweeps past convergence is free and the stop is exactly the first n with
-//     ||V^{n+1}-V^n|| < tol (R6);
-//   - folds |V^{n+1}-V^n| into res[n] with one atomicMax per CTA.
+// Work decomposition: every view (the whole grid, or the bounding box of one
+// sub-domain) is cut into tiles; one CTA per tile of every view, all views in one
+// launch.  Two exact short-cuts, both bit-identical to the plain Jacobi sweep:
+//   * stopped views: a CTA exits at once when its view already met the stopping
+//     rule (res[n-1] < tol), so the stop is exactly the first n with
+//     ||V^{n+1}-V^n|| < tol (R6) and sweeps launched past it cost nothing;
+//   * quiet tiles: T(V)|_tile depends only on V over the tile's dependency
+//     neighbourhood (the tiles within the largest foot offset).  If no node of that
+//     neighbourhood changed (bitwise) in sweep n-1, then V^{n+1} = V^n on the tile,
+//     which the other buffer already holds (it holds V^{n-1} = V^n there), so the
+//     tile is skipped.  Work per sweep follows the active front, not the grid.
+//
+// Kernels:
+//   k_sweep_local2d<T,KQ,PC>  2-D, isotropic dynamics f = c(x) a (A = b = 0) with
+//       every foot within one cell (Courant <= 1): the foot's cell is fixed by the
+//       control's quadrant, so the 3x3 neighbourhood is staged once in shared memory
+//       and the bracket of every control is 3 FMA + 1 min in registers
+//       (difference form of the bilinear interpolant, prescaled per node).
+//   k_sweep_generic<T,DIM>    any dynamics / cost / h / dim: per node, per control,
+//       foot + multilinear interpolation, corners through L1/L2.
+// Every CTA folds |V^{n+1}-V^n| of its tile into res[n] (one atomicMax) and
+// publishes its "changed" flag for sweep n+1.
 #pragma once
 
+#include <algorithm>
 #include <vector>
 
 #include "hj_host.cuh"
 
 namespace hj {
 
-template <typename T, int DIM>
-__global__ void __launch_bounds__(256)
-    k_sweep_generic(const DevProblem<T, T> P, const SweepView<T> *__restrict__ views, int64_t it,
-                    double tol) {
-    const SweepView<T> &vw = views[blockIdx.y];
-    if (it > 0 && *(volatile double *)&vw.res[it - 1] < tol) return;
-    const int64_t o[3] = {vw.o[0], vw.o[1], vw.o[2]};
-    const int64_t vn[3] = {vw.vn[0], vw.vn[1], vw.vn[2]};
-    const T *__restrict__ Vi = vw.V[it & 1];
-    T *__restrict__ Vo = vw.V[(it + 1) & 1];
-    const int8_t *__restrict__ cls = vw.cls;
-    const int64_t nodes = vw.nodes;
-    T rmax = T(0);
-    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nodes;
-         t += (int64_t)gridDim.x * blockDim.x) {
-        int64_t li = t % vn[0], r = t / vn[0];
-        int64_t lj = r % vn[1], lk = r / vn[1];
-        int64_t gi[3] = {li + o[0], lj + o[1], lk + o[2]};
-        int64_t gidx = gi[0] + P.n[0] * (gi[1] + P.n[1] * gi[2]);
-        int8_t c = cls[t];
-        T vin = Vi[t];
-        T v;
-        if (c == -2) {
-            v = P.v_out;
-        } else if (c >= 0) {
-            v = P.g ? P.g[gidx] : T(0);
-        } else {
-            T x[3] = {0, 0, 0};
+// ---------------------------------------------------------------------------
+// shared pieces
+// ---------------------------------------------------------------------------
+template <typename T>
+struct TileView {          // per-view tiling, filled by sweep_prepare
+    int32_t nt[3];         // tiles per axis
+    int64_t tiles;         // nt0*nt1*nt2
+    int64_t tile_base;     // first global tile index of this view
+    uint8_t *chg;          // [2][tiles] changed flags (parity of the sweep)
+};
+
+template <typename T>
+struct SweepGroup {        // device-resident description of one launch
+    SweepView<T> v[HJ_MAX_SUBDOMAINS];
+    TileView<T> t[HJ_MAX_SUBDOMAINS];
+    int n_views;
+    int tile_dim[3];       // TX, TY, TZ (nodes)
+    int radius[3];         // dependency radius in tiles
+    int periodic[3];       // periodic axes (views span them fully)
+};
+
+// Locate (view, tile) of this CTA; false if the view has stopped.
+template <typename T>
+__device__ __forceinline__ int find_view(const SweepGroup<T> *__restrict__ G, int64_t b) {
+    int v = 0;
+    while (v + 1 < G->n_views && G->t[v + 1].tile_base <= b) ++v;
+    return v;
+}
+
+// Is any tile of the dependency neighbourhood changed in the previous sweep?
+// (block-wide; every thread returns the same answer).  Periodic axes wrap.
+template <typename T>
+__device__ __forceinline__ bool tile_active(const SweepGroup<T> *__restrict__ G, int v,
+                                            const int tc[3], int64_t it) {
+    if (it == 0) return true;
+    const TileView<T> &tv = G->t[v];
+    const uint8_t *prev = tv.chg + ((it - 1) & 1) * tv.tiles;
+    const int rx = G->radius[0], ry = G->radius[1], rz = G->radius[2];
+    const int wx = 2 * rx + 1, wy = 2 * ry + 1, wz = 2 * rz + 1;
+    const int count = wx * wy * wz;
+    int any = 0;
+    for (int e = threadIdx.x; e < count; e += blockDim.x) {
+        int c[3] = {tc[0] + e % wx - rx, tc[1] + (e / wx) % wy - ry, tc[2] + e / (wx * wy) - rz};
+        bool ok = true;
 #pragma unroll
-            for (int d = 0; d < DIM; ++d) x[d] = fma((T)gi[d], P.dx[d], P.lo[d]);
-            T cs = (P.speed && P.dyn == HJ_DYN_AFFINE) ? P.speed[gidx] : T(1);
-            T base = (P.cost == HJ_COST_KRUZKOV) ? P.kcost : P.h * cost_state(P, x);
-            T best = (T)INFINITY;
-            for (int k = 0; k < P.K; ++k) {
-                T f[3];
-                dynamics(P, x, cs, k, f);
-                T delta[3] = {0, 0, 0};
-#pragma unroll
-                for (int d = 0; d < DIM; ++d) delta[d] = P.hdx[d] * f[d];
-                T I = interp<T, T, DIM>(Vi, o, vn, P.n, P.periodic, gi, delta, P.v_out);
-                T ck = (P.cost == HJ_COST_KRUZKOV) ? base : fma(P.h * P.lr, P.csq[k], base);
-                T cand = fma(P.beta, I, ck);
-                best = cand < best ? cand : best;
+        for (int d = 0; d < 3; ++d) {
+            if (c[d] >= 0 && c[d] < tv.nt[d]) continue;
+            if (G->periodic[d]) {
+                c[d] = ((c[d] % tv.nt[d]) + tv.nt[d]) % tv.nt[d];
+            } else {
+                ok = false;
             }
-            v = best;
         }
-        Vo[t] = v;
-        T dv = v > vin ? v - vin : vin - v;
-        rmax = dv > rmax ? dv : rmax;
+        if (ok) any |= prev[c[0] + tv.nt[0] * ((int64_t)c[1] + (int64_t)tv.nt[1] * c[2])];
     }
-    // CTA max -> one atomic
+    return __syncthreads_or(any) != 0;
+}
+
+template <typename T>
+__device__ __forceinline__ void tile_finish(const SweepGroup<T> *__restrict__ G, int v,
+                                            int64_t tile, int64_t it, T rmax, int changed) {
 #pragma unroll
     for (int s = 16; s > 0; s >>= 1) {
         T other = __shfl_down_sync(0xffffffffu, rmax, s);
         rmax = other > rmax ? other : rmax;
     }
-    __shared__ T red[8];
+    __shared__ T red[32];
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = rmax;
-    __syncthreads();
+    int any = __syncthreads_or(changed);
     if (threadIdx.x == 0) {
         T m = red[0];
         for (int w = 1; w < (int)(blockDim.x >> 5); ++w) m = red[w] > m ? red[w] : m;
-        if (m > T(0)) atomic_max_nonneg(&vw.res[it], (double)m);
+        if (m > T(0)) atomic_max_nonneg(&G->v[v].res[it], (double)m);
+        G->t[v].chg[(it & 1) * G->t[v].tiles + tile] = (uint8_t)(any != 0);
     }
 }
 
 template <typename T>
-struct SweepLaunch {
-    int dim;
-    dim3 grid;
-    int n_views;
-};
+__device__ __forceinline__ bool same_bits(T a, T b);
+template <>
+__device__ __forceinline__ bool same_bits<float>(float a, float b) {
+    return __float_as_uint(a) == __float_as_uint(b);
+}
+template <>
+__device__ __forceinline__ bool same_bits<double>(double a, double b) {
+    return __double_as_longlong(a) == __double_as_longlong(b);
+}
 
-template <typename T>
-hj_status sweep_prepare(const hj_grid &g, const hj_problem &p,
-                        const std::vector<SweepView<T>> &views, SweepLaunch<T> &L) {
-    int64_t mx = 1;
-    for (auto &v : views) mx = std::max<int64_t>(mx, v.nodes);
-    L.dim = g.dim;
-    L.n_views = (int)views.size();
-    L.grid = dim3((unsigned)std::min<int64_t>((mx + 255) / 256, 148 * 8), L.n_views);
-    return HJ_OK;
+// generic per-node bracket-min (global-memory corners)
+template <typename T, int DIM>
+__device__ __forceinline__ T node_update_generic(const DevProblem<T, T> &P, const T *__restrict__ Vi,
+                                                 const int64_t o[3], const int64_t vn[3],
+                                                 const int64_t gi[3], int64_t gidx) {
+    T x[3] = {0, 0, 0};
+#pragma unroll
+    for (int d = 0; d < DIM; ++d) x[d] = fma((T)gi[d], P.dx[d], P.lo[d]);
+    T cs = (P.speed && P.dyn == HJ_DYN_AFFINE) ? P.speed[gidx] : T(1);
+    T base = (P.cost == HJ_COST_KRUZKOV) ? P.kcost : P.h * cost_state(P, x);
+    T best = (T)INFINITY;
+    for (int k = 0; k < P.K; ++k) {
+        T f[3];
+        dynamics(P, x, cs, k, f);
+        T delta[3] = {0, 0, 0};
+#pragma unroll
+        for (int d = 0; d < DIM; ++d) delta[d] = P.hdx[d] * f[d];
+        T I = interp<T, T, DIM>(Vi, o, vn, P.n, P.periodic, gi, delta, P.v_out);
+        T ck = (P.cost == HJ_COST_KRUZKOV) ? base : fma(P.h * P.lr, P.csq[k], base);
+        T cand = fma(P.beta, I, ck);
+        best = cand < best ? cand : best;
+    }
+    return best;
 }
 
 template <typename T>
-hj_status sweep_launch(const DevProblem<T, T> &P, const SweepView<T> *d_views,
-                       const SweepLaunch<T> &L, int64_t it, double tol, cudaStream_t s) {
-    if (L.dim == 2)
-        k_sweep_generic<T, 2><<<L.grid, 256, 0, s>>>(P, d_views, it, tol);
-    else
-        k_sweep_generic<T, 3><<<L.grid, 256, 0, s>>>(P, d_views, it, tol);
+__device__ __forceinline__ T node_update_edge(const DevProblem<T, T> &P, const T *__restrict__ Vi,
+                                           int64_t o0, int64_t o1, int64_t vn0, int64_t vn1,
+                                           int64_t g0, int64_t g1, int64_t gidx) {
+    const int64_t o[3] = {o0, o1, 0}, vn[3] = {vn0, vn1, 1}, gi[3] = {g0, g1, 0};
+    return node_update_generic<T, 2>(P, Vi, o, vn, gi, gidx);
+}
+
+// ---------------------------------------------------------------------------
+// generic tiled kernel: tile 32 x 8 x 1, one node per thread
+// ---------------------------------------------------------------------------
+template <typename T, int DIM>
+__global__ void __launch_bounds__(256)
+    k_sweep_generic(const DevProblem<T, T> P, const SweepGroup<T> *__restrict__ G, int64_t it,
+                    double tol) {
+    const int64_t b = blockIdx.x;
+    const int v = find_view(G, b);
+    const SweepView<T> &vw = G->v[v];
+    if (it > 0 && *(volatile double *)&vw.res[it - 1] < tol) return;
+    const TileView<T> &tv = G->t[v];
+    const int64_t tile = b - tv.tile_base;
+    const int tc[3] = {(int)(tile % tv.nt[0]), (int)((tile / tv.nt[0]) % tv.nt[1]),
+                       (int)(tile / ((int64_t)tv.nt[0] * tv.nt[1]))};
+    if (!tile_active(G, v, tc, it)) {
+        if (threadIdx.x == 0) tv.chg[(it & 1) * tv.tiles + tile] = 0;
+        return;
+    }
+    const int64_t o[3] = {vw.o[0], vw.o[1], vw.o[2]};
+    const int64_t vn[3] = {vw.vn[0], vw.vn[1], vw.vn[2]};
+    const T *__restrict__ Vi = vw.V[it & 1];
+    T *__restrict__ Vo = vw.V[(it + 1) & 1];
+    const int64_t li = (int64_t)tc[0] * 32 + (threadIdx.x & 31);
+    const int64_t lj = (int64_t)tc[1] * 8 + (threadIdx.x >> 5);
+    const int64_t lk = tc[2];
+    T rmax = T(0);
+    int changed = 0;
+    if (li < vn[0] && lj < vn[1] && lk < vn[2]) {
+        const int64_t t = li + vn[0] * (lj + vn[1] * lk);
+        const int64_t gi[3] = {li + o[0], lj + o[1], lk + o[2]};
+        const int64_t gidx = gi[0] + P.n[0] * (gi[1] + P.n[1] * gi[2]);
+        const int8_t c = vw.cls[t];
+        const T vin = Vi[t];
+        T vnew;
+        if (c == -2)
+            vnew = P.v_out;
+        else if (c >= 0)
+            vnew = P.g ? P.g[gidx] : T(0);
+        else {
+            vnew = node_update_generic<T, DIM>(P, Vi, o, vn, gi, gidx);
+            if (P.monotone) vnew = fmin(vnew, vin);
+        }
+        Vo[t] = vnew;
+        rmax = vnew > vin ? vnew - vin : vin - vnew;
+        changed = !same_bits(vnew, vin);
+    }
+    tile_finish(G, v, tile, it, rmax, changed);
+}
+
+// ---------------------------------------------------------------------------
+// local 2-D kernel: tile 32 x 32, 256 threads, 4 rows per thread
+// ---------------------------------------------------------------------------
+template <typename T>
+struct LocalCtrl {
+    // quadrant q: bit0 -> foot x offset <= 0, bit1 -> foot y offset <= 0.
+    // ax = |u_x| h/dx, ay = |u_y| h/dy of the controls of that quadrant (padded to KQ
+    // by repeating a control: repeats do not change a min); ck = per-control cost.
+    T ax[4][32], ay[4][32], ck[4][32];
+};
+
+template <typename T, int KQ, bool PC>
+__global__ void __launch_bounds__(256, 2)
+    k_sweep_local2d(const DevProblem<T, T> P, const LocalCtrl<T> C,
+                    const SweepGroup<T> *__restrict__ G, int64_t it, double tol) {
+    constexpr int TX = 32, TY = 32, RY = 4, SW = TX + 2;
+    __shared__ T s[(TY + 2) * SW];
+    const int64_t b = blockIdx.x;
+    const int v = find_view(G, b);
+    const SweepView<T> &vw = G->v[v];
+    if (it > 0 && *(volatile double *)&vw.res[it - 1] < tol) return;
+    const TileView<T> &tv = G->t[v];
+    const int64_t tile = b - tv.tile_base;
+    const int tc[3] = {(int)(tile % tv.nt[0]), (int)(tile / tv.nt[0]), 0};
+    if (!tile_active(G, v, tc, it)) {
+        if (threadIdx.x == 0) tv.chg[(it & 1) * tv.tiles + tile] = 0;
+        return;
+    }
+    const int64_t vn0 = vw.vn[0], vn1 = vw.vn[1];
+    const T *__restrict__ Vi = vw.V[it & 1];
+    T *__restrict__ Vo = vw.V[(it + 1) & 1];
+    const int64_t x0 = (int64_t)tc[0] * TX, y0 = (int64_t)tc[1] * TY;
+    const T v_out = P.v_out;
+    // stage the tile + 1-node halo (outside the view: ghost = v_out)
+    for (int e = threadIdx.x; e < (TY + 2) * SW; e += 256) {
+        const int r = e / SW, c = e - r * SW;
+        const int64_t li = x0 + c - 1, lj = y0 + r - 1;
+        T val = v_out;
+        if (li >= 0 && lj >= 0 && li < vn0 && lj < vn1) val = Vi[li + vn0 * lj];
+        s[e] = val;
+    }
+    __syncthreads();
+    const int lx = threadIdx.x & 31, ly0 = (threadIdx.x >> 5) * RY;
+    const int64_t o0 = vw.o[0], o1 = vw.o[1];
+    const int64_t n0 = P.n[0], n1 = P.n[1];
+    T rmax = T(0);
+    int changed = 0;
+#pragma unroll 1
+    for (int r = 0; r < RY; ++r) {
+        const int ly = ly0 + r;
+        const int64_t li = x0 + lx, lj = y0 + ly;
+        if (li >= vn0 || lj >= vn1) continue;
+        const int64_t t = li + vn0 * lj;
+        const int64_t gi[3] = {li + o0, lj + o1, 0};
+        const int64_t gidx = gi[0] + n0 * gi[1];
+        const int8_t c = vw.cls[t];
+        const T *sp = s + (ly + 1) * SW + (lx + 1);
+        const T V00 = sp[0];
+        T vnew;
+        if (c == -2) {
+            vnew = v_out;
+        } else if (c >= 0) {
+            vnew = P.g ? P.g[gidx] : T(0);
+        } else if (gi[0] == 0 || gi[1] == 0 || gi[0] == n0 - 1 || gi[1] == n1 - 1) {
+            // on the box edge a foot can leave the box (R3): exact generic bracket
+            vnew = node_update_edge<T>(P, Vi, o0, o1, vn0, vn1, gi[0], gi[1], gidx);
+        } else {
+            const T Vm0 = sp[-1], Vp0 = sp[1], V0m = sp[-SW], V0p = sp[SW];
+            const T Vmm = sp[-SW - 1], Vpm = sp[-SW + 1], Vmp = sp[SW - 1], Vpp = sp[SW + 1];
+            const T sc = P.speed ? P.speed[gidx] : T(1);
+            T base;
+            if (P.cost == HJ_COST_KRUZKOV) {
+                base = P.kcost;
+            } else {
+                const T x[3] = {fma((T)gi[0], P.dx[0], P.lo[0]), fma((T)gi[1], P.dx[1], P.lo[1]),
+                                T(0)};
+                base = P.h * cost_state(P, x);
+            }
+            const T C0 = fma(P.beta, V00, base);
+            const T bs = P.beta * sc, bss = bs * sc;
+            T best = (T)INFINITY;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const T Vx = (q & 1) ? Vm0 : Vp0;
+                const T Vy = (q & 2) ? V0m : V0p;
+                const T Vxy = (q == 0) ? Vpp : (q == 1) ? Vmp : (q == 2) ? Vpm : Vmm;
+                const T Dx = Vx - V00, Dy = Vy - V00, Dxy = (Vxy - Vx) - Dy;
+                const T A1 = bs * Dx, A2 = bs * Dy, A3 = bss * Dxy;
+#pragma unroll
+                for (int k = 0; k < KQ; ++k) {
+                    const T ax = C.ax[q][k], ay = C.ay[q][k];
+                    const T u = fma(ax, A1, PC ? C0 + C.ck[q][k] : C0);
+                    const T cand = fma(ay, fma(ax, A3, A2), u);
+                    best = fmin(best, cand);
+                }
+            }
+            vnew = best;
+        }
+        if (c == -1 && P.monotone) vnew = fmin(vnew, V00);
+        Vo[t] = vnew;
+        const T dv = vnew > V00 ? vnew - V00 : V00 - vnew;
+        rmax = dv > rmax ? dv : rmax;
+        changed |= !same_bits(vnew, V00);
+    }
+    tile_finish(G, v, tile, it, rmax, changed);
+}
+
+// ---------------------------------------------------------------------------
+// host side: choose the kernel, tile the views, launch
+// ---------------------------------------------------------------------------
+enum SweepKind { SWEEP_GENERIC = 0, SWEEP_LOCAL2D = 1 };
+
+template <typename T>
+struct SweepLaunch {
+    int kind = SWEEP_GENERIC;
+    int dim = 2;
+    int kq = 0;
+    bool per_ctrl_cost = false;
+    int64_t total_tiles = 0;
+    SweepGroup<T> *d_group = nullptr;   // device copy (inside the caller's workspace)
+    LocalCtrl<T> ctrl;
+};
+
+// bytes of change flags a view needs under the smallest tiling (32 x 8 x 1)
+inline int64_t chg_bytes_for(const int64_t vn[3]) {
+    int64_t t = ((vn[0] + 31) / 32) * ((vn[1] + 7) / 8) * vn[2];
+    return 2 * t;
+}
+
+hj_status speed_max(const void *speed, int dtype, int64_t N, cudaStream_t s, double *out);
+
+// Largest |foot offset| per axis in cells over the whole box (a safe bound).
+inline void foot_bound(const hj_grid &g, const hj_problem &p, double cmax, double H[3]) {
+    double xmax[3] = {0, 0, 0};
+    for (int d = 0; d < g.dim; ++d) xmax[d] = std::max(std::fabs(g.lo[d]), std::fabs(g.hi[d]));
+    for (int d = 0; d < 3; ++d) H[d] = 0;
+    double umax[3] = {0, 0, 0}, amax = 0;
+    for (int k = 0; k < p.n_controls; ++k) {
+        for (int d = 0; d < 3; ++d) umax[d] = std::max(umax[d], std::fabs(p.controls[k][d]));
+        amax = std::max(amax, std::fabs(p.controls[k][0]));
+    }
+    for (int d = 0; d < g.dim; ++d) {
+        double f = 0;
+        if (p.dynamics == HJ_DYN_AFFINE) {
+            f = cmax * umax[d] + std::fabs(p.b[d]);
+            for (int e = 0; e < g.dim; ++e) f += std::fabs(p.A[d][e]) * xmax[e];
+        } else if (p.dynamics == HJ_DYN_DUBINS) {
+            f = d < 2 ? std::fabs(p.dubins_v) : std::fabs(p.dubins_w) * amax;
+        } else {
+            f = d == 0 ? xmax[1]
+                       : std::fabs(p.vdp_mu) * (1 + xmax[0] * xmax[0]) * xmax[1] + xmax[0] + amax;
+        }
+        H[d] = p.h * f / grid_spacing(g, d);
+    }
+}
+
+template <typename T>
+hj_status sweep_prepare(const hj_grid &g, const hj_problem &p, const hj_fields &f,
+                        std::vector<SweepView<T>> &views, const std::vector<uint8_t *> &chg,
+                        void *d_group_mem, cudaStream_t s, SweepLaunch<T> &L) {
+    const int dtype = sizeof(T) == 8 ? HJ_F64 : HJ_F32;
+    double cmax = 1.0;
+    if (f.speed && p.dynamics == HJ_DYN_AFFINE) {
+        hj_status st = speed_max(f.speed, dtype, grid_nodes(g), s, &cmax);
+        if (st != HJ_OK) return st;
+    }
+    double H[3];
+    foot_bound(g, p, cmax, H);
+    L.dim = g.dim;
+    bool iso = p.dynamics == HJ_DYN_AFFINE && g.dim == 2;
+    for (int d = 0; d < 3 && iso; ++d) {
+        if (p.b[d] != 0) iso = false;
+        for (int e = 0; e < 3; ++e)
+            if (p.A[d][e] != 0) iso = false;
+    }
+    const bool local = iso && H[0] <= 1 + 1e-6 && H[1] <= 1 + 1e-6 && !g.periodic[0] &&
+                       !g.periodic[1];
+    L.kind = SWEEP_GENERIC;
+    int tile_dim[3] = {32, 8, 1};
+    if (local) {
+        // sort the controls by quadrant; balance controls on an axis (|u| < 1e-9)
+        std::vector<int> quad[4];
+        double dx = grid_spacing(g, 0), dy = grid_spacing(g, 1);
+        std::vector<int> axis_ctrl;
+        for (int k = 0; k < p.n_controls; ++k) {
+            double ux = p.controls[k][0], uy = p.controls[k][1];
+            if (std::fabs(ux) < 1e-9 || std::fabs(uy) < 1e-9) {
+                axis_ctrl.push_back(k);
+                continue;
+            }
+            quad[(ux < 0 ? 1 : 0) | (uy < 0 ? 2 : 0)].push_back(k);
+        }
+        for (int k : axis_ctrl) {
+            double ux = p.controls[k][0], uy = p.controls[k][1];
+            int best = -1;
+            for (int q = 0; q < 4; ++q) {
+                bool okx = std::fabs(ux) < 1e-9 || ((q & 1) ? ux < 0 : ux > 0);
+                bool oky = std::fabs(uy) < 1e-9 || ((q & 2) ? uy < 0 : uy > 0);
+                if (okx && oky && (best < 0 || quad[q].size() < quad[best].size())) best = q;
+            }
+            quad[best].push_back(k);
+        }
+        size_t mx = 1;
+        for (auto &q : quad) mx = std::max(mx, q.size());
+        const int choices[] = {4, 8, 12, 16, 24, 32};
+        int kq = 0;
+        for (int c : choices)
+            if ((size_t)c >= mx) {
+                kq = c;
+                break;
+            }
+        if (kq) {
+            L.kind = SWEEP_LOCAL2D;
+            L.kq = kq;
+            L.per_ctrl_cost = p.cost == HJ_COST_DISCOUNTED && p.lr != 0;
+            memset(&L.ctrl, 0, sizeof(L.ctrl));
+            for (int q = 0; q < 4; ++q) {
+                // an empty quadrant repeats some control of another quadrant's... any
+                // control works as padding only inside its own quadrant: use a
+                // weight-0 "stay" entry (ax = ay = 0 gives beta V00 + cost, which is
+                // a valid bracket only if that control exists) -> repeat a real one.
+                std::vector<int> &lst = quad[q];
+                for (int j = 0; j < kq; ++j) {
+                    int k = lst.empty() ? -1 : lst[std::min<size_t>(j, lst.size() - 1)];
+                    if (k < 0) {
+                        L.ctrl.ax[q][j] = L.ctrl.ay[q][j] = 0;
+                        L.ctrl.ck[q][j] = (T)INFINITY;   // never the min
+                        continue;
+                    }
+                    L.ctrl.ax[q][j] = (T)(std::fabs(p.controls[k][0]) * p.h / dx);
+                    L.ctrl.ay[q][j] = (T)(std::fabs(p.controls[k][1]) * p.h / dy);
+                    double a2 = 0;
+                    for (int c = 0; c < 3; ++c) a2 += p.controls[k][c] * p.controls[k][c];
+                    L.ctrl.ck[q][j] = (T)(p.h * p.lr * a2);
+                }
+                if (lst.empty()) L.per_ctrl_cost = true;   // the +inf padding needs ck
+            }
+            tile_dim[0] = 32;
+            tile_dim[1] = 32;
+        }
+    }
+    SweepGroup<T> hg;
+    memset(&hg, 0, sizeof(hg));
+    hg.n_views = (int)views.size();
+    int64_t base = 0;
+    for (int d = 0; d < 3; ++d) {
+        hg.tile_dim[d] = tile_dim[d];
+        hg.periodic[d] = d < g.dim ? g.periodic[d] : 0;
+    }
+    for (int d = 0; d < 3; ++d) {
+        hg.radius[d] = d < g.dim ? (int)std::ceil((H[d] + 1.0) / tile_dim[d]) : 0;
+        if (L.kind == SWEEP_LOCAL2D) hg.radius[d] = d < 2 ? 1 : 0;
+    }
+    for (size_t q = 0; q < views.size(); ++q) {
+        hg.v[q] = views[q];
+        TileView<T> &tv = hg.t[q];
+        for (int d = 0; d < 3; ++d)
+            tv.nt[d] = (int32_t)((views[q].vn[d] + tile_dim[d] - 1) / tile_dim[d]);
+        tv.tiles = (int64_t)tv.nt[0] * tv.nt[1] * tv.nt[2];
+        tv.tile_base = base;
+        tv.chg = chg[q];
+        base += tv.tiles;
+    }
+    L.total_tiles = base;
+    L.d_group = (SweepGroup<T> *)d_group_mem;
+    cudaError_t e = cudaMemcpyAsync(L.d_group, &hg, sizeof(hg), cudaMemcpyHostToDevice, s);
+    if (e != cudaSuccess) {
+        set_error("sweep_prepare upload: %s", cudaGetErrorString(e));
+        return HJ_ERR_CUDA;
+    }
+    // the host struct must outlive the async copy
+    e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) {
+        set_error("sweep_prepare sync: %s", cudaGetErrorString(e));
+        return HJ_ERR_CUDA;
+    }
+    return HJ_OK;
+}
+
+template <typename T, bool PC>
+static void launch_local(const DevProblem<T, T> &P, const SweepLaunch<T> &L, int64_t it,
+                         double tol, cudaStream_t s) {
+    dim3 grid((unsigned)L.total_tiles);
+    switch (L.kq) {
+        case 4: k_sweep_local2d<T, 4, PC><<<grid, 256, 0, s>>>(P, L.ctrl, L.d_group, it, tol); break;
+        case 8: k_sweep_local2d<T, 8, PC><<<grid, 256, 0, s>>>(P, L.ctrl, L.d_group, it, tol); break;
+        case 12: k_sweep_local2d<T, 12, PC><<<grid, 256, 0, s>>>(P, L.ctrl, L.d_group, it, tol); break;
+        case 16: k_sweep_local2d<T, 16, PC><<<grid, 256, 0, s>>>(P, L.ctrl, L.d_group, it, tol); break;
+        case 24: k_sweep_local2d<T, 24, PC><<<grid, 256, 0, s>>>(P, L.ctrl, L.d_group, it, tol); break;
+        default: k_sweep_local2d<T, 32, PC><<<grid, 256, 0, s>>>(P, L.ctrl, L.d_group, it, tol); break;
+    }
+}
+
+template <typename T>
+hj_status sweep_launch(const DevProblem<T, T> &P, const SweepLaunch<T> &L, int64_t it, double tol,
+                       cudaStream_t s) {
+    if (L.total_tiles == 0) return HJ_OK;
+    if (L.kind == SWEEP_LOCAL2D) {
+        if (L.per_ctrl_cost)
+            launch_local<T, true>(P, L, it, tol, s);
+        else
+            launch_local<T, false>(P, L, it, tol, s);
+    } else if (L.dim == 2) {
+        k_sweep_generic<T, 2><<<(unsigned)L.total_tiles, 256, 0, s>>>(P, L.d_group, it, tol);
+    } else {
+        k_sweep_generic<T, 3><<<(unsigned)L.total_tiles, 256, 0, s>>>(P, L.d_group, it, tol);
+    }
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) {
         set_error("sweep launch failed: %s", cudaGetErrorString(e));
@@ -116,8 +517,5 @@ hj_status sweep_launch(const DevProblem<T, T> &P, const SweepView<T> *d_views,
     }
     return HJ_OK;
 }
-
-template <typename T>
-void sweep_release(SweepLaunch<T> &) {}
 
 }  // namespace hj
