@@ -181,7 +181,8 @@ def main():
     torch.cuda.synchronize()
 
     st = torch.cuda.current_stream()
-    step_ms, updates, fine_updates, sweep_ms, sweep_launches, launches = [], 0, 0, 0.0, 0, 0
+    step_ms, updates, fine_eval, sweep_ms, sweep_launches, launches = [], 0, 0, 0.0, 0, 0
+    evaluated = 0
     with ClockSampler(local) as clocks:
         for _ in range(args.steps):
             l2_flush.fill_(1)                       # L2 flush between timed steps
@@ -198,7 +199,8 @@ def main():
             fr = [r for r in res["reports"] if r is not None]
             u = rc["node_updates"] + sum(r["node_updates"] for r in fr)
             updates += u
-            fine_updates += sum(r["node_updates"] for r in fr)
+            fine_eval += sum(r["evaluated_updates"] for r in fr)
+            evaluated += rc["evaluated_updates"] + sum(r["evaluated_updates"] for r in fr)
             if fr:
                 sweep_ms += fr[0]["device_ms"]
                 sweep_launches += fr[0]["launches"] - len(fr) - 3
@@ -206,11 +208,11 @@ def main():
             launches += rc["launches"] + 2 + 2 + sum(r["launches"] for r in fr)
     total_ms = float(np.sum(step_ms))
     if world > 1:
-        t = torch.tensor([total_ms, updates], dtype=torch.float64, device="cuda")
+        t = torch.tensor([total_ms, updates, evaluated], dtype=torch.float64, device="cuda")
         tmax = t.clone()
         dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
         dist.all_reduce(t, op=dist.ReduceOp.SUM)
-        total_ms, updates = float(tmax[0]), float(t[1])
+        total_ms, updates, evaluated = float(tmax[0]), float(t[1]), float(t[2])
     value = updates / (total_ms / 1e3)
 
     # ---- end to end through the public API with host buffers ------------------
@@ -259,7 +261,7 @@ def main():
     sm_mhz = float(peaks.get("sm_max_mhz", 1965.0))
     peak_ops = 148 * 4 * 32 * sm_mhz * 1e6 / 1e12          # issue slots, T lane-op/s
     dim = cfg.fine.grid.dim
-    achieved = fine_updates * ALGO_OPS_PER_UPDATE[dim] / (sweep_ms / 1e3) / 1e12 if sweep_ms else 0
+    achieved = fine_eval * ALGO_OPS_PER_UPDATE[dim] / (sweep_ms / 1e3) / 1e12 if sweep_ms else 0
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):
@@ -290,6 +292,8 @@ def main():
                        "parallelism": f"subdomains over {world} GPU(s)",
                        "l2": "flushed (256 MiB write) between timed steps"},
             "time_to_solution_ms": total_ms / args.steps,
+            "evaluated_updates_per_s": evaluated / (total_ms / 1e3),
+            "fine_sweeps": max((r["iterations"] for r in res["reports"] if r), default=0),
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "ms_per_step": e2e_total / len(e2e_ms)},
             "gpu_launches": launches,

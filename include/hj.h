@@ -122,9 +122,12 @@ typedef struct {
     double residual;        /* ||V^{n} - V^{n-1}||_inf of the last one          */
     int32_t converged;      /* residual < tol                                   */
     int32_t reserved;
-    int64_t node_updates;   /* interior nodes x controls evaluated (all sweeps)   */
+    int64_t node_updates;   /* Jacobi work: interior nodes x controls x iterations */
     double device_ms;       /* device time of the iteration (CUDA events)       */
     int64_t launches;       /* kernels this call launched (sweeps + helpers)    */
+    int64_t evaluated_updates; /* interior nodes x controls actually evaluated: the
+                               sweeps skip tiles whose inputs did not change (their
+                               T(V) is known exactly), so this is <= node_updates  */
 } hj_report;
 
 typedef struct {            /* one fine sub-domain S_k (hj_partition_plan)       */

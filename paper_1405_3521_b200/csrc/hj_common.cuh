@@ -42,6 +42,7 @@ struct SweepView {
     T *V[2];           // iterate buffers (dense over the view)
     const int8_t *cls; // >= 0 target piece, -1 interior, -2 ghost (outside S_k)
     double *res;       // res[n] = ||V^{n+1} - V^n||_inf (atomicMax on the bits)
+    unsigned long long *work;  // interior nodes evaluated (summed over sweeps)
 };
 
 template <typename T>

@@ -299,6 +299,7 @@ static hj_status solve_impl(const hj_grid &grid, const hj_problem &prob, const h
     hv.V[1] = V1;
     hv.cls = f.piece;
     hv.res = res;
+    hv.work = cnt + 1;
     auto P = make_dev_problem<T, T>(grid, prob, f);
     HJ_CUDA(cudaMemsetAsync(res, 0, max_iter * sizeof(double), s));
     HJ_CUDA(cudaMemsetAsync(cnt, 0, 64, s));
@@ -318,10 +319,12 @@ static hj_status solve_impl(const hj_grid &grid, const hj_problem &prob, const h
     if (st != HJ_OK) return st;
     int64_t it = r.iters[0];
     if (it & 1) HJ_CUDA(cudaMemcpyAsync(V, V1, N * sizeof(T), cudaMemcpyDeviceToDevice, s));
-    unsigned long long interior = 0;
-    HJ_CUDA(cudaMemcpyAsync(&interior, cnt, sizeof(interior), cudaMemcpyDeviceToHost, s));
+    unsigned long long counts[2] = {0, 0};
+    HJ_CUDA(cudaMemcpyAsync(counts, cnt, sizeof(counts), cudaMemcpyDeviceToHost, s));
     HJ_CUDA(cudaStreamSynchronize(s));
+    const unsigned long long interior = counts[0];
     if (rep) {
+        rep->evaluated_updates = (int64_t)counts[1] * prob.n_controls;
         rep->iterations = it;
         rep->residual = r.resid[0];
         rep->converged = r.converged[0];
@@ -369,7 +372,7 @@ static PartLayout part_layout(int m, const hj_subdomain *plan, int64_t max_iter)
     L.off_asm = c.off;
     c.take((size_t)m * sizeof(AsmView<T>));
     L.off_cnt = c.off;
-    c.take((size_t)m * sizeof(unsigned long long));
+    c.take((size_t)2 * m * sizeof(unsigned long long));
     L.total = c.off;
     return L;
 }
@@ -416,6 +419,7 @@ static hj_status partitioned_impl(const hj_grid &grid, const hj_problem &prob,
         v.V[1] = (T *)(base + L.off_v1[k]);
         v.cls = (const int8_t *)(base + L.off_cls[k]);
         v.res = res + (size_t)hv.size() * max_iter;
+        v.work = cnt + m + hv.size();
         int blocks = (int)std::min<int64_t>((v.nodes + 255) / 256, 148 * 16);
         k_subdomain_classes<<<blocks, 256, 0, s>>>(mask, f.piece, k, v.o[0], v.o[1], v.o[2],
                                                    v.vn[0], v.vn[1], v.nodes, n0, n1,
@@ -435,7 +439,7 @@ static hj_status partitioned_impl(const hj_grid &grid, const hj_problem &prob,
         return HJ_OK;
     }
     HJ_CUDA(cudaMemsetAsync(res, 0, (size_t)nv * max_iter * sizeof(double), s));
-    HJ_CUDA(cudaMemsetAsync(cnt, 0, (size_t)m * sizeof(unsigned long long), s));
+    HJ_CUDA(cudaMemsetAsync(cnt, 0, (size_t)2 * m * sizeof(unsigned long long), s));
     SweepLaunch<T> SL;
     hj_status st = sweep_prepare(grid, prob, f, hv, chgs, group, s, SL);
     if (st != HJ_OK) return st;
@@ -461,8 +465,8 @@ static hj_status partitioned_impl(const hj_grid &grid, const hj_problem &prob,
     HJ_CUDA(cudaMemcpyAsync(d_asm, ha.data(), nv * sizeof(AsmView<T>), cudaMemcpyHostToDevice, s));
     k_assemble<T><<<gblocks, 256, 0, s>>>(d_asm, nv, mask, n0, n1, N, (T)prob.v_out, Vbar);
     HJ_CUDA(cudaGetLastError());
-    std::vector<unsigned long long> interior(m, 0);
-    HJ_CUDA(cudaMemcpyAsync(interior.data(), cnt, nv * sizeof(unsigned long long),
+    std::vector<unsigned long long> interior(2 * m, 0);
+    HJ_CUDA(cudaMemcpyAsync(interior.data(), cnt, 2 * m * sizeof(unsigned long long),
                             cudaMemcpyDeviceToHost, s));
     HJ_CUDA(cudaStreamSynchronize(s));
     bool all = true;
@@ -474,6 +478,7 @@ static hj_status partitioned_impl(const hj_grid &grid, const hj_problem &prob,
             rp.residual = r.resid[q];
             rp.converged = r.converged[q];
             rp.node_updates = (int64_t)interior[q] * prob.n_controls * r.iters[q];
+            rp.evaluated_updates = (int64_t)interior[m + q] * prob.n_controls;
             rp.device_ms = r.ms;
             rp.launches = q == 0 ? r.launches + nv + 3 + (f.speed ? 1 : 0) : 0;  // counted once
         }

@@ -92,7 +92,11 @@ __device__ __forceinline__ bool tile_active(const SweepGroup<T> *__restrict__ G,
 
 template <typename T>
 __device__ __forceinline__ void tile_finish(const SweepGroup<T> *__restrict__ G, int v,
-                                            int64_t tile, int64_t it, T rmax, int changed) {
+                                            int64_t tile, int64_t it, T rmax, int changed,
+                                            int evaluated) {
+    evaluated = __reduce_add_sync(0xffffffffu, evaluated);
+    if ((threadIdx.x & 31) == 0 && evaluated)
+        atomicAdd(G->v[v].work, (unsigned long long)evaluated);
 #pragma unroll
     for (int s = 16; s > 0; s >>= 1) {
         T other = __shfl_down_sync(0xffffffffu, rmax, s);
@@ -145,14 +149,6 @@ __device__ __forceinline__ T node_update_generic(const DevProblem<T, T> &P, cons
     return best;
 }
 
-template <typename T>
-__device__ __forceinline__ T node_update_edge(const DevProblem<T, T> &P, const T *__restrict__ Vi,
-                                           int64_t o0, int64_t o1, int64_t vn0, int64_t vn1,
-                                           int64_t g0, int64_t g1, int64_t gidx) {
-    const int64_t o[3] = {o0, o1, 0}, vn[3] = {vn0, vn1, 1}, gi[3] = {g0, g1, 0};
-    return node_update_generic<T, 2>(P, Vi, o, vn, gi, gidx);
-}
-
 // ---------------------------------------------------------------------------
 // generic tiled kernel: tile 32 x 8 x 1, one node per thread
 // ---------------------------------------------------------------------------
@@ -180,7 +176,7 @@ __global__ void __launch_bounds__(256)
     const int64_t lj = (int64_t)tc[1] * 8 + (threadIdx.x >> 5);
     const int64_t lk = tc[2];
     T rmax = T(0);
-    int changed = 0;
+    int changed = 0, evaluated = 0;
     if (li < vn[0] && lj < vn[1] && lk < vn[2]) {
         const int64_t t = li + vn[0] * (lj + vn[1] * lk);
         const int64_t gi[3] = {li + o[0], lj + o[1], lk + o[2]};
@@ -195,12 +191,13 @@ __global__ void __launch_bounds__(256)
         else {
             vnew = node_update_generic<T, DIM>(P, Vi, o, vn, gi, gidx);
             if (P.monotone) vnew = fmin(vnew, vin);
+            evaluated = 1;
         }
         Vo[t] = vnew;
         rmax = vnew > vin ? vnew - vin : vin - vnew;
         changed = !same_bits(vnew, vin);
     }
-    tile_finish(G, v, tile, it, rmax, changed);
+    tile_finish(G, v, tile, it, rmax, changed, evaluated);
 }
 
 // ---------------------------------------------------------------------------
@@ -249,7 +246,7 @@ __global__ void __launch_bounds__(256, 2)
     const int64_t o0 = vw.o[0], o1 = vw.o[1];
     const int64_t n0 = P.n[0], n1 = P.n[1];
     T rmax = T(0);
-    int changed = 0;
+    int changed = 0, evaluated = 0;
 #pragma unroll 1
     for (int r = 0; r < RY; ++r) {
         const int ly = ly0 + r;
@@ -266,9 +263,6 @@ __global__ void __launch_bounds__(256, 2)
             vnew = v_out;
         } else if (c >= 0) {
             vnew = P.g ? P.g[gidx] : T(0);
-        } else if (gi[0] == 0 || gi[1] == 0 || gi[0] == n0 - 1 || gi[1] == n1 - 1) {
-            // on the box edge a foot can leave the box (R3): exact generic bracket
-            vnew = node_update_edge<T>(P, Vi, o0, o1, vn0, vn1, gi[0], gi[1], gidx);
         } else {
             const T Vm0 = sp[-1], Vp0 = sp[1], V0m = sp[-SW], V0p = sp[SW];
             const T Vmm = sp[-SW - 1], Vpm = sp[-SW + 1], Vmp = sp[SW - 1], Vpp = sp[SW + 1];
@@ -283,23 +277,52 @@ __global__ void __launch_bounds__(256, 2)
             }
             const T C0 = fma(P.beta, V00, base);
             const T bs = P.beta * sc, bss = bs * sc;
+            const bool lo_x = gi[0] == 0, hi_x = gi[0] == n0 - 1;
+            const bool lo_y = gi[1] == 0, hi_y = gi[1] == n1 - 1;
             T best = (T)INFINITY;
+            if (!(lo_x | hi_x | lo_y | hi_y)) {
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const T Vx = (q & 1) ? Vm0 : Vp0;
-                const T Vy = (q & 2) ? V0m : V0p;
-                const T Vxy = (q == 0) ? Vpp : (q == 1) ? Vmp : (q == 2) ? Vpm : Vmm;
-                const T Dx = Vx - V00, Dy = Vy - V00, Dxy = (Vxy - Vx) - Dy;
-                const T A1 = bs * Dx, A2 = bs * Dy, A3 = bss * Dxy;
+                for (int q = 0; q < 4; ++q) {
+                    const T Vx = (q & 1) ? Vm0 : Vp0;
+                    const T Vy = (q & 2) ? V0m : V0p;
+                    const T Vxy = (q == 0) ? Vpp : (q == 1) ? Vmp : (q == 2) ? Vpm : Vmm;
+                    const T Dx = Vx - V00, Dy = Vy - V00, Dxy = (Vxy - Vx) - Dy;
+                    const T A1 = bs * Dx, A2 = bs * Dy, A3 = bss * Dxy;
 #pragma unroll
-                for (int k = 0; k < KQ; ++k) {
-                    const T ax = C.ax[q][k], ay = C.ay[q][k];
-                    const T u = fma(ax, A1, PC ? C0 + C.ck[q][k] : C0);
-                    const T cand = fma(ay, fma(ax, A3, A2), u);
-                    best = fmin(best, cand);
+                    for (int k = 0; k < KQ; ++k) {
+                        const T ax = C.ax[q][k], ay = C.ay[q][k];
+                        const T u = fma(ax, A1, PC ? C0 + C.ck[q][k] : C0);
+                        const T cand = fma(ay, fma(ax, A3, A2), u);
+                        best = fmin(best, cand);
+                    }
+                }
+            } else {
+                // box-edge node (R3): a foot moving out by more than BOX_EPS cells reads
+                // v_out; within BOX_EPS it is clamped onto the edge (weight 0)
+                const T c_out = fma(P.beta, v_out, base);
+                const T eps = (T)BOX_EPS;
+#pragma unroll 1
+                for (int q = 0; q < 4; ++q) {
+                    const bool ex = (q & 1) ? lo_x : hi_x, ey = (q & 2) ? lo_y : hi_y;
+                    const T Vx = (q & 1) ? Vm0 : Vp0;
+                    const T Vy = (q & 2) ? V0m : V0p;
+                    const T Vxy = (q == 0) ? Vpp : (q == 1) ? Vmp : (q == 2) ? Vpm : Vmm;
+                    const T Dx = P.beta * (Vx - V00), Dy = P.beta * (Vy - V00);
+                    const T Dxy = P.beta * ((Vxy - Vx) - (Vy - V00));
+#pragma unroll 1
+                    for (int k = 0; k < KQ; ++k) {
+                        T wx = sc * C.ax[q][k], wy = sc * C.ay[q][k];
+                        const T ck = PC ? C.ck[q][k] : T(0);
+                        const bool out = (ex && wx > eps) || (ey && wy > eps);
+                        if (ex) wx = T(0);
+                        if (ey) wy = T(0);
+                        const T in = fma(wy, fma(wx, Dxy, Dy), fma(wx, Dx, C0)) + ck;
+                        best = fmin(best, out ? c_out + ck : in);
+                    }
                 }
             }
             vnew = best;
+            ++evaluated;
         }
         if (c == -1 && P.monotone) vnew = fmin(vnew, V00);
         Vo[t] = vnew;
@@ -307,7 +330,7 @@ __global__ void __launch_bounds__(256, 2)
         rmax = dv > rmax ? dv : rmax;
         changed |= !same_bits(vnew, V00);
     }
-    tile_finish(G, v, tile, it, rmax, changed);
+    tile_finish(G, v, tile, it, rmax, changed, evaluated);
 }
 
 // ---------------------------------------------------------------------------

@@ -55,12 +55,13 @@ class hj_report(ctypes.Structure):
     _fields_ = [("iterations", ctypes.c_int64), ("residual", ctypes.c_double),
                 ("converged", ctypes.c_int32), ("reserved", ctypes.c_int32),
                 ("node_updates", ctypes.c_int64), ("device_ms", ctypes.c_double),
-                ("launches", ctypes.c_int64)]
+                ("launches", ctypes.c_int64), ("evaluated_updates", ctypes.c_int64)]
 
     def as_dict(self):
         return dict(iterations=self.iterations, residual=self.residual,
                     converged=bool(self.converged), node_updates=self.node_updates,
-                    device_ms=self.device_ms, launches=self.launches)
+                    device_ms=self.device_ms, launches=self.launches,
+                    evaluated_updates=self.evaluated_updates)
 
 
 class hj_subdomain(ctypes.Structure):

@@ -23,6 +23,13 @@ def solve_set_for_rank(owners, rank):
     return bits
 
 
+def gather_min(V, group=None):
+    """The method's only collective: element-wise MIN of the ranks' assembled fields
+    (each rank holds v_out where it owns no sub-domain, and every value is <= v_out)."""
+    torch.distributed.all_reduce(V, op=torch.distributed.ReduceOp.MIN, group=group)
+    return V
+
+
 def run_isa(cfg, dtype="f32", device="cuda", rank=0, world=1, group=None, fine=None, coarse=None,
             gather=True):
     """Returns dict(V=assembled fine field (on every rank after the MIN all-reduce when
@@ -43,7 +50,7 @@ def run_isa(cfg, dtype="f32", device="cuda", rank=0, world=1, group=None, fine=N
     Vbar, reps = hj.hj_solve_partitioned(fine, lab["mask"], cfg.m, plan, ws, solve_set=solve_set)
     ev[3].record(s)
     if world > 1 and gather:
-        torch.distributed.all_reduce(Vbar, op=torch.distributed.ReduceOp.MIN, group=group)
+        gather_min(Vbar, group)
     ev[4].record(s)
     torch.cuda.synchronize()
     t["coarse_ms"] = ev[0].elapsed_time(ev[1])

@@ -43,7 +43,7 @@ def test_struct_layouts_match_header(tmp_path):
                        "l0", "lr", "v_out"],
         "hj_fields": ["speed", "piece", "g"],
         "hj_report": ["iterations", "residual", "converged", "node_updates", "device_ms",
-                      "launches"],
+                      "launches", "evaluated_updates"],
         "hj_subdomain": ["lo", "hi", "n_nodes", "box_nodes", "work"],
     }
     cname = {"lam": "lambda"}
