@@ -81,6 +81,16 @@ enum {
  *                        (|x| over the non-periodic axes, |a| over controls[k][0..2]). */
 enum { HJ_COST_KRUZKOV = 0, HJ_COST_DISCOUNTED = 1 };
 
+/* Sweep kernels (all compute the same Jacobi sweep).  AUTO picks, in
+ * order: LOCAL when the problem qualifies (2-D, f = c(x) u_a, every foot within one
+ * cell, no periodic axis) — packed (FFMA2, two nodes per instruction) for fp32,
+ * scalar for fp64; FIELD2D for any other 2-D affine / Van der Pol problem without
+ * periodic axes; DUBINS for Dubins dynamics whose heading step is <= 1 cell; GENERIC
+ * otherwise.  The two LOCAL kernels give bit-identical iterates; the others evaluate
+ * the same bracket in other operation orders (equal up to rounding). */
+enum { HJ_SWEEP_AUTO = 0, HJ_SWEEP_GENERIC = 1, HJ_SWEEP_LOCAL_SCALAR = 2,
+       HJ_SWEEP_LOCAL_PACKED = 3, HJ_SWEEP_FIELD2D = 4, HJ_SWEEP_DUBINS = 5 };
+
 typedef struct {
     int32_t dim;            /* 2 or 3                                          */
     int32_t periodic[3];    /* 1 = periodic axis (e.g. Dubins heading)         */
@@ -92,7 +102,9 @@ typedef struct {
     int32_t dynamics;                        /* HJ_DYN_*                      */
     int32_t cost;                            /* HJ_COST_*                     */
     int32_t n_controls;                      /* 1 .. HJ_MAX_CONTROLS          */
-    int32_t reserved;
+    int32_t sweep_kernel;                    /* HJ_SWEEP_*: 0 = automatic choice;
+                                                an explicit kernel the problem does
+                                                not qualify for -> HJ_ERR_UNSUPPORTED */
     double controls[HJ_MAX_CONTROLS][3];     /* discrete control set A (PAPER.md
                                                 line 248), meaning per dynamics */
     double A[3][3], b[3];                    /* affine drift                  */

@@ -50,6 +50,7 @@ struct SweepGroup {        // device-resident description of one launch
     int n_views;
     int tile_dim[3];       // TX, TY, TZ (nodes)
     int radius[3];         // dependency radius in tiles
+    int halo[3];           // foot bound in cells, ceil(max |delta_d|) (fast-path test)
     int periodic[3];       // periodic axes (views span them fully)
 };
 
@@ -334,16 +335,429 @@ __global__ void __launch_bounds__(256, 2)
 }
 
 // ---------------------------------------------------------------------------
+// local 2-D kernel, fp32, packed: two nodes per FFMA2 (sm_100a fma.rn.f32x2).
+// Same tile, staging and per-node arithmetic as k_sweep_local2d<float> — each
+// node's candidate is fma(ay, fma(ax, A3, A2), fma(ax, A1, C0)) in the same
+// rounding order, so the result is bit-identical — but the rows (ly, ly+1) of a
+// thread share every instruction: lane .x = row ly, lane .y = row ly+1, the
+// control constants broadcast from uniform registers.  Per node x control update:
+// 1.5 FFMA2 + 0.5 FMNMX3 issue slots (vs 3 FFMA + 0.5 FMNMX3 scalar).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
+__device__ __forceinline__ void sincos_t(float a, float *s, float *c) { sincosf(a, s, c); }
+__device__ __forceinline__ void sincos_t(double a, double *s, double *c) { sincos(a, s, c); }
+
+template <bool PC>
+__device__ __forceinline__ float local_edge_node(const DevProblem<float, float> &P,
+                                                 const LocalCtrl<float> &C, int KQ,
+                                                 const float *sp, float C0, float sc,
+                                                 float base, bool lo_x, bool hi_x, bool lo_y,
+                                                 bool hi_y) {
+    constexpr int SW = 34;
+    const float V00 = sp[0], Vm0 = sp[-1], Vp0 = sp[1], V0m = sp[-SW], V0p = sp[SW];
+    const float Vmm = sp[-SW - 1], Vpm = sp[-SW + 1], Vmp = sp[SW - 1], Vpp = sp[SW + 1];
+    const float c_out = fmaf(P.beta, P.v_out, base);
+    const float eps = (float)BOX_EPS;
+    float best = INFINITY;
+#pragma unroll 1
+    for (int q = 0; q < 4; ++q) {
+        const bool ex = (q & 1) ? lo_x : hi_x, ey = (q & 2) ? lo_y : hi_y;
+        const float Vx = (q & 1) ? Vm0 : Vp0;
+        const float Vy = (q & 2) ? V0m : V0p;
+        const float Vxy = (q == 0) ? Vpp : (q == 1) ? Vmp : (q == 2) ? Vpm : Vmm;
+        const float Dx = P.beta * (Vx - V00), Dy = P.beta * (Vy - V00);
+        const float Dxy = P.beta * ((Vxy - Vx) - (Vy - V00));
+#pragma unroll 1
+        for (int k = 0; k < KQ; ++k) {
+            float wx = sc * C.ax[q][k], wy = sc * C.ay[q][k];
+            const float ck = PC ? C.ck[q][k] : 0.f;
+            const bool out = (ex && wx > eps) || (ey && wy > eps);
+            if (ex) wx = 0.f;
+            if (ey) wy = 0.f;
+            const float in = fmaf(wy, fmaf(wx, Dxy, Dy), fmaf(wx, Dx, C0)) + ck;
+            best = fminf(best, out ? c_out + ck : in);
+        }
+    }
+    return best;
+}
+
+template <int KQ, bool PC>
+__global__ void __launch_bounds__(256, 2)
+    k_sweep_local2d_x2(const DevProblem<float, float> P, const LocalCtrl<float> C,
+                       const SweepGroup<float> *__restrict__ G, int64_t it, double tol) {
+    constexpr int TX = 32, TY = 32, RY = 4, SW = TX + 2;
+    __shared__ float s[(TY + 2) * SW];
+    const int64_t b = blockIdx.x;
+    const int v = find_view(G, b);
+    const SweepView<float> &vw = G->v[v];
+    if (it > 0 && *(volatile double *)&vw.res[it - 1] < tol) return;
+    const TileView<float> &tv = G->t[v];
+    const int64_t tile = b - tv.tile_base;
+    const int tc[3] = {(int)(tile % tv.nt[0]), (int)(tile / tv.nt[0]), 0};
+    if (!tile_active(G, v, tc, it)) {
+        if (threadIdx.x == 0) tv.chg[(it & 1) * tv.tiles + tile] = 0;
+        return;
+    }
+    const int64_t vn0 = vw.vn[0], vn1 = vw.vn[1];
+    const float *__restrict__ Vi = vw.V[it & 1];
+    float *__restrict__ Vo = vw.V[(it + 1) & 1];
+    const int64_t x0 = (int64_t)tc[0] * TX, y0 = (int64_t)tc[1] * TY;
+    const float v_out = P.v_out;
+    for (int e = threadIdx.x; e < (TY + 2) * SW; e += 256) {
+        const int r = e / SW, c = e - r * SW;
+        const int64_t li = x0 + c - 1, lj = y0 + r - 1;
+        float val = v_out;
+        if (li >= 0 && lj >= 0 && li < vn0 && lj < vn1) val = Vi[li + vn0 * lj];
+        s[e] = val;
+    }
+    __syncthreads();
+    const int lx = threadIdx.x & 31, ly0 = (threadIdx.x >> 5) * RY;
+    const int64_t o0 = vw.o[0], o1 = vw.o[1];
+    const int64_t n0 = P.n[0], n1 = P.n[1];
+    float rmax = 0.f;
+    int changed = 0, evaluated = 0;
+#pragma unroll 1
+    for (int r = 0; r < RY; r += 2) {
+        // per node of the pair: class, staged neighbourhood, speed, base cost
+        bool valid[2], fast[2], edge[2][4];
+        int8_t c[2];
+        int64_t t[2], gidx[2];
+        float C0[2], A1[4][2], A2[4][2], A3[4][2], sc[2], base[2];
+        const float *sp[2];
+#pragma unroll
+        for (int p = 0; p < 2; ++p) {
+            const int ly = ly0 + r + p;
+            const int64_t li = x0 + lx, lj = y0 + ly;
+            valid[p] = li < vn0 && lj < vn1;
+            t[p] = li + vn0 * lj;
+            const int64_t gi0 = li + o0, gi1 = lj + o1;
+            gidx[p] = gi0 + n0 * gi1;
+            c[p] = valid[p] ? vw.cls[t[p]] : (int8_t)-2;
+            sp[p] = s + (ly + 1) * SW + (lx + 1);
+            edge[p][0] = gi0 == 0;
+            edge[p][1] = gi0 == n0 - 1;
+            edge[p][2] = gi1 == 0;
+            edge[p][3] = gi1 == n1 - 1;
+            const bool interior = valid[p] && c[p] == -1;
+            fast[p] = interior && !(edge[p][0] | edge[p][1] | edge[p][2] | edge[p][3]);
+            sc[p] = (interior && P.speed) ? P.speed[gidx[p]] : 1.f;
+            if (P.cost == HJ_COST_KRUZKOV) {
+                base[p] = P.kcost;
+            } else {
+                const float x[3] = {fmaf((float)gi0, P.dx[0], P.lo[0]),
+                                    fmaf((float)gi1, P.dx[1], P.lo[1]), 0.f};
+                base[p] = P.h * cost_state(P, x);
+            }
+            const float *q0 = sp[p];
+            const float V00 = q0[0];
+            C0[p] = fmaf(P.beta, V00, base[p]);
+            const float bs = P.beta * sc[p], bss = bs * sc[p];
+            const float Vm0 = q0[-1], Vp0 = q0[1], V0m = q0[-SW], V0p = q0[SW];
+            const float Vmm = q0[-SW - 1], Vpm = q0[-SW + 1], Vmp = q0[SW - 1], Vpp = q0[SW + 1];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const float Vx = (q & 1) ? Vm0 : Vp0;
+                const float Vy = (q & 2) ? V0m : V0p;
+                const float Vxy = (q == 0) ? Vpp : (q == 1) ? Vmp : (q == 2) ? Vpm : Vmm;
+                const float Dx = Vx - V00, Dy = Vy - V00, Dxy = (Vxy - Vx) - Dy;
+                A1[q][p] = bs * Dx;
+                A2[q][p] = bs * Dy;
+                A3[q][p] = bss * Dxy;
+            }
+        }
+        float best[2] = {INFINITY, INFINITY};
+        if (fast[0] || fast[1]) {
+            const float2 c0 = f2(C0[0], C0[1]);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const float2 a1 = f2(A1[q][0], A1[q][1]), a2 = f2(A2[q][0], A2[q][1]);
+                const float2 a3 = f2(A3[q][0], A3[q][1]);
+#pragma unroll
+                for (int k = 0; k < KQ; k += 2) {
+                    const float ax0 = C.ax[q][k], ay0 = C.ay[q][k];
+                    const float ax1 = C.ax[q][k + 1], ay1 = C.ay[q][k + 1];
+                    const float2 u0 = __ffma2_rn(
+                        f2(ax0, ax0), a1, PC ? __fadd2_rn(c0, f2(C.ck[q][k], C.ck[q][k])) : c0);
+                    const float2 u1 = __ffma2_rn(
+                        f2(ax1, ax1), a1,
+                        PC ? __fadd2_rn(c0, f2(C.ck[q][k + 1], C.ck[q][k + 1])) : c0);
+                    const float2 w0 = __ffma2_rn(f2(ax0, ax0), a3, a2);
+                    const float2 w1 = __ffma2_rn(f2(ax1, ax1), a3, a2);
+                    const float2 k0 = __ffma2_rn(f2(ay0, ay0), w0, u0);
+                    const float2 k1 = __ffma2_rn(f2(ay1, ay1), w1, u1);
+                    best[0] = fminf(best[0], fminf(k0.x, k1.x));
+                    best[1] = fminf(best[1], fminf(k0.y, k1.y));
+                }
+            }
+        }
+#pragma unroll
+        for (int p = 0; p < 2; ++p) {
+            if (!valid[p]) continue;
+            const float V00 = sp[p][0];
+            float vnew;
+            if (c[p] == -2) {
+                vnew = v_out;
+            } else if (c[p] >= 0) {
+                vnew = P.g ? P.g[gidx[p]] : 0.f;
+            } else {
+                vnew = fast[p] ? best[p]
+                               : local_edge_node<PC>(P, C, KQ, sp[p], C0[p], sc[p], base[p],
+                                                     edge[p][0], edge[p][1], edge[p][2],
+                                                     edge[p][3]);
+                if (P.monotone) vnew = fminf(vnew, V00);
+                ++evaluated;
+            }
+            Vo[t[p]] = vnew;
+            const float dv = vnew > V00 ? vnew - V00 : V00 - vnew;
+            rmax = dv > rmax ? dv : rmax;
+            changed |= !same_bits(vnew, V00);
+        }
+    }
+    tile_finish(G, v, tile, it, rmax, changed, evaluated);
+}
+
+// ---------------------------------------------------------------------------
+// lean 2-D kernel for feet of the form  delta_k(x) = D(x) + S(x) * U_k  (index
+// units), which covers every 2-D family of hj.h:
+//   affine      D = (h/dx) (A x + b),             S = (h/dx) c(x),   U_k = u_k
+//   Van der Pol D = (h/dx) (x1, mu(1-x0^2)x1-x0), S = (0, h/dx1),    U_k = (0, a_k)
+// Any foot distance.  Corners are read through L1 (__ldg: the buffer read is never
+// written in the same launch).  Tiles whose whole footprint (tile +- the host's
+// foot bound) lies inside the view take the fast path: no box/view tests, 32-bit
+// corner offsets; the other tiles use the full R3/R10 rule of interp().
+// Tile 32 x 8, one node per thread.
+// ---------------------------------------------------------------------------
+template <typename T, int DYN>
+__global__ void __launch_bounds__(256)
+    k_sweep_field2d(const DevProblem<T, T> P, const SweepGroup<T> *__restrict__ G, int64_t it,
+                    double tol) {
+    const int64_t b = blockIdx.x;
+    const int v = find_view(G, b);
+    const SweepView<T> &vw = G->v[v];
+    if (it > 0 && *(volatile double *)&vw.res[it - 1] < tol) return;
+    const TileView<T> &tv = G->t[v];
+    const int64_t tile = b - tv.tile_base;
+    const int tc[3] = {(int)(tile % tv.nt[0]), (int)(tile / tv.nt[0]), 0};
+    if (!tile_active(G, v, tc, it)) {
+        if (threadIdx.x == 0) tv.chg[(it & 1) * tv.tiles + tile] = 0;
+        return;
+    }
+    const int vn0 = (int)vw.vn[0], vn1 = (int)vw.vn[1];
+    const T *__restrict__ Vi = vw.V[it & 1];
+    T *__restrict__ Vo = vw.V[(it + 1) & 1];
+    const int li = tc[0] * 32 + (threadIdx.x & 31);
+    const int lj = tc[1] * 8 + (threadIdx.x >> 5);
+    // tile-uniform fast-path test: every corner of every foot inside the view
+    const int hx = G->halo[0], hy = G->halo[1];
+    const bool fast = tc[0] * 32 - hx >= 0 && tc[0] * 32 + 31 + hx + 1 <= vn0 - 1 &&
+                      tc[1] * 8 - hy >= 0 && tc[1] * 8 + 7 + hy + 1 <= vn1 - 1;
+    T rmax = T(0);
+    int changed = 0, evaluated = 0;
+    if (li < vn0 && lj < vn1) {
+        const int64_t t = li + (int64_t)vn0 * lj;
+        const int64_t gi[3] = {li + vw.o[0], lj + vw.o[1], 0};
+        const int64_t gidx = gi[0] + P.n[0] * gi[1];
+        const int8_t c = vw.cls[t];
+        const T vin = Vi[t];
+        T vnew;
+        if (c == -2) {
+            vnew = P.v_out;
+        } else if (c >= 0) {
+            vnew = P.g ? P.g[gidx] : T(0);
+        } else {
+            const T x0 = fma((T)gi[0], P.dx[0], P.lo[0]), x1 = fma((T)gi[1], P.dx[1], P.lo[1]);
+            T D0, D1, S0, S1;
+            if (DYN == HJ_DYN_AFFINE) {
+                const T cs = P.speed ? P.speed[gidx] : T(1);
+                D0 = P.hdx[0] * fma(P.A[0], x0, fma(P.A[1], x1, P.b[0]));
+                D1 = P.hdx[1] * fma(P.A[3], x0, fma(P.A[4], x1, P.b[1]));
+                S0 = P.hdx[0] * cs;
+                S1 = P.hdx[1] * cs;
+            } else {   // Van der Pol
+                D0 = P.hdx[0] * x1;
+                D1 = P.hdx[1] * fma(P.vdp_mu * (T(1) - x0 * x0), x1, -x0);
+                S0 = T(0);
+                S1 = P.hdx[1];
+            }
+            T base;
+            if (P.cost == HJ_COST_KRUZKOV) {
+                base = P.kcost;
+            } else {
+                const T x[3] = {x0, x1, T(0)};
+                base = P.h * cost_state(P, x);
+            }
+            const T hlr = P.h * P.lr;
+            T best = (T)INFINITY;
+            if (fast) {
+                const T *__restrict__ Vn = Vi + t;
+#pragma unroll 4
+                for (int k = 0; k < P.K; ++k) {
+                    // affine: u_k = controls[k][0..1]; Van der Pol: a_k = controls[k][0]
+                    const T d0 = DYN == HJ_DYN_AFFINE ? fma(S0, P.ctrl[k][0], D0) : D0;
+                    const T d1 = fma(S1, P.ctrl[k][DYN == HJ_DYN_AFFINE ? 1 : 0], D1);
+                    const T f0 = floor(d0), f1 = floor(d1);
+                    const T w0 = d0 - f0, w1 = d1 - f1;
+                    const T *__restrict__ p = Vn + ((int)f0 + vn0 * (int)f1);
+                    const T a00 = __ldg(p), a10 = __ldg(p + 1);
+                    const T a01 = __ldg(p + vn0), a11 = __ldg(p + vn0 + 1);
+                    const T I = lerp<T>(lerp<T>(a00, a10, w0), lerp<T>(a01, a11, w0), w1);
+                    const T ck = (P.cost == HJ_COST_KRUZKOV) ? base : fma(hlr, P.csq[k], base);
+                    best = fmin(best, fma(P.beta, I, ck));
+                }
+            } else {
+                const int64_t o[3] = {vw.o[0], vw.o[1], 0};
+                const int64_t vn[3] = {vn0, vn1, 1};
+#pragma unroll 1
+                for (int k = 0; k < P.K; ++k) {
+                    const T delta[3] = {
+                        DYN == HJ_DYN_AFFINE ? fma(S0, P.ctrl[k][0], D0) : D0,
+                        fma(S1, P.ctrl[k][DYN == HJ_DYN_AFFINE ? 1 : 0], D1), T(0)};
+                    const T I = interp<T, T, 2>(Vi, o, vn, P.n, P.periodic, gi, delta, P.v_out);
+                    const T ck = (P.cost == HJ_COST_KRUZKOV) ? base : fma(hlr, P.csq[k], base);
+                    best = fmin(best, fma(P.beta, I, ck));
+                }
+            }
+            vnew = best;
+            if (P.monotone) vnew = fmin(vnew, vin);
+            evaluated = 1;
+        }
+        Vo[t] = vnew;
+        rmax = vnew > vin ? vnew - vin : vin - vnew;
+        changed = !same_bits(vnew, vin);
+    }
+    tile_finish(G, v, tile, it, rmax, changed, evaluated);
+}
+
+// ---------------------------------------------------------------------------
+// Dubins car (§2 dynamics family; BASELINE config 4): the (x,y) part of
+// every foot, h v (cos th, sin th), is the same for all controls of a node and
+// only the heading moves with the control (h w a_k).  When |h w a_k| <= 1 heading
+// cell, the trilinear interpolant at the foot is exactly
+//     I_k = I0 + |d_k| (I_{+-1} - I0),   d_k = h w a_k / dth,
+// with I_{-1}, I0, I_{+1} the bilinear (x,y) interpolants at the foot on the heading
+// planes th-1, th, th+1 (periodic) — so per node 3 bilinear interpolants, then per
+// control 1 select + 2 FMA + 1 min.  Tile 32 x 8 (x, y) on one heading plane.
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void __launch_bounds__(256)
+    k_sweep_dubins(const DevProblem<T, T> P, const SweepGroup<T> *__restrict__ G, int64_t it,
+                   double tol) {
+    const int64_t b = blockIdx.x;
+    const int v = find_view(G, b);
+    const SweepView<T> &vw = G->v[v];
+    if (it > 0 && *(volatile double *)&vw.res[it - 1] < tol) return;
+    const TileView<T> &tv = G->t[v];
+    const int64_t tile = b - tv.tile_base;
+    const int tc[3] = {(int)(tile % tv.nt[0]), (int)((tile / tv.nt[0]) % tv.nt[1]),
+                       (int)(tile / ((int64_t)tv.nt[0] * tv.nt[1]))};
+    if (!tile_active(G, v, tc, it)) {
+        if (threadIdx.x == 0) tv.chg[(it & 1) * tv.tiles + tile] = 0;
+        return;
+    }
+    const int vn0 = (int)vw.vn[0], vn1 = (int)vw.vn[1], vn2 = (int)vw.vn[2];
+    const T *__restrict__ Vi = vw.V[it & 1];
+    T *__restrict__ Vo = vw.V[(it + 1) & 1];
+    const int li = tc[0] * 32 + (threadIdx.x & 31);
+    const int lj = tc[1] * 8 + (threadIdx.x >> 5);
+    const int lk = tc[2];
+    T rmax = T(0);
+    int changed = 0, evaluated = 0;
+    if (li < vn0 && lj < vn1) {
+        const int64_t plane = (int64_t)vn0 * vn1;
+        const int64_t t = li + (int64_t)vn0 * lj + plane * lk;
+        const int64_t gi0 = li + vw.o[0], gi1 = lj + vw.o[1], gi2 = lk + vw.o[2];
+        const int64_t gidx = gi0 + P.n[0] * (gi1 + P.n[1] * gi2);
+        const int8_t c = vw.cls[t];
+        const T vin = Vi[t];
+        T vnew;
+        if (c == -2) {
+            vnew = P.v_out;
+        } else if (c >= 0) {
+            vnew = P.g ? P.g[gidx] : T(0);
+        } else {
+            const T th = fma((T)gi2, P.dx[2], P.lo[2]);
+            T sn, cn;
+            sincos_t(th, &sn, &cn);
+            const T d0 = P.hdx[0] * (P.dub_v * cn), d1 = P.hdx[1] * (P.dub_v * sn);
+            const T kc = P.kcost;
+            T best = (T)INFINITY;
+            // (x, y) part of the foot: box rule R3 on the global grid
+            const T lo0 = -(T)gi0, hi0 = (T)(P.n[0] - 1 - gi0);
+            const T lo1 = -(T)gi1, hi1 = (T)(P.n[1] - 1 - gi1);
+            const T eps = (T)BOX_EPS;
+            const bool inside = d0 >= lo0 - eps && d0 <= hi0 + eps && d1 >= lo1 - eps &&
+                                d1 <= hi1 + eps;
+            T base = kc;
+            if (P.cost != HJ_COST_KRUZKOV) {
+                const T x[3] = {fma((T)gi0, P.dx[0], P.lo[0]), fma((T)gi1, P.dx[1], P.lo[1]), th};
+                base = P.h * cost_state(P, x);
+            }
+            const T hlr = P.h * P.lr;
+            if (!inside) {
+                for (int k = 0; k < P.K; ++k) {
+                    const T ck = (P.cost == HJ_COST_KRUZKOV) ? base : fma(hlr, P.csq[k], base);
+                    best = fmin(best, fma(P.beta, P.v_out, ck));
+                }
+            } else {
+                T x = d0 < lo0 ? lo0 : (d0 > hi0 ? hi0 : d0);
+                T y = d1 < lo1 ? lo1 : (d1 > hi1 ? hi1 : d1);
+                T fx = floor(x), fy = floor(y);
+                int64_t cx = gi0 + (int64_t)fx, cy = gi1 + (int64_t)fy;
+                T wx = x - fx, wy = y - fy;
+                if (cx > P.n[0] - 2) { cx = P.n[0] - 2; wx = T(1); }
+                if (cy > P.n[1] - 2) { cy = P.n[1] - 2; wy = T(1); }
+                // view-local corners; outside the view: ghost v_out (R10)
+                const int64_t ax = cx - vw.o[0], ay = cy - vw.o[1];
+                const T vo = P.v_out;
+                T I3[3];
+#pragma unroll
+                for (int s = 0; s < 3; ++s) {
+                    int64_t kk = lk + s - 1;        // views span the periodic heading axis
+                    if (kk < 0) kk += vn2;
+                    if (kk >= vn2) kk -= vn2;
+                    const T *pl = Vi + plane * kk;
+                    auto at = [&](int64_t i, int64_t j) -> T {
+                        return (i >= 0 && j >= 0 && i < vn0 && j < vn1) ? __ldg(pl + i + vn0 * j)
+                                                                        : vo;
+                    };
+                    const T a = lerp<T>(at(ax, ay), at(ax + 1, ay), wx);
+                    const T bb = lerp<T>(at(ax, ay + 1), at(ax + 1, ay + 1), wx);
+                    I3[s] = lerp<T>(a, bb, wy);
+                }
+                const T dM = I3[0] - I3[1], dP = I3[2] - I3[1];
+                const T hw = P.hdx[2] * P.dub_w;
+#pragma unroll 4
+                for (int k = 0; k < P.K; ++k) {
+                    const T dk = hw * P.ctrl[k][0];
+                    const T I = fma(fabs(dk), dk < T(0) ? dM : dP, I3[1]);
+                    const T ck = (P.cost == HJ_COST_KRUZKOV) ? base : fma(hlr, P.csq[k], base);
+                    best = fmin(best, fma(P.beta, I, ck));
+                }
+            }
+            vnew = best;
+            if (P.monotone) vnew = fmin(vnew, vin);
+            evaluated = 1;
+        }
+        Vo[t] = vnew;
+        rmax = vnew > vin ? vnew - vin : vin - vnew;
+        changed = !same_bits(vnew, vin);
+    }
+    tile_finish(G, v, tile, it, rmax, changed, evaluated);
+}
+
+// ---------------------------------------------------------------------------
 // host side: choose the kernel, tile the views, launch
 // ---------------------------------------------------------------------------
-enum SweepKind { SWEEP_GENERIC = 0, SWEEP_LOCAL2D = 1 };
+enum SweepKind { SWEEP_GENERIC = 0, SWEEP_LOCAL2D = 1, SWEEP_FIELD2D = 2, SWEEP_DUBINS = 3 };
 
 template <typename T>
 struct SweepLaunch {
     int kind = SWEEP_GENERIC;
     int dim = 2;
+    int dyn = HJ_DYN_AFFINE;
     int kq = 0;
     bool per_ctrl_cost = false;
+    bool packed = false;                // fp32 local kernel on FFMA2 (k_sweep_local2d_x2)
     int64_t total_tiles = 0;
     SweepGroup<T> *d_group = nullptr;   // device copy (inside the caller's workspace)
     LocalCtrl<T> ctrl;
@@ -401,8 +815,19 @@ hj_status sweep_prepare(const hj_grid &g, const hj_problem &p, const hj_fields &
         for (int e = 0; e < 3; ++e)
             if (p.A[d][e] != 0) iso = false;
     }
+    const int want = p.sweep_kernel;
+    if (want < HJ_SWEEP_AUTO || want > HJ_SWEEP_DUBINS) {
+        set_error("unknown sweep_kernel %d", want);
+        return HJ_ERR_INVALID;
+    }
+    if (want == HJ_SWEEP_LOCAL_PACKED && sizeof(T) != 4) {
+        set_error("HJ_SWEEP_LOCAL_PACKED is an fp32 kernel");
+        return HJ_ERR_UNSUPPORTED;
+    }
     const bool local = iso && H[0] <= 1 + 1e-6 && H[1] <= 1 + 1e-6 && !g.periodic[0] &&
-                       !g.periodic[1];
+                       !g.periodic[1] &&
+                       (want == HJ_SWEEP_AUTO || want == HJ_SWEEP_LOCAL_SCALAR ||
+                        want == HJ_SWEEP_LOCAL_PACKED);
     L.kind = SWEEP_GENERIC;
     int tile_dim[3] = {32, 8, 1};
     if (local) {
@@ -440,6 +865,7 @@ hj_status sweep_prepare(const hj_grid &g, const hj_problem &p, const hj_fields &
         if (kq) {
             L.kind = SWEEP_LOCAL2D;
             L.kq = kq;
+            L.packed = sizeof(T) == 4 && want != HJ_SWEEP_LOCAL_SCALAR;
             L.per_ctrl_cost = p.cost == HJ_COST_DISCOUNTED && p.lr != 0;
             memset(&L.ctrl, 0, sizeof(L.ctrl));
             for (int q = 0; q < 4; ++q) {
@@ -467,6 +893,27 @@ hj_status sweep_prepare(const hj_grid &g, const hj_problem &p, const hj_fields &
             tile_dim[1] = 32;
         }
     }
+    if (L.kind == SWEEP_GENERIC && want != HJ_SWEEP_GENERIC && want != HJ_SWEEP_LOCAL_SCALAR &&
+        want != HJ_SWEEP_LOCAL_PACKED) {
+        if (g.dim == 2 && (p.dynamics == HJ_DYN_AFFINE || p.dynamics == HJ_DYN_VANDERPOL) &&
+            !g.periodic[0] && !g.periodic[1] && (want == HJ_SWEEP_AUTO || want == HJ_SWEEP_FIELD2D))
+            L.kind = SWEEP_FIELD2D;
+        else if (p.dynamics == HJ_DYN_DUBINS && H[2] <= 1.0 && !g.periodic[0] && !g.periodic[1] &&
+                 (want == HJ_SWEEP_AUTO || want == HJ_SWEEP_DUBINS))
+            L.kind = SWEEP_DUBINS;
+    }
+    L.dyn = p.dynamics;
+    if ((want == HJ_SWEEP_FIELD2D && L.kind != SWEEP_FIELD2D) ||
+        (want == HJ_SWEEP_DUBINS && L.kind != SWEEP_DUBINS)) {
+        set_error("sweep_kernel %d requested, but the problem does not qualify for it", want);
+        return HJ_ERR_UNSUPPORTED;
+    }
+    if ((want == HJ_SWEEP_LOCAL_SCALAR || want == HJ_SWEEP_LOCAL_PACKED) &&
+        L.kind != SWEEP_LOCAL2D) {
+        set_error("sweep_kernel %d requested, but the problem does not qualify for the local "
+                  "kernel (2-D, f = c(x) u_a, foot within one cell, no periodic axis)", want);
+        return HJ_ERR_UNSUPPORTED;
+    }
     SweepGroup<T> hg;
     memset(&hg, 0, sizeof(hg));
     hg.n_views = (int)views.size();
@@ -477,6 +924,7 @@ hj_status sweep_prepare(const hj_grid &g, const hj_problem &p, const hj_fields &
     }
     for (int d = 0; d < 3; ++d) {
         hg.radius[d] = d < g.dim ? (int)std::ceil((H[d] + 1.0) / tile_dim[d]) : 0;
+        hg.halo[d] = d < g.dim ? (int)std::ceil(H[d] * (1.0 + 1e-6) + 1e-6) : 0;
         if (L.kind == SWEEP_LOCAL2D) hg.radius[d] = d < 2 ? 1 : 0;
     }
     for (size_t q = 0; q < views.size(); ++q) {
@@ -505,9 +953,26 @@ hj_status sweep_prepare(const hj_grid &g, const hj_problem &p, const hj_fields &
     return HJ_OK;
 }
 
+template <bool PC>
+static void launch_local_x2(const DevProblem<float, float> &P, const SweepLaunch<float> &L,
+                            int64_t it, double tol, cudaStream_t s) {
+    dim3 grid((unsigned)L.total_tiles);
+    switch (L.kq) {
+        case 4: k_sweep_local2d_x2<4, PC><<<grid, 256, 0, s>>>(P, L.ctrl, L.d_group, it, tol); break;
+        case 8: k_sweep_local2d_x2<8, PC><<<grid, 256, 0, s>>>(P, L.ctrl, L.d_group, it, tol); break;
+        case 12: k_sweep_local2d_x2<12, PC><<<grid, 256, 0, s>>>(P, L.ctrl, L.d_group, it, tol); break;
+        case 16: k_sweep_local2d_x2<16, PC><<<grid, 256, 0, s>>>(P, L.ctrl, L.d_group, it, tol); break;
+        case 24: k_sweep_local2d_x2<24, PC><<<grid, 256, 0, s>>>(P, L.ctrl, L.d_group, it, tol); break;
+        default: k_sweep_local2d_x2<32, PC><<<grid, 256, 0, s>>>(P, L.ctrl, L.d_group, it, tol); break;
+    }
+}
+
 template <typename T, bool PC>
 static void launch_local(const DevProblem<T, T> &P, const SweepLaunch<T> &L, int64_t it,
                          double tol, cudaStream_t s) {
+    if constexpr (sizeof(T) == 4) {
+        if (L.packed) return launch_local_x2<PC>(P, L, it, tol, s);
+    }
     dim3 grid((unsigned)L.total_tiles);
     switch (L.kq) {
         case 4: k_sweep_local2d<T, 4, PC><<<grid, 256, 0, s>>>(P, L.ctrl, L.d_group, it, tol); break;
@@ -528,6 +993,13 @@ hj_status sweep_launch(const DevProblem<T, T> &P, const SweepLaunch<T> &L, int64
             launch_local<T, true>(P, L, it, tol, s);
         else
             launch_local<T, false>(P, L, it, tol, s);
+    } else if (L.kind == SWEEP_FIELD2D) {
+        if (L.dyn == HJ_DYN_AFFINE)
+            k_sweep_field2d<T, HJ_DYN_AFFINE><<<(unsigned)L.total_tiles, 256, 0, s>>>(P, L.d_group, it, tol);
+        else
+            k_sweep_field2d<T, HJ_DYN_VANDERPOL><<<(unsigned)L.total_tiles, 256, 0, s>>>(P, L.d_group, it, tol);
+    } else if (L.kind == SWEEP_DUBINS) {
+        k_sweep_dubins<T><<<(unsigned)L.total_tiles, 256, 0, s>>>(P, L.d_group, it, tol);
     } else if (L.dim == 2) {
         k_sweep_generic<T, 2><<<(unsigned)L.total_tiles, 256, 0, s>>>(P, L.d_group, it, tol);
     } else {

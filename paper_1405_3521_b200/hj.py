@@ -38,7 +38,7 @@ class hj_grid(ctypes.Structure):
 
 class hj_problem(ctypes.Structure):
     _fields_ = [("dynamics", ctypes.c_int32), ("cost", ctypes.c_int32),
-                ("n_controls", ctypes.c_int32), ("reserved", ctypes.c_int32),
+                ("n_controls", ctypes.c_int32), ("sweep_kernel", ctypes.c_int32),
                 ("controls", (ctypes.c_double * 3) * MAX_CONTROLS),
                 ("A", (ctypes.c_double * 3) * 3), ("b", ctypes.c_double * 3),
                 ("dubins_v", ctypes.c_double), ("dubins_w", ctypes.c_double),
@@ -73,6 +73,11 @@ class hj_subdomain(ctypes.Structure):
 EXPORTS = ["hj_last_error", "hj_version", "hj_solve_workspace_bytes", "hj_solve",
            "hj_coarse_feedback", "hj_label_subdomains", "hj_partition_plan",
            "hj_assign_subdomains", "hj_solve_partitioned"]
+
+
+# hj.h HJ_SWEEP_*
+SWEEP_KERNELS = {"auto": 0, "generic": 1, "local_scalar": 2, "local_packed": 3, "field2d": 4,
+                 "dubins": 5}
 
 
 def lib():
@@ -159,11 +164,13 @@ def make_problem(prob) -> hj_problem:
 class DeviceProblem:
     """hj_grid / hj_problem structs plus the problem's node fields on the device."""
 
-    def __init__(self, prob, dtype="f32", device="cuda", piece=None, speed=None, g=None):
+    def __init__(self, prob, dtype="f32", device="cuda", piece=None, speed=None, g=None,
+                 sweep_kernel="auto"):
         self.prob = prob
         self.dtype = dtype
         self.grid = make_grid(prob.grid)
         self.cprob = make_problem(prob)
+        self.cprob.sweep_kernel = SWEEP_KERNELS[sweep_kernel]
         td = _torch_dtype(dtype)
         self.piece = piece if piece is not None else torch.as_tensor(
             np.ascontiguousarray(prob.piece, np.int8)).to(device)

@@ -70,6 +70,48 @@ def test_solve_matches_oracle(idx, dtype, oracle_cache):
         assert abs(rep["iterations"] - it_o) <= max(2, it_o // 10)   # fp32 residual noise
 
 
+KERNELS = {1: ("generic", "field2d", "local_scalar", "local_packed"),
+           2: ("generic", "field2d", "local_scalar", "local_packed"),
+           3: ("generic", "field2d"), 4: ("generic", "dubins"), 5: ("generic", "field2d")}
+
+
+@pytest.mark.parametrize("idx", [1, 2, 3, 4, 5])
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+def test_sweep_kernels_match_oracle(idx, dtype, oracle_cache):
+    """Every sweep kernel (hj.h HJ_SWEEP_*) the config qualifies for, against the oracle;
+    the scalar and the packed (FFMA2) local kernels evaluate each node in the same
+    operation order and must agree bit for bit, iteration count included."""
+    cfg = _cfg(idx)
+    Vo, it_o, _ = _oracle_solve(oracle_cache, idx)
+    tol = cfg.fine.tol if dtype == "f64" else max(cfg.fine.tol, 1e-7)
+    out = {}
+    for kernel in KERNELS[idx]:
+        if kernel == "local_packed" and dtype == "f64":
+            with pytest.raises(hj.HJError):      # the packed kernel is fp32-only
+                hj.hj_solve(hj.DeviceProblem(cfg.fine, dtype, sweep_kernel=kernel), tol=tol)
+            continue
+        dp = hj.DeviceProblem(cfg.fine, dtype, sweep_kernel=kernel)
+        V, rep = hj.hj_solve(dp, tol=tol)
+        err = np.abs(V.double().cpu().numpy() - Vo).max()
+        assert err <= TOL[dtype], (kernel, err)
+        if dtype == "f64":
+            assert rep["iterations"] == it_o, (kernel, rep["iterations"], it_o)
+        out[kernel] = (V.cpu(), rep["iterations"])
+    if "local_packed" in out:
+        assert torch.equal(out["local_scalar"][0], out["local_packed"][0])
+        assert out["local_scalar"][1] == out["local_packed"][1]
+
+
+def test_local_kernel_refuses_nonlocal_problem():
+    cfg = _cfg(3)                        # Zermelo drift: feet leave the 3x3 cell block
+    with pytest.raises(hj.HJError, match="does not qualify"):
+        hj.hj_solve(hj.DeviceProblem(cfg.fine, "f32", sweep_kernel="local_packed"))
+    with pytest.raises(hj.HJError, match="does not qualify"):
+        hj.hj_solve(hj.DeviceProblem(cfg.fine, "f32", sweep_kernel="dubins"))
+    with pytest.raises(hj.HJError, match="does not qualify"):
+        hj.hj_solve(hj.DeviceProblem(_cfg(4).fine, "f32", sweep_kernel="field2d"))
+
+
 @pytest.mark.parametrize("idx", [1, 2, 4, 5])
 def test_feedback_bitexact(idx, oracle_cache):
     cfg = _cfg(idx)
