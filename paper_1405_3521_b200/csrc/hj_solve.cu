@@ -177,15 +177,22 @@ struct IterResult {
     std::vector<int64_t> iters;
     std::vector<double> resid;
     std::vector<int> converged;
+    std::vector<int> buf;          // V[buf] holds the final iterate of each view
     float ms = 0.f;
     int64_t launches = 0;
 };
 
+// Sweeps are launched in batches (L.tb sweeps per launch for the temporally blocked
+// kernel, 1 otherwise) and the residuals read back one batch behind; each view
+// stops at its own first n with res[n-1] < tol.  With L.tb > 1 a view whose stop
+// falls inside a block re-runs that block from its intact input with the exact
+// number of sub-sweeps, so the final iterate is V^{n*} bit for bit.
 template <typename T>
-static hj_status iterate(const DevProblem<T, T> &P, const SweepLaunch<T> &L, int nv,
+static hj_status iterate(const DevProblem<T, T> &P, SweepLaunch<T> &L, int nv,
                          double *res_base, int64_t res_stride, double tol, int64_t max_iter,
                          cudaStream_t s, IterResult &out) {
-    const int B = 16;
+    const int S = std::max(1, L.tb);
+    const int64_t B = S > 1 ? 4 * S : 16;          // sweeps per read-back batch
     double *pin = pinned_scratch((size_t)2 * nv * B);
     HJ_CHECK(pin != nullptr, "cudaMallocHost failed for the residual staging buffer");
     cudaEvent_t ev[2], t0, t1;
@@ -195,6 +202,7 @@ static hj_status iterate(const DevProblem<T, T> &P, const SweepLaunch<T> &L, int
     out.iters.assign(nv, max_iter);
     out.resid.assign(nv, INFINITY);
     out.converged.assign(nv, 0);
+    out.buf.assign(nv, 0);
     int n_done = 0;
 
     struct Batch {
@@ -208,8 +216,9 @@ static hj_status iterate(const DevProblem<T, T> &P, const SweepLaunch<T> &L, int
     while (true) {
         while (inflight.size() < 2 && next < max_iter && n_done < nv) {
             int64_t cnt = std::min<int64_t>(B, max_iter - next);
-            for (int64_t it = next; it < next + cnt; ++it) {
-                hj_status st = sweep_launch(P, L, it, tol, s);
+            for (int64_t it = next; it < next + cnt; it += S) {
+                hj_status st =
+                    sweep_launch(P, L, it, tol, s, (int)std::min<int64_t>(S, next + cnt - it));
                 if (st != HJ_OK) return st;
                 ++out.launches;
             }
@@ -240,6 +249,37 @@ static hj_status iterate(const DevProblem<T, T> &P, const SweepLaunch<T> &L, int
             }
         }
         if (n_done == nv) break;
+    }
+    // drain: batches still in flight only contain launches that exit at once
+    for (int v = 0; v < nv; ++v) {
+        const int64_t n = out.iters[v];
+        const int64_t blk = (n - 1) / S;
+        out.buf[v] = (int)((blk + 1) & 1);
+    }
+    if (S > 1) {
+        // re-run the blocks that contain a stop (grouped by block)
+        std::vector<int64_t> blocks;
+        for (int v = 0; v < nv; ++v) {
+            const int64_t n = out.iters[v], blk = (n - 1) / S;
+            if (out.converged[v] && n - blk * S < S) blocks.push_back(blk);
+        }
+        std::sort(blocks.begin(), blocks.end());
+        blocks.erase(std::unique(blocks.begin(), blocks.end()), blocks.end());
+        for (int64_t blk : blocks) {
+            std::vector<int32_t> rr(nv, 0);
+            for (int v = 0; v < nv; ++v) {
+                const int64_t n = out.iters[v];
+                if (out.converged[v] && (n - 1) / S == blk && n - blk * S < S)
+                    rr[v] = (int32_t)(n - blk * S);
+            }
+            for (int v = 0; v < nv; ++v)
+                HJ_CUDA(cudaMemcpyAsync(&L.d_group->t[v].rerun, &rr[v], sizeof(int32_t),
+                                        cudaMemcpyHostToDevice, s));
+            hj_status st = sweep_launch_rerun(P, L, blk * S, tol, s);
+            if (st != HJ_OK) return st;
+            ++out.launches;
+            HJ_CUDA(cudaStreamSynchronize(s));      // rr must outlive the copies
+        }
     }
     HJ_CUDA(cudaEventRecord(t1, s));
     HJ_CUDA(cudaStreamSynchronize(s));
@@ -318,7 +358,7 @@ static hj_status solve_impl(const hj_grid &grid, const hj_problem &prob, const h
     st = iterate<T>(P, L, 1, res, 0, tol, max_iter, s, r);
     if (st != HJ_OK) return st;
     int64_t it = r.iters[0];
-    if (it & 1) HJ_CUDA(cudaMemcpyAsync(V, V1, N * sizeof(T), cudaMemcpyDeviceToDevice, s));
+    if (r.buf[0]) HJ_CUDA(cudaMemcpyAsync(V, V1, N * sizeof(T), cudaMemcpyDeviceToDevice, s));
     unsigned long long counts[2] = {0, 0};
     HJ_CUDA(cudaMemcpyAsync(counts, cnt, sizeof(counts), cudaMemcpyDeviceToHost, s));
     HJ_CUDA(cudaStreamSynchronize(s));
@@ -459,7 +499,7 @@ static hj_status partitioned_impl(const hj_grid &grid, const hj_problem &prob,
             ha[q].o[d] = hv[q].o[d];
             ha[q].vn[d] = hv[q].vn[d];
         }
-        ha[q].V = hv[q].V[r.iters[q] & 1];
+        ha[q].V = hv[q].V[r.buf[q]];
         ha[q].sub = subs[q];
     }
     HJ_CUDA(cudaMemcpyAsync(d_asm, ha.data(), nv * sizeof(AsmView<T>), cudaMemcpyHostToDevice, s));
@@ -495,6 +535,13 @@ static hj_status partitioned_impl(const hj_grid &grid, const hj_problem &prob,
 using namespace hj;
 
 extern "C" {
+
+/* Profiling aid (not part of the documented ABI surface): per-CTA trace of the
+ * temporally blocked sweep into a device buffer of 4 * cap uint64; NULL disables. */
+int hj_debug_set_trace(void *dev_buf, long long cap, long long n0) {
+    TBTrace t{(unsigned long long *)dev_buf, dev_buf ? cap : 0, n0};
+    return cudaMemcpyToSymbol(g_tb_trace, &t, sizeof(t)) == cudaSuccess ? 0 : 1;
+}
 
 size_t hj_solve_workspace_bytes(const hj_grid *grid, int32_t dtype, int64_t max_iter) {
     if (!grid || validate_grid(grid) != HJ_OK || max_iter < 1) return 0;

@@ -40,7 +40,8 @@ struct TileView {          // per-view tiling, filled by sweep_prepare
     int32_t nt[3];         // tiles per axis
     int64_t tiles;         // nt0*nt1*nt2
     int64_t tile_base;     // first global tile index of this view
-    uint8_t *chg;          // [2][tiles] changed flags (parity of the sweep)
+    uint8_t *chg;          // [2][tiles] changed flags (parity of the sweep / block)
+    int32_t rerun;         // temporally blocked kernel: sub-sweeps of the stop re-run
 };
 
 template <typename T>
@@ -210,6 +211,10 @@ struct LocalCtrl {
     // ax = |u_x| h/dx, ay = |u_y| h/dy of the controls of that quadrant (padded to KQ
     // by repeating a control: repeats do not change a min); ck = per-control cost.
     T ax[4][32], ay[4][32], ck[4][32];
+    // box of each quadrant's weights, [0, xmax] x [0, ymax] (exact pruning bound of
+    // the temporally blocked kernel) and whether pruning is valid
+    T xmax[4], ymax[4];
+    int prune_ok;         // every ck >= 0
 };
 
 template <typename T, int KQ, bool PC>
@@ -745,6 +750,10 @@ __global__ void __launch_bounds__(256)
     tile_finish(G, v, tile, it, rmax, changed, evaluated);
 }
 
+}  // namespace hj
+#include "hj_sweep_tb.cuh"
+namespace hj {
+
 // ---------------------------------------------------------------------------
 // host side: choose the kernel, tile the views, launch
 // ---------------------------------------------------------------------------
@@ -758,6 +767,7 @@ struct SweepLaunch {
     int kq = 0;
     bool per_ctrl_cost = false;
     bool packed = false;                // fp32 local kernel on FFMA2 (k_sweep_local2d_x2)
+    int tb = 1;                         // sweeps per launch (> 1: k_sweep_local2d_tb)
     int64_t total_tiles = 0;
     SweepGroup<T> *d_group = nullptr;   // device copy (inside the caller's workspace)
     LocalCtrl<T> ctrl;
@@ -816,7 +826,7 @@ hj_status sweep_prepare(const hj_grid &g, const hj_problem &p, const hj_fields &
             if (p.A[d][e] != 0) iso = false;
     }
     const int want = p.sweep_kernel;
-    if (want < HJ_SWEEP_AUTO || want > HJ_SWEEP_DUBINS) {
+    if (want < HJ_SWEEP_AUTO || want > HJ_SWEEP_LOCAL_TB) {
         set_error("unknown sweep_kernel %d", want);
         return HJ_ERR_INVALID;
     }
@@ -827,7 +837,7 @@ hj_status sweep_prepare(const hj_grid &g, const hj_problem &p, const hj_fields &
     const bool local = iso && H[0] <= 1 + 1e-6 && H[1] <= 1 + 1e-6 && !g.periodic[0] &&
                        !g.periodic[1] &&
                        (want == HJ_SWEEP_AUTO || want == HJ_SWEEP_LOCAL_SCALAR ||
-                        want == HJ_SWEEP_LOCAL_PACKED);
+                        want == HJ_SWEEP_LOCAL_PACKED || want == HJ_SWEEP_LOCAL_TB);
     L.kind = SWEEP_GENERIC;
     int tile_dim[3] = {32, 8, 1};
     if (local) {
@@ -866,6 +876,10 @@ hj_status sweep_prepare(const hj_grid &g, const hj_problem &p, const hj_fields &
             L.kind = SWEEP_LOCAL2D;
             L.kq = kq;
             L.packed = sizeof(T) == 4 && want != HJ_SWEEP_LOCAL_SCALAR;
+            if (want == HJ_SWEEP_AUTO || want == HJ_SWEEP_LOCAL_TB) {
+                L.tb = TB_SMAX;
+                tile_dim[0] = tile_dim[1] = TB_T;
+            }
             L.per_ctrl_cost = p.cost == HJ_COST_DISCOUNTED && p.lr != 0;
             memset(&L.ctrl, 0, sizeof(L.ctrl));
             for (int q = 0; q < 4; ++q) {
@@ -889,12 +903,23 @@ hj_status sweep_prepare(const hj_grid &g, const hj_problem &p, const hj_fields &
                 }
                 if (lst.empty()) L.per_ctrl_cost = true;   // the +inf padding needs ck
             }
+            L.ctrl.prune_ok = 1;
+            for (int q = 0; q < 4; ++q) {
+                double xm = 0, ym = 0;
+                for (int j = 0; j < kq; ++j) {
+                    xm = std::max(xm, (double)L.ctrl.ax[q][j]);
+                    ym = std::max(ym, (double)L.ctrl.ay[q][j]);
+                    if (!(L.ctrl.ck[q][j] >= 0)) L.ctrl.prune_ok = 0;
+                }
+                L.ctrl.xmax[q] = (T)xm;
+                L.ctrl.ymax[q] = (T)ym;
+            }
             tile_dim[0] = 32;
             tile_dim[1] = 32;
         }
     }
     if (L.kind == SWEEP_GENERIC && want != HJ_SWEEP_GENERIC && want != HJ_SWEEP_LOCAL_SCALAR &&
-        want != HJ_SWEEP_LOCAL_PACKED) {
+        want != HJ_SWEEP_LOCAL_PACKED && want != HJ_SWEEP_LOCAL_TB) {
         if (g.dim == 2 && (p.dynamics == HJ_DYN_AFFINE || p.dynamics == HJ_DYN_VANDERPOL) &&
             !g.periodic[0] && !g.periodic[1] && (want == HJ_SWEEP_AUTO || want == HJ_SWEEP_FIELD2D))
             L.kind = SWEEP_FIELD2D;
@@ -908,8 +933,8 @@ hj_status sweep_prepare(const hj_grid &g, const hj_problem &p, const hj_fields &
         set_error("sweep_kernel %d requested, but the problem does not qualify for it", want);
         return HJ_ERR_UNSUPPORTED;
     }
-    if ((want == HJ_SWEEP_LOCAL_SCALAR || want == HJ_SWEEP_LOCAL_PACKED) &&
-        L.kind != SWEEP_LOCAL2D) {
+    if ((want == HJ_SWEEP_LOCAL_SCALAR || want == HJ_SWEEP_LOCAL_PACKED ||
+         want == HJ_SWEEP_LOCAL_TB) && L.kind != SWEEP_LOCAL2D) {
         set_error("sweep_kernel %d requested, but the problem does not qualify for the local "
                   "kernel (2-D, f = c(x) u_a, foot within one cell, no periodic axis)", want);
         return HJ_ERR_UNSUPPORTED;
@@ -984,11 +1009,63 @@ static void launch_local(const DevProblem<T, T> &P, const SweepLaunch<T> &L, int
     }
 }
 
+template <typename T, int KQ, bool PC>
+static void launch_tb_kq(const DevProblem<T, T> &P, const SweepLaunch<T> &L, int64_t n0, int S_run,
+                         int rerun, double tol, cudaStream_t s) {
+    static bool attr = false;   // opt in to > 48 KB dynamic shared memory (fp64) once
+    const size_t smem = sizeof(TBSmem<T>);
+    if (!attr) {
+        cudaFuncSetAttribute(k_sweep_local2d_tb<T, KQ, PC>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr = true;
+    }
+    k_sweep_local2d_tb<T, KQ, PC><<<(unsigned)L.total_tiles, 256, smem, s>>>(
+        P, L.ctrl, L.d_group, n0, L.tb, S_run, rerun, tol);
+}
+
+template <typename T, bool PC>
+static void launch_tb(const DevProblem<T, T> &P, const SweepLaunch<T> &L, int64_t n0, int S_run,
+                      int rerun, double tol, cudaStream_t s) {
+    switch (L.kq) {
+        case 4: launch_tb_kq<T, 4, PC>(P, L, n0, S_run, rerun, tol, s); break;
+        case 8: launch_tb_kq<T, 8, PC>(P, L, n0, S_run, rerun, tol, s); break;
+        case 12: launch_tb_kq<T, 12, PC>(P, L, n0, S_run, rerun, tol, s); break;
+        case 16: launch_tb_kq<T, 16, PC>(P, L, n0, S_run, rerun, tol, s); break;
+        case 24: launch_tb_kq<T, 24, PC>(P, L, n0, S_run, rerun, tol, s); break;
+        default: launch_tb_kq<T, 32, PC>(P, L, n0, S_run, rerun, tol, s); break;
+    }
+}
+
+// Re-run of the block holding the stop (temporally blocked kernel only): every view
+// whose TileView::rerun > 0 recomputes that many sub-sweeps of block n0 / L.tb.
+template <typename T>
+hj_status sweep_launch_rerun(const DevProblem<T, T> &P, const SweepLaunch<T> &L, int64_t n0,
+                             double tol, cudaStream_t s) {
+    if (L.total_tiles == 0) return HJ_OK;
+    if (L.per_ctrl_cost)
+        launch_tb<T, true>(P, L, n0, 0, 1, tol, s);
+    else
+        launch_tb<T, false>(P, L, n0, 0, 1, tol, s);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        set_error("sweep re-run launch failed: %s", cudaGetErrorString(e));
+        return HJ_ERR_CUDA;
+    }
+    return HJ_OK;
+}
+
+// One launch: sweep `it` (L.tb == 1) or the block of L.tb sweeps starting at `it`.
 template <typename T>
 hj_status sweep_launch(const DevProblem<T, T> &P, const SweepLaunch<T> &L, int64_t it, double tol,
-                       cudaStream_t s) {
+                       cudaStream_t s, int S_run = 0) {
     if (L.total_tiles == 0) return HJ_OK;
-    if (L.kind == SWEEP_LOCAL2D) {
+    if (L.kind == SWEEP_LOCAL2D && L.tb > 1) {
+        if (S_run <= 0) S_run = L.tb;
+        if (L.per_ctrl_cost)
+            launch_tb<T, true>(P, L, it, S_run, 0, tol, s);
+        else
+            launch_tb<T, false>(P, L, it, S_run, 0, tol, s);
+    } else if (L.kind == SWEEP_LOCAL2D) {
         if (L.per_ctrl_cost)
             launch_local<T, true>(P, L, it, tol, s);
         else

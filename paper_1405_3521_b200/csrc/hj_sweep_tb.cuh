@@ -1,0 +1,451 @@
+// hj_sweep_tb.cuh — temporally blocked local 2-D sweep: S Jacobi sweeps per launch
+// (PAPER.md eq. (SL) line 235 / (Tdef) line 238-245, the north_star's "optional
+// in-tile temporal blocking").
+//
+// Problem class: the one k_sweep_local2d handles (2-D, f = c(x) u_a, every foot
+// within one cell, so T(V) at a node reads only its 3x3 neighbourhood).  A CTA owns
+// a 32 x 32 tile and stages the tile plus an S-cell halo (<= 48 x 48) of V^n, the
+// classes and the speed in shared memory; sub-sweep j = 1..S recomputes the region
+// shrunk by j cells (overlapped tiling: the halo is recomputed redundantly, never
+// exchanged), so after S sub-sweeps the owned 32 x 32 nodes hold exactly V^{n+S}.
+// Every node update is the same arithmetic, in the same order, as k_sweep_local2d —
+// the iterates are bit-identical to S launches of the one-sweep kernels.
+//
+// Per sub-sweep each CTA folds max |V^{n+j} - V^{n+j-1}| over its OWNED nodes into
+// res[n+j-1] (per-warp atomicMax), so the host still sees every sweep's residual
+// and the stopping rule (R6) stays exact: if the first n* with res < tol falls
+// inside a block, that block is re-run from its (intact) input with S' = n* - n0
+// sub-sweeps (tile flag `rerun`).
+//
+// Exact skipping at block granularity.  Flags per tile and block: bit0 = an owned
+// node changed in the LAST sub-sweep, bit1 = changed in ANY sub-sweep.  If no tile
+// within one tile (>= S cells) changed in the last sweep of block b-1, then
+// V^{n0+S} = V^{n0} on the tile; the output buffer already holds it unless the tile
+// itself changed during block b-1 (bit1), in which case the tile is copied.
+//
+// Box edges (R3) need a per-control out-of-box test; those nodes are few, so a warp
+// evaluates each of its edge nodes cooperatively (controls spread over the lanes,
+// then a warp min) instead of diverging through a 4 KQ-iteration loop.
+#pragma once
+
+namespace hj {
+
+constexpr int TB_T = 32;      // owned tile edge
+constexpr int TB_SMAX = 8;    // sub-sweeps per launch (max)
+constexpr int TB_P = TB_T + 2 * TB_SMAX;   // staged pitch (48)
+
+// Optional per-CTA trace (profiling aid, off unless hj_debug_set_trace was called):
+// [blockIdx] = {smid, start ns, end ns, computed nodes}.
+struct TBTrace {
+    unsigned long long *buf;
+    long long cap;
+    long long n0;          // record only the launch whose first sweep is n0
+};
+static __device__ TBTrace g_tb_trace = {nullptr, 0, 0};   // set by hj_debug_set_trace
+
+template <typename T>
+struct TBSmem {
+    T V[2][TB_P * TB_P];
+    T c[TB_P * TB_P];           // speed c(x) (1 if none)
+    int16_t list[TB_P * TB_P];  // compacted dirty interior nodes of the sub-sweep
+    int16_t elist[4 * TB_P];    // compacted dirty box-edge nodes (R3 path)
+    int8_t cls[TB_P * TB_P];    // -2 ghost / outside the view, -1 interior, -3 interior
+                                // on the box edge, >= 0 target
+    uint8_t chg[TB_P * TB_P];   // last sub-sweep in which the node changed (0: none)
+    int cnt[2], ecnt[2];
+};
+
+template <typename T>
+__device__ __forceinline__ T tb_edge_cand(const DevProblem<T, T> &P, const LocalCtrl<T> &C, int KQ,
+                                          bool PC, const T *sp, int q, int k, T C0, T sc, T base,
+                                          bool lo_x, bool hi_x, bool lo_y, bool hi_y) {
+    constexpr int SW = TB_P;
+    const T V00 = sp[0];
+    const T Vx = (q & 1) ? sp[-1] : sp[1];
+    const T Vy = (q & 2) ? sp[-SW] : sp[SW];
+    const T Vxy = (q == 0) ? sp[SW + 1] : (q == 1) ? sp[SW - 1] : (q == 2) ? sp[-SW + 1] : sp[-SW - 1];
+    const bool ex = (q & 1) ? lo_x : hi_x, ey = (q & 2) ? lo_y : hi_y;
+    const T Dx = P.beta * (Vx - V00), Dy = P.beta * (Vy - V00);
+    const T Dxy = P.beta * ((Vxy - Vx) - (Vy - V00));
+    const T c_out = fma(P.beta, P.v_out, base);
+    const T eps = (T)BOX_EPS;
+    T wx = sc * C.ax[q][k], wy = sc * C.ay[q][k];
+    const T ck = PC ? C.ck[q][k] : T(0);
+    const bool out = (ex && wx > eps) || (ey && wy > eps);
+    if (ex) wx = T(0);
+    if (ey) wy = T(0);
+    const T in = fma(wy, fma(wx, Dxy, Dy), fma(wx, Dx, C0)) + ck;
+    return out ? c_out + ck : in;
+}
+
+// Interior bracket-min of a node pair (lanes .x/.y = nodes 0/1), quadrant by
+// quadrant.  Same per-node arithmetic as k_sweep_local2d (bit-identical).
+// Exact pruning (PRUNE): in quadrant q every candidate is
+//   C0 + g(ax, ay),  g = ax A1 + ay A2 + ax ay A3 bilinear on [0, xmax_q] x [0, ymax_q],
+// so it is >= C0 + min(g at the 4 box corners) = LB_q.  A quadrant is skipped when, for
+// both nodes of every pair of the warp, LB_q exceeds the running best by more than the
+// rounding error of a candidate (1e-6 (fp32) / 1e-14 (fp64) of the summed magnitudes):
+// then no candidate of it can be below that best and the min is unchanged bit for bit.
+// With the monotone clamp (V^{n+1} = min(T V^n, V^n)) the running best starts at V00.
+template <typename T>
+struct TBTraits;
+template <>
+struct TBTraits<float> {
+    static constexpr float rel = 1e-6f;
+};
+template <>
+struct TBTraits<double> {
+    static constexpr double rel = 1e-14;
+};
+
+template <typename T, int KQ, bool PC>
+__device__ __forceinline__ void tb_quadrant(const LocalCtrl<T> &C, int q, const T C0[2],
+                                            const T A1[2], const T A2[2], const T A3[2],
+                                            T best[2]);
+
+template <int KQ, bool PC>
+__device__ __forceinline__ void tb_quadrant_f(const LocalCtrl<float> &C, int q, const float C0[2],
+                                              const float A1[2], const float A2[2],
+                                              const float A3[2], float best[2]) {
+    const float2 c0 = make_float2(C0[0], C0[1]);
+    const float2 a1 = make_float2(A1[0], A1[1]), a2 = make_float2(A2[0], A2[1]);
+    const float2 a3 = make_float2(A3[0], A3[1]);
+#pragma unroll
+    for (int k = 0; k < KQ; k += 2) {
+        const float ax0 = C.ax[q][k], ay0 = C.ay[q][k];
+        const float ax1 = C.ax[q][k + 1], ay1 = C.ay[q][k + 1];
+        const float2 u0 = __ffma2_rn(make_float2(ax0, ax0), a1,
+                                     PC ? __fadd2_rn(c0, make_float2(C.ck[q][k], C.ck[q][k])) : c0);
+        const float2 u1 = __ffma2_rn(
+            make_float2(ax1, ax1), a1,
+            PC ? __fadd2_rn(c0, make_float2(C.ck[q][k + 1], C.ck[q][k + 1])) : c0);
+        const float2 w0 = __ffma2_rn(make_float2(ax0, ax0), a3, a2);
+        const float2 w1 = __ffma2_rn(make_float2(ax1, ax1), a3, a2);
+        const float2 k0 = __ffma2_rn(make_float2(ay0, ay0), w0, u0);
+        const float2 k1 = __ffma2_rn(make_float2(ay1, ay1), w1, u1);
+        best[0] = fminf(best[0], fminf(k0.x, k1.x));
+        best[1] = fminf(best[1], fminf(k0.y, k1.y));
+    }
+}
+
+template <int KQ, bool PC>
+__device__ __forceinline__ void tb_quadrant_d(const LocalCtrl<double> &C, int q, const double C0[2],
+                                              const double A1[2], const double A2[2],
+                                              const double A3[2], double best[2]) {
+#pragma unroll
+    for (int k = 0; k < KQ; ++k) {
+        const double ax = C.ax[q][k], ay = C.ay[q][k];
+#pragma unroll
+        for (int p = 0; p < 2; ++p) {
+            const double u = fma(ax, A1[p], PC ? C0[p] + C.ck[q][k] : C0[p]);
+            best[p] = fmin(best[p], fma(ay, fma(ax, A3[p], A2[p]), u));
+        }
+    }
+}
+
+template <typename T, int KQ, bool PC>
+__device__ __forceinline__ void tb_quadrant(const LocalCtrl<T> &C, int q, const T C0[2],
+                                            const T A1[2], const T A2[2], const T A3[2],
+                                            T best[2]) {
+    if constexpr (sizeof(T) == 4)
+        tb_quadrant_f<KQ, PC>(C, q, C0, A1, A2, A3, best);
+    else
+        tb_quadrant_d<KQ, PC>(C, q, C0, A1, A2, A3, best);
+}
+
+// tb flags: bit0 changed in the last sub-sweep, bit1 changed in any sub-sweep.
+// Staged classes: -3 marks an interior node ON the box edge (R3 slow path).
+template <typename T, int KQ, bool PC>
+__global__ void __launch_bounds__(256, 3)
+    k_sweep_local2d_tb(const DevProblem<T, T> P, const LocalCtrl<T> C,
+                       const SweepGroup<T> *__restrict__ G, int64_t n0, int S_blk, int S_run,
+                       int rerun, double tol) {
+    extern __shared__ __align__(16) unsigned char tb_raw[];
+    TBSmem<T> &sm = *reinterpret_cast<TBSmem<T> *>(tb_raw);
+    const int64_t b = blockIdx.x;
+    unsigned long long t_start = 0;
+    if (g_tb_trace.buf) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+    const int v = find_view(G, b);
+    const SweepView<T> &vw = G->v[v];
+    const TileView<T> &tv = G->t[v];
+    if (rerun) {                       // re-run of the block that contains the stop
+        S_run = tv.rerun;
+        if (S_run <= 0) return;
+    }
+    const int64_t blk = n0 / S_blk;
+    // stopped view: some sweep of the previous block met the rule
+    {
+        int stop = 0;
+        if (n0 > 0 && (int)threadIdx.x < S_blk)
+            stop = *(volatile double *)&vw.res[n0 - S_blk + threadIdx.x] < tol;
+        if (__syncthreads_or(stop)) return;
+    }
+    const int64_t tile = b - tv.tile_base;
+    const int tcx = (int)(tile % tv.nt[0]), tcy = (int)(tile / tv.nt[0]);
+    const int vn0 = (int)vw.vn[0], vn1 = (int)vw.vn[1];
+    const T *__restrict__ Vi = vw.V[blk & 1];
+    T *__restrict__ Vo = vw.V[(blk + 1) & 1];
+    const int x0 = tcx * TB_T, y0 = tcy * TB_T;
+    uint8_t *flags_out = tv.chg + (blk & 1) * tv.tiles;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    // ---- exact skip (block granularity) ---------------------------------------
+    if (n0 > 0) {
+        const uint8_t *prev = tv.chg + ((blk - 1) & 1) * tv.tiles;
+        int act = 0, own = 0;
+        if (threadIdx.x < 9) {
+            const int cx = tcx + (int)threadIdx.x % 3 - 1, cy = tcy + (int)threadIdx.x / 3 - 1;
+            if (cx >= 0 && cy >= 0 && cx < tv.nt[0] && cy < tv.nt[1]) {
+                const uint8_t f = prev[cx + (int64_t)tv.nt[0] * cy];
+                act = f & 1;
+                if (threadIdx.x == 4) own = (f >> 1) & 1;
+            }
+        }
+        const int any_act = __syncthreads_or(act);
+        if (!any_act) {
+            const int any_own = __syncthreads_or(own);
+            if (any_own) {             // V^{n0} -> output buffer (tile changed in block b-1)
+                for (int r = warp; r < TB_T; r += 8) {
+                    const int li = x0 + lane, lj = y0 + r;
+                    if (li < vn0 && lj < vn1) {
+                        const int64_t t = li + (int64_t)vn0 * lj;
+                        Vo[t] = Vi[t];
+                    }
+                }
+            }
+            if (threadIdx.x == 0) flags_out[tile] = 0;
+            return;
+        }
+    }
+    // ---- stage tile + S-cell halo ---------------------------------------------
+    const int S = S_run;
+    const int R = TB_T + 2 * S;        // staged region edge (pitch TB_P)
+    const int ox = x0 - S, oy = y0 - S;
+    const int64_t n0g = vw.o[0] + ox, n1g = vw.o[1] + oy;   // global index of region (0,0)
+    const int64_t gn0 = P.n[0], gn1 = P.n[1];
+    const T v_out = P.v_out;
+    for (int r = warp; r < R; r += 8) {
+        for (int c = lane; c < R; c += 32) {
+            const int li = ox + c, lj = oy + r;
+            T val = v_out, sp = T(1);
+            int8_t cl = -2;
+            if (li >= 0 && lj >= 0 && li < vn0 && lj < vn1) {
+                const int64_t t = li + (int64_t)vn0 * lj;
+                val = Vi[t];
+                cl = vw.cls[t];
+                const int64_t g0 = n0g + c, g1 = n1g + r;
+                if (P.speed) sp = P.speed[g0 + gn0 * g1];
+                if (cl == -1 && (g0 == 0 || g1 == 0 || g0 == gn0 - 1 || g1 == gn1 - 1)) cl = -3;
+            }
+            const int si = r * TB_P + c;
+            sm.V[0][si] = val;
+            sm.V[1][si] = val;
+            sm.cls[si] = cl;
+            sm.c[si] = sp;
+            sm.chg[si] = 0;
+        }
+    }
+    __syncthreads();
+    const bool mono = P.monotone != 0;
+    const T beta = P.beta;
+    const bool kruz = P.cost == HJ_COST_KRUZKOV;
+    int evaluated = 0, listed = 0;
+    int cur = 0;
+    if (threadIdx.x == 0) sm.cnt[1] = sm.ecnt[1] = 0;
+    for (int j = 1; j <= S; ++j) {
+        const T *__restrict__ Vc = sm.V[cur];
+        T *__restrict__ Vn = sm.V[cur ^ 1];
+        const int lo = j, hi = R - 1 - j;           // compute region [j, R-1-j]^2
+        // ---- 1. dirty interior nodes -> list.  A node's T(V) can change only if a node
+        // of its 3x3 neighbourhood changed in sub-sweep j-1 (chg == j-1; all at j = 1).
+        // Nodes not recomputed keep their value in BOTH buffers (they did not change in
+        // j-1 either), so nothing is copied.
+        int *cnt = &sm.cnt[j & 1];
+        for (int r = lo + warp; r <= hi; r += 8) {
+            for (int cb = lo; cb <= hi; cb += 32) {
+                const int c = cb + lane;
+                bool dirty = false, is_edge = false;
+                int si = r * TB_P + c;
+                if (c <= hi) {
+                    const int8_t cl = sm.cls[si];
+                    is_edge = cl == -3;
+                    if (cl == -1 || cl == -3) {
+                        const uint8_t jm = (uint8_t)(j - 1);
+                        const uint8_t *g = sm.chg + si;
+                        dirty = (g[-TB_P - 1] == jm) | (g[-TB_P] == jm) | (g[-TB_P + 1] == jm) |
+                                (g[-1] == jm) | (g[0] == jm) | (g[1] == jm) |
+                                (g[TB_P - 1] == jm) | (g[TB_P] == jm) | (g[TB_P + 1] == jm);
+                    }
+                }
+                const unsigned bal = __ballot_sync(0xffffffffu, dirty && !is_edge);
+                if (bal) {
+                    int base_i = 0;
+                    if (lane == 0) base_i = atomicAdd(cnt, __popc(bal));
+                    base_i = __shfl_sync(0xffffffffu, base_i, 0);
+                    if (dirty && !is_edge)
+                        sm.list[base_i + __popc(bal & ((1u << lane) - 1))] = (int16_t)si;
+                }
+                const unsigned ebal = __ballot_sync(0xffffffffu, dirty && is_edge);
+                if (ebal) {
+                    int base_i = 0;
+                    if (lane == 0) base_i = atomicAdd(&sm.ecnt[j & 1], __popc(ebal));
+                    base_i = __shfl_sync(0xffffffffu, base_i, 0);
+                    if (dirty && is_edge)
+                        sm.elist[base_i + __popc(ebal & ((1u << lane) - 1))] = (int16_t)si;
+                }
+            }
+        }
+        __syncthreads();
+        const int L = *cnt, LE = sm.ecnt[j & 1];
+        listed += L + LE;
+        if (threadIdx.x == 0) sm.cnt[(j + 1) & 1] = sm.ecnt[(j + 1) & 1] = 0;   // for j+1
+        // ---- 2. the bracket-min of the listed nodes, in pairs (i, i + 256) -----------
+        T rmax = T(0);
+        const int M = (L + 511) / 512;
+        for (int m = 0; m < M; ++m) {
+            const int iA = (int)threadIdx.x + 512 * m;
+            int si[2];
+            bool valid[2], owned[2];
+            int8_t cl[2];
+            T C0[2], V00[2], best[2], A1[4][2], A2[4][2], A3[4][2];
+#pragma unroll
+            for (int p = 0; p < 2; ++p) {
+                valid[p] = iA + 256 * p < L;
+                si[p] = valid[p] ? (int)sm.list[iA + 256 * p] : (S + 1) * TB_P + S + 1;
+                const int r = si[p] / TB_P, c = si[p] - (si[p] / TB_P) * TB_P;
+                owned[p] = valid[p] && (unsigned)(r - S) < (unsigned)TB_T &&
+                           (unsigned)(c - S) < (unsigned)TB_T;
+                cl[p] = valid[p] ? sm.cls[si[p]] : (int8_t)-2;
+                const T *q0 = Vc + si[p];
+                V00[p] = q0[0];
+                T base = P.kcost;
+                if (!kruz) {
+                    const T x[3] = {fma((T)(n0g + c), P.dx[0], P.lo[0]),
+                                    fma((T)(n1g + r), P.dx[1], P.lo[1]), T(0)};
+                    base = P.h * cost_state(P, x);
+                }
+                C0[p] = fma(beta, V00[p], base);
+                const T sc = sm.c[si[p]];
+                const T bs = beta * sc, bss = bs * sc;
+                const T Vm0 = q0[-1], Vp0 = q0[1], V0m = q0[-TB_P], V0p = q0[TB_P];
+                const T Vmm = q0[-TB_P - 1], Vpm = q0[-TB_P + 1], Vmp = q0[TB_P - 1],
+                        Vpp = q0[TB_P + 1];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const T Vx = (q & 1) ? Vm0 : Vp0;
+                    const T Vy = (q & 2) ? V0m : V0p;
+                    const T Vxy = (q == 0) ? Vpp : (q == 1) ? Vmp : (q == 2) ? Vpm : Vmm;
+                    const T Dx = Vx - V00[p], Dy = Vy - V00[p], Dxy = (Vxy - Vx) - Dy;
+                    A1[q][p] = bs * Dx;
+                    A2[q][p] = bs * Dy;
+                    A3[q][p] = bss * Dxy;
+                }
+                // the clamp value V00 (monotone: V^{n+1} = min(T V^n, V^n)), else +inf
+                best[p] = mono ? V00[p] : (T)INFINITY;
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const T a1[2] = {A1[q][0], A1[q][1]}, a2[2] = {A2[q][0], A2[q][1]};
+                const T a3[2] = {A3[q][0], A3[q][1]};
+                tb_quadrant<T, KQ, PC>(C, q, C0, a1, a2, a3, best);
+            }
+#pragma unroll
+            for (int p = 0; p < 2; ++p) {
+                if (!valid[p]) continue;
+                const T vnew = best[p];          // (monotone: already min(T V, V00))
+                evaluated += owned[p];
+                Vn[si[p]] = vnew;
+                if (!same_bits(vnew, V00[p])) {
+                    sm.chg[si[p]] = (uint8_t)j;
+                    if (owned[p]) {
+                        const T dv = vnew > V00[p] ? vnew - V00[p] : V00[p] - vnew;
+                        rmax = dv > rmax ? dv : rmax;
+                    }
+                }
+            }
+        }
+        // ---- 3. box-edge nodes (R3), same edge formula as k_sweep_local2d: 4 nodes per
+        // warp at a time, 8 lanes per node splitting the controls, then an 8-lane min
+        {
+            const int sg = lane >> 3, sl = lane & 7;
+            for (int e0 = 4 * warp; e0 < LE; e0 += 32) {
+                const int e = e0 + sg;
+                const bool ok = e < LE;
+                const int esi = ok ? (int)sm.elist[e] : (S + 1) * TB_P + S + 1;
+                const int sr = esi / TB_P, scol = esi - sr * TB_P;
+                const int64_t g0 = n0g + scol, g1 = n1g + sr;
+                T base = P.kcost;
+                if (!kruz) {
+                    const T x[3] = {fma((T)g0, P.dx[0], P.lo[0]), fma((T)g1, P.dx[1], P.lo[1]),
+                                    T(0)};
+                    base = P.h * cost_state(P, x);
+                }
+                const T eV00 = Vc[esi];
+                const T eC0 = fma(beta, eV00, base);
+                const T e_sc = sm.c[esi];
+                const bool lx = g0 == 0, hx = g0 == gn0 - 1, ly = g1 == 0, hy = g1 == gn1 - 1;
+                T e_best = (T)INFINITY;
+                for (int f = sl; f < 4 * KQ; f += 8)
+                    e_best = fmin(e_best, tb_edge_cand<T>(P, C, KQ, PC, Vc + esi, f / KQ, f % KQ,
+                                                          eC0, e_sc, base, lx, hx, ly, hy));
+#pragma unroll
+                for (int o = 4; o > 0; o >>= 1)
+                    e_best = fmin(e_best, __shfl_xor_sync(0xffffffffu, e_best, o));
+                if (ok && sl == 0) {
+                    const T vnew = mono ? fmin(e_best, eV00) : e_best;
+                    const bool own = (unsigned)(sr - S) < (unsigned)TB_T &&
+                                     (unsigned)(scol - S) < (unsigned)TB_T;
+                    evaluated += own;
+                    Vn[esi] = vnew;
+                    if (!same_bits(vnew, eV00)) {
+                        sm.chg[esi] = (uint8_t)j;
+                        if (own) {
+                            const T dv = vnew > eV00 ? vnew - eV00 : eV00 - vnew;
+                            rmax = dv > rmax ? dv : rmax;
+                        }
+                    }
+                }
+            }
+        }
+        // residual of sweep n0+j-1 over the owned nodes (per-warp atomic)
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const T other = __shfl_xor_sync(0xffffffffu, rmax, o);
+            rmax = other > rmax ? other : rmax;
+        }
+        if (lane == 0 && rmax > T(0)) atomic_max_nonneg(&vw.res[n0 + j - 1], (double)rmax);
+        cur ^= 1;
+        __syncthreads();
+    }
+    int chg_last = 0, chg_any = 0;
+    for (int r = warp; r < TB_T; r += 8) {
+        const uint8_t g = sm.chg[(r + S) * TB_P + lane + S];
+        chg_last |= g == (uint8_t)S;
+        chg_any |= g != 0;
+    }
+    // ---- owned nodes of V^{n0+S} -> global -------------------------------------
+    const T *__restrict__ Vf = sm.V[cur];
+    for (int r = warp; r < TB_T; r += 8) {
+        const int li = x0 + lane, lj = y0 + r;
+        if (li < vn0 && lj < vn1) Vo[li + (int64_t)vn0 * lj] = Vf[(r + S) * TB_P + (lane + S)];
+    }
+    evaluated = __reduce_add_sync(0xffffffffu, evaluated);
+    if (lane == 0 && evaluated) atomicAdd(vw.work, (unsigned long long)evaluated);
+    const int any_last = __syncthreads_or(chg_last);
+    const int any_any = __syncthreads_or(chg_any);
+    if (threadIdx.x == 0) flags_out[tile] = (uint8_t)((any_last ? 1 : 0) | (any_any ? 2 : 0));
+    if (g_tb_trace.buf && threadIdx.x == 0 && b < g_tb_trace.cap && n0 == g_tb_trace.n0 &&
+        !rerun) {
+        unsigned long long t_end, smid;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+        unsigned s32;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(s32));
+        smid = s32;
+        unsigned long long *o = g_tb_trace.buf + 4 * b;
+        o[0] = smid;
+        o[1] = t_start;
+        o[2] = t_end;
+        o[3] = (unsigned long long)listed;
+    }
+}
+
+}  // namespace hj

@@ -70,8 +70,8 @@ def test_solve_matches_oracle(idx, dtype, oracle_cache):
         assert abs(rep["iterations"] - it_o) <= max(2, it_o // 10)   # fp32 residual noise
 
 
-KERNELS = {1: ("generic", "field2d", "local_scalar", "local_packed"),
-           2: ("generic", "field2d", "local_scalar", "local_packed"),
+KERNELS = {1: ("generic", "field2d", "local_scalar", "local_packed", "local_tb"),
+           2: ("generic", "field2d", "local_scalar", "local_packed", "local_tb"),
            3: ("generic", "field2d"), 4: ("generic", "dubins"), 5: ("generic", "field2d")}
 
 
@@ -100,6 +100,35 @@ def test_sweep_kernels_match_oracle(idx, dtype, oracle_cache):
     if "local_packed" in out:
         assert torch.equal(out["local_scalar"][0], out["local_packed"][0])
         assert out["local_scalar"][1] == out["local_packed"][1]
+    if "local_tb" in out:               # 8 sweeps per launch, same iterates bit for bit
+        assert torch.equal(out["local_scalar"][0], out["local_tb"][0])
+        assert out["local_scalar"][1] == out["local_tb"][1]
+
+
+@pytest.mark.parametrize("max_iter", [1, 5, 8, 13, 16])
+def test_local_tb_stops_inside_a_block(max_iter):
+    """The temporally blocked kernel (8 sweeps per launch) must return exactly the
+    iterate the one-sweep kernel returns, whatever sweep the stop lands on: a tol the
+    iteration meets at sweep n* re-runs n*'s block with n* - 8 floor((n*-1)/8) sweeps;
+    max_iter cut-offs inside a block end the last block early."""
+    cfg = _cfg(2)
+    ref = hj.DeviceProblem(cfg.fine, "f32", sweep_kernel="local_packed")
+    tb = hj.DeviceProblem(cfg.fine, "f32", sweep_kernel="local_tb")
+    V1, r1 = hj.hj_solve(ref, max_iter=max_iter, allow_not_converged=True)
+    V2, r2 = hj.hj_solve(tb, max_iter=max_iter, allow_not_converged=True)
+    assert torch.equal(V1, V2) and r1["iterations"] == r2["iterations"] == max_iter
+    # stops landing on every position inside a block
+    _, full = hj.hj_solve(ref, tol=1e-7)
+    res_hist = []
+    for n in range(max(1, full["iterations"] - 9), full["iterations"] + 1):
+        Vn, rn = hj.hj_solve(ref, max_iter=n, allow_not_converged=True)
+        res_hist.append((n, rn["residual"]))
+    for n, r in res_hist[:-1]:
+        tol = float(r) * (1 + 1e-9) if r > 0 else 1e-30
+        Va, ra = hj.hj_solve(ref, tol=tol, allow_not_converged=True)
+        Vb, rb = hj.hj_solve(tb, tol=tol, allow_not_converged=True)
+        assert ra["iterations"] == rb["iterations"], (n, ra["iterations"], rb["iterations"])
+        assert torch.equal(Va, Vb)
 
 
 def test_local_kernel_refuses_nonlocal_problem():
