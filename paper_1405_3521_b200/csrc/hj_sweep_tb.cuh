@@ -51,7 +51,10 @@ struct TBSmem {
     int16_t elist[4 * TB_P];    // compacted dirty box-edge nodes (R3 path)
     int8_t cls[TB_P * TB_P];    // -2 ghost / outside the view, -1 interior, -3 interior
                                 // on the box edge, >= 0 target
-    uint8_t chg[TB_P * TB_P];   // last sub-sweep in which the node changed (0: none)
+    // row bitmasks (bit c of word [r] = column c; the region is <= 48 < 64 wide)
+    unsigned long long imask[TB_P];    // fast interior nodes (class -1)
+    unsigned long long emask[TB_P];    // interior nodes on the box edge (class -3)
+    unsigned int chm[2][TB_P][2];      // changed in the sub-sweep of that parity
     int cnt[2], ecnt[2];
 };
 
@@ -241,14 +244,28 @@ __global__ void __launch_bounds__(256, 3)
             sm.V[1][si] = val;
             sm.cls[si] = cl;
             sm.c[si] = sp;
-            sm.chg[si] = 0;
+        }
+    }
+    __syncthreads();
+    for (int r = warp; r < R; r += 8) {           // class masks; sub-sweep 1: all dirty
+        const int8_t c0 = lane < R ? sm.cls[r * TB_P + lane] : (int8_t)-2;
+        const int8_t c1 = lane + 32 < R ? sm.cls[r * TB_P + lane + 32] : (int8_t)-2;
+        const unsigned i0 = __ballot_sync(0xffffffffu, c0 == -1),
+                       i1 = __ballot_sync(0xffffffffu, c1 == -1);
+        const unsigned e0 = __ballot_sync(0xffffffffu, c0 == -3),
+                       e1 = __ballot_sync(0xffffffffu, c1 == -3);
+        if (lane == 0) {
+            sm.imask[r] = (unsigned long long)i0 | ((unsigned long long)i1 << 32);
+            sm.emask[r] = (unsigned long long)e0 | ((unsigned long long)e1 << 32);
+            sm.chm[0][r][0] = sm.chm[0][r][1] = 0xffffffffu;
+            sm.chm[1][r][0] = sm.chm[1][r][1] = 0u;
         }
     }
     __syncthreads();
     const bool mono = P.monotone != 0;
     const T beta = P.beta;
     const bool kruz = P.cost == HJ_COST_KRUZKOV;
-    int evaluated = 0, listed = 0;
+    int evaluated = 0, listed = 0, chg_any = 0;
     int cur = 0;
     if (threadIdx.x == 0) sm.cnt[1] = sm.ecnt[1] = 0;
     for (int j = 1; j <= S; ++j) {
@@ -260,37 +277,40 @@ __global__ void __launch_bounds__(256, 3)
         // Nodes not recomputed keep their value in BOTH buffers (they did not change in
         // j-1 either), so nothing is copied.
         int *cnt = &sm.cnt[j & 1];
-        for (int r = lo + warp; r <= hi; r += 8) {
-            for (int cb = lo; cb <= hi; cb += 32) {
-                const int c = cb + lane;
-                bool dirty = false, is_edge = false;
-                int si = r * TB_P + c;
-                if (c <= hi) {
-                    const int8_t cl = sm.cls[si];
-                    is_edge = cl == -3;
-                    if (cl == -1 || cl == -3) {
-                        const uint8_t jm = (uint8_t)(j - 1);
-                        const uint8_t *g = sm.chg + si;
-                        dirty = (g[-TB_P - 1] == jm) | (g[-TB_P] == jm) | (g[-TB_P + 1] == jm) |
-                                (g[-1] == jm) | (g[0] == jm) | (g[1] == jm) |
-                                (g[TB_P - 1] == jm) | (g[TB_P] == jm) | (g[TB_P + 1] == jm);
+        {
+            const unsigned (*pm)[2] = sm.chm[(j - 1) & 1];
+            const unsigned long long cols =
+                ((hi >= 63 ? ~0ull : ((1ull << (hi + 1)) - 1))) & ~((1ull << lo) - 1);
+            for (int r = lo + warp; r <= hi; r += 8) {
+                auto row = [&](int rr) -> unsigned long long {
+                    return (unsigned long long)pm[rr][0] | ((unsigned long long)pm[rr][1] << 32);
+                };
+                unsigned long long m = row(r - 1) | row(r) | row(r + 1);
+                m = (m | (m << 1) | (m >> 1)) & cols;
+                const unsigned long long dI = m & sm.imask[r], dE = m & sm.emask[r];
+                if (dI) {
+                    int base_i = 0;
+                    if (lane == 0) base_i = atomicAdd(cnt, __popcll(dI));
+                    base_i = __shfl_sync(0xffffffffu, base_i, 0);
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const int c = lane + 32 * h;
+                        if ((dI >> c) & 1ull)
+                            sm.list[base_i + __popcll(dI & ((1ull << c) - 1))] =
+                                (int16_t)(r * TB_P + c);
                     }
                 }
-                const unsigned bal = __ballot_sync(0xffffffffu, dirty && !is_edge);
-                if (bal) {
+                if (dE) {
                     int base_i = 0;
-                    if (lane == 0) base_i = atomicAdd(cnt, __popc(bal));
+                    if (lane == 0) base_i = atomicAdd(&sm.ecnt[j & 1], __popcll(dE));
                     base_i = __shfl_sync(0xffffffffu, base_i, 0);
-                    if (dirty && !is_edge)
-                        sm.list[base_i + __popc(bal & ((1u << lane) - 1))] = (int16_t)si;
-                }
-                const unsigned ebal = __ballot_sync(0xffffffffu, dirty && is_edge);
-                if (ebal) {
-                    int base_i = 0;
-                    if (lane == 0) base_i = atomicAdd(&sm.ecnt[j & 1], __popc(ebal));
-                    base_i = __shfl_sync(0xffffffffu, base_i, 0);
-                    if (dirty && is_edge)
-                        sm.elist[base_i + __popc(ebal & ((1u << lane) - 1))] = (int16_t)si;
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const int c = lane + 32 * h;
+                        if ((dE >> c) & 1ull)
+                            sm.elist[base_i + __popcll(dE & ((1ull << c) - 1))] =
+                                (int16_t)(r * TB_P + c);
+                    }
                 }
             }
         }
@@ -298,6 +318,10 @@ __global__ void __launch_bounds__(256, 3)
         const int L = *cnt, LE = sm.ecnt[j & 1];
         listed += L + LE;
         if (threadIdx.x == 0) sm.cnt[(j + 1) & 1] = sm.ecnt[(j + 1) & 1] = 0;   // for j+1
+        // changed masks of sub-sweep j (its parity slot was read by this scan: reuse it)
+        for (int r = threadIdx.x; r < TB_P; r += blockDim.x)
+            sm.chm[j & 1][r][0] = sm.chm[j & 1][r][1] = 0u;
+        __syncthreads();
         // ---- 2. the bracket-min of the listed nodes, in pairs (i, i + 256) -----------
         T rmax = T(0);
         const int M = (L + 511) / 512;
@@ -355,7 +379,9 @@ __global__ void __launch_bounds__(256, 3)
                 evaluated += owned[p];
                 Vn[si[p]] = vnew;
                 if (!same_bits(vnew, V00[p])) {
-                    sm.chg[si[p]] = (uint8_t)j;
+                    const int r = si[p] / TB_P, c = si[p] - r * TB_P;
+                    atomicOr(&sm.chm[j & 1][r][c >> 5], 1u << (c & 31));
+                    chg_any |= owned[p];
                     if (owned[p]) {
                         const T dv = vnew > V00[p] ? vnew - V00[p] : V00[p] - vnew;
                         rmax = dv > rmax ? dv : rmax;
@@ -397,7 +423,8 @@ __global__ void __launch_bounds__(256, 3)
                     evaluated += own;
                     Vn[esi] = vnew;
                     if (!same_bits(vnew, eV00)) {
-                        sm.chg[esi] = (uint8_t)j;
+                        atomicOr(&sm.chm[j & 1][sr][scol >> 5], 1u << (scol & 31));
+                        chg_any |= own;
                         if (own) {
                             const T dv = vnew > eV00 ? vnew - eV00 : eV00 - vnew;
                             rmax = dv > rmax ? dv : rmax;
@@ -416,11 +443,12 @@ __global__ void __launch_bounds__(256, 3)
         cur ^= 1;
         __syncthreads();
     }
-    int chg_last = 0, chg_any = 0;
-    for (int r = warp; r < TB_T; r += 8) {
-        const uint8_t g = sm.chg[(r + S) * TB_P + lane + S];
-        chg_last |= g == (uint8_t)S;
-        chg_any |= g != 0;
+    int chg_last = 0;
+    if (threadIdx.x < TB_T) {                       // owned rows S..S+31, cols S..S+31
+        const int r = S + threadIdx.x;
+        const unsigned long long m =
+            (unsigned long long)sm.chm[S & 1][r][0] | ((unsigned long long)sm.chm[S & 1][r][1] << 32);
+        chg_last = ((m >> S) & 0xffffffffull) != 0;
     }
     // ---- owned nodes of V^{n0+S} -> global -------------------------------------
     const T *__restrict__ Vf = sm.V[cur];
