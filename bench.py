@@ -29,9 +29,12 @@ import hj_workloads as W  # noqa: E402
 
 METRIC = "grid-node x control updates/sec per sweep; time-to-solution at 1/2/4/8 B200"
 UNIT = "node-control updates/s"
-# per node x control update, the minimal lane instructions of the bilinear bracket-min
-# (2 weight products, 3 FMA of the difference-form interpolation, 1 min): DESIGN.md §7
-ALGO_OPS_PER_UPDATE = {2: 6, 3: 11}
+# Roofline of the fine sweep: the bracket of one node x control update is
+# a bilinear form in the control's weights, so at least 3 fused multiply-adds (the
+# difference form C0 + ax A1 + ay (A2 + ax A3)); the FMA pipes retire 128 FMA lanes per
+# SM clock (FFMA2 packs two per issue slot but not per pipe cycle — measured).
+FMA_PER_UPDATE = {2: 3, 3: 3}
+FMA_LANES_PER_SM_CLK = 128
 
 
 def load_peaks():
@@ -259,21 +262,22 @@ def main():
 
     peaks, peak_kind = load_peaks()
     sm_mhz = float(peaks.get("sm_max_mhz", 1965.0))
-    peak_ops = 148 * 4 * 32 * sm_mhz * 1e6 / 1e12          # issue slots, T lane-op/s
+    peak_fma = 148 * FMA_LANES_PER_SM_CLK * sm_mhz * 1e6 / 1e12   # T FMA/s
     dim = cfg.fine.grid.dim
-    achieved = fine_eval * ALGO_OPS_PER_UPDATE[dim] / (sweep_ms / 1e3) / 1e12 if sweep_ms else 0
+    achieved = fine_eval * FMA_PER_UPDATE[dim] / (sweep_ms / 1e3) / 1e12 if sweep_ms else 0
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):
         with open(tpath) as f:
             traffic = json.load(f).get(cfg.name)
-    roofline = {"bound": "alu", "achieved": achieved, "peak": peak_ops, "unit": "Tlane-op/s",
-                "frac": achieved / peak_ops, "traffic": traffic,
-                "kernel": "fine sweep (k_sweep_*)",
+    roofline = {"bound": "alu", "achieved": achieved, "peak": peak_fma, "unit": "TFMA/s",
+                "frac": achieved / peak_fma, "traffic": traffic,
+                "kernel": "fine sweep (k_sweep_*): evaluated node x control updates x 3 FMA "
+                          "/ fine-solve device time",
                 "avg_launch_us": 1e3 * sweep_ms / max(sweep_launches, 1),
-                "peak_source": f"issue slots 148 SM x 4 x 32 lanes x {sm_mhz:.0f} MHz "
-                               f"({peak_kind} sm_max_mhz)",
-                "ops_per_update": ALGO_OPS_PER_UPDATE[dim]}
+                "peak_source": f"FMA pipes 148 SM x {FMA_LANES_PER_SM_CLK} lanes x "
+                               f"{sm_mhz:.0f} MHz ({peak_kind} sm_max_mhz; DESIGN.md §6)",
+                "fma_per_update": FMA_PER_UPDATE[dim]}
 
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
