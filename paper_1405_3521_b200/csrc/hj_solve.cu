@@ -310,6 +310,7 @@ static size_t solve_ws(const hj_grid &g, int64_t max_iter) {
     c.take(chg_bytes_for(vn));
     c.take(sizeof(SweepGroup<T>));
     c.take(64);
+    c.take(wl_bytes_for(tiles_finest(vn)));
     return c.off;
 }
 
@@ -330,6 +331,7 @@ static hj_status solve_impl(const hj_grid &grid, const hj_problem &prob, const h
     uint8_t *chg = (uint8_t *)c.take(chg_bytes_for(hv.vn));
     void *group = c.take(sizeof(SweepGroup<T>));
     unsigned long long *cnt = (unsigned long long *)c.take(64);
+    void *wl = c.take(wl_bytes_for(tiles_finest(hv.vn)));
     if (!c.ok()) {
         set_error("workspace too small: need %zu bytes, got %zu", c.off, ws_bytes);
         return HJ_ERR_WORKSPACE;
@@ -346,7 +348,7 @@ static hj_status solve_impl(const hj_grid &grid, const hj_problem &prob, const h
     std::vector<SweepView<T>> hvs{hv};
     std::vector<uint8_t *> chgs{chg};
     SweepLaunch<T> L;
-    hj_status st = sweep_prepare(grid, prob, f, hvs, chgs, group, s, L);
+    hj_status st = sweep_prepare(grid, prob, f, hvs, chgs, group, wl, s, L);
     if (st != HJ_OK) return st;
     const SweepView<T> *d_view = &L.d_group->v[0];
     int blocks = (int)std::min<int64_t>((N + 255) / 256, 148 * 16);
@@ -384,7 +386,7 @@ static hj_status solve_impl(const hj_grid &grid, const hj_problem &prob, const h
 // ---------------------------------------------------------------------------
 struct PartLayout {
     std::vector<size_t> off_v0, off_v1, off_cls, off_chg;
-    size_t off_res, off_views, off_asm, off_cnt, total;
+    size_t off_res, off_views, off_asm, off_cnt, off_wl, total;
 };
 
 template <typename T>
@@ -405,6 +407,15 @@ static PartLayout part_layout(int m, const hj_subdomain *plan, int64_t max_iter)
         L.off_chg.push_back(c.off);
         c.take(plan[k].n_nodes > 0 ? chg_bytes_for(vn) : 0);
     }
+    int64_t tiles = 0;
+    for (int k = 0; k < m; ++k) {
+        if (plan[k].n_nodes <= 0) continue;
+        int64_t vn[3];
+        for (int d = 0; d < 3; ++d) vn[d] = plan[k].hi[d] - plan[k].lo[d] + 1;
+        tiles += tiles_finest(vn);
+    }
+    L.off_wl = c.off;
+    c.take(wl_bytes_for(tiles));
     L.off_res = c.off;
     c.take((size_t)m * max_iter * sizeof(double));
     L.off_views = c.off;
@@ -481,7 +492,7 @@ static hj_status partitioned_impl(const hj_grid &grid, const hj_problem &prob,
     HJ_CUDA(cudaMemsetAsync(res, 0, (size_t)nv * max_iter * sizeof(double), s));
     HJ_CUDA(cudaMemsetAsync(cnt, 0, (size_t)2 * m * sizeof(unsigned long long), s));
     SweepLaunch<T> SL;
-    hj_status st = sweep_prepare(grid, prob, f, hv, chgs, group, s, SL);
+    hj_status st = sweep_prepare(grid, prob, f, hv, chgs, group, base + L.off_wl, s, SL);
     if (st != HJ_OK) return st;
     const SweepView<T> *d_views = &SL.d_group->v[0];
     int blocks = (int)std::min<int64_t>((max_nodes + 255) / 256, 148 * 16);

@@ -44,10 +44,26 @@ struct TileView {          // per-view tiling, filled by sweep_prepare
     int32_t rerun;         // temporally blocked kernel: sub-sweeps of the stop re-run
 };
 
+// Device work list of the tiles a sweep (or a block of sweeps) must visit: a tile is
+// listed for sweep n+1 iff a tile within the dependency radius changed in sweep n
+// (the exact "quiet tile" rule, see above), so launches are persistent grids that
+// walk the list instead of one CTA per tile.  Two parities of (items, mark bitmap)
+// and a ring of three counters: launch n reads count[n%3], appends to count[(n+1)%3]
+// and zeroes count[(n+2)%3]; every visited tile clears its own mark bit.
+struct WorkList {
+    int32_t *items[2];
+    int32_t *count;       // [3]
+    uint32_t *mark[2];    // bitmaps over global tile ids
+};
+
 template <typename T>
 struct SweepGroup {        // device-resident description of one launch
     SweepView<T> v[HJ_MAX_SUBDOMAINS];
     TileView<T> t[HJ_MAX_SUBDOMAINS];
+    WorkList wl;
+    int total_tiles;
+    int dense;             // 1: visit every tile every sweep, one CTA per tile, no list
+                           //    (discounted problems change everywhere until they stop)
     int n_views;
     int tile_dim[3];       // TX, TY, TZ (nodes)
     int radius[3];         // dependency radius in tiles
@@ -93,9 +109,77 @@ __device__ __forceinline__ bool tile_active(const SweepGroup<T> *__restrict__ G,
 }
 
 template <typename T>
-__device__ __forceinline__ void tile_finish(const SweepGroup<T> *__restrict__ G, int v,
-                                            int64_t tile, int64_t it, T rmax, int changed,
-                                            int evaluated) {
+__device__ __forceinline__ void tile_coords(const TileView<T> &tv, int64_t tile, int tc[3]) {
+    tc[0] = (int)(tile % tv.nt[0]);
+    tc[1] = (int)((tile / tv.nt[0]) % tv.nt[1]);
+    tc[2] = (int)(tile / ((int64_t)tv.nt[0] * tv.nt[1]));
+}
+
+__device__ __forceinline__ void wl_push(const WorkList &wl, int64_t nit, int gid) {
+    const uint32_t bit = 1u << (gid & 31);
+    uint32_t *w = &wl.mark[nit & 1][gid >> 5];
+    // already listed (the common case when the active set is dense): no atomic
+    if (*(volatile uint32_t *)w & bit) return;
+    const uint32_t old = atomicOr(w, bit);
+    if (!(old & bit)) wl.items[nit & 1][atomicAdd(&wl.count[nit % 3], 1)] = gid;
+}
+
+// list every tile within (rx, ry, rz) tiles of tile tc of view v for launch nit
+template <typename T>
+__device__ __forceinline__ void push_neighbours(const SweepGroup<T> *__restrict__ G, int v,
+                                                const int tc[3], int rx, int ry, int rz,
+                                                int64_t nit) {
+    const TileView<T> &tv = G->t[v];
+    const int wx = 2 * rx + 1, wy = 2 * ry + 1, wz = 2 * rz + 1;
+    const int count = wx * wy * wz;
+    for (int e = threadIdx.x; e < count; e += blockDim.x) {
+        int c[3] = {tc[0] + e % wx - rx, tc[1] + (e / wx) % wy - ry, tc[2] + e / (wx * wy) - rz};
+        bool ok = true;
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+            if (c[d] >= 0 && c[d] < tv.nt[d]) continue;
+            if (G->periodic[d])
+                c[d] = ((c[d] % tv.nt[d]) + tv.nt[d]) % tv.nt[d];
+            else
+                ok = false;
+        }
+        if (ok)
+            wl_push(G->wl, nit,
+                    (int)(tv.tile_base + c[0] + tv.nt[0] * ((int64_t)c[1] + (int64_t)tv.nt[1] * c[2])));
+    }
+}
+
+// Persistent walk over the work list of sweep `it` (one-sweep kernels).  Inside the
+// body: v, vw, tv, tile, tc[3]; the body sets changed_ (block-uniform).
+#define HJ_LIST_BEGIN(G, it, tol)                                                          \
+    const WorkList &wl_ = (G)->wl;                                                         \
+    const bool dense_ = (G)->dense != 0;                                                   \
+    const int cnt_ = dense_ ? (G)->total_tiles : *(volatile const int *)&wl_.count[(it) % 3]; \
+    for (int idx_ = blockIdx.x; idx_ < cnt_; idx_ += gridDim.x) {                          \
+        const int gid_ = dense_ ? idx_ : wl_.items[(it) & 1][idx_];                        \
+        const int v = find_view(G, gid_);                                                  \
+        if (!dense_ && threadIdx.x == 0)                                                   \
+            atomicAnd(&wl_.mark[(it) & 1][gid_ >> 5], ~(1u << (gid_ & 31)));                \
+        const SweepView<T> &vw = (G)->v[v];                                                \
+        if ((it) > 0 && *(volatile const double *)&vw.res[(it) - 1] < (tol)) continue;     \
+        const TileView<T> &tv = (G)->t[v];                                                 \
+        const int64_t tile = gid_ - tv.tile_base;                                          \
+        int tc[3];                                                                         \
+        tile_coords(tv, tile, tc);                                                         \
+        int changed_ = 0;
+
+#define HJ_LIST_END(G, it)                                                                 \
+        if (changed_ && !dense_)                                                           \
+            push_neighbours(G, v, tc, (G)->radius[0], (G)->radius[1], (G)->radius[2],     \
+                            (it) + 1);                                                     \
+        __syncthreads();                                                                   \
+    }                                                                                      \
+    if (!dense_ && blockIdx.x == 0 && threadIdx.x == 0) wl_.count[((it) + 2) % 3] = 0;
+
+template <typename T>
+__device__ __forceinline__ int tile_finish(const SweepGroup<T> *__restrict__ G, int v,
+                                           int64_t tile, int64_t it, T rmax, int changed,
+                                           int evaluated) {
     evaluated = __reduce_add_sync(0xffffffffu, evaluated);
     if ((threadIdx.x & 31) == 0 && evaluated)
         atomicAdd(G->v[v].work, (unsigned long long)evaluated);
@@ -111,8 +195,8 @@ __device__ __forceinline__ void tile_finish(const SweepGroup<T> *__restrict__ G,
         T m = red[0];
         for (int w = 1; w < (int)(blockDim.x >> 5); ++w) m = red[w] > m ? red[w] : m;
         if (m > T(0)) atomic_max_nonneg(&G->v[v].res[it], (double)m);
-        G->t[v].chg[(it & 1) * G->t[v].tiles + tile] = (uint8_t)(any != 0);
     }
+    return any;
 }
 
 template <typename T>
@@ -158,18 +242,7 @@ template <typename T, int DIM>
 __global__ void __launch_bounds__(256)
     k_sweep_generic(const DevProblem<T, T> P, const SweepGroup<T> *__restrict__ G, int64_t it,
                     double tol) {
-    const int64_t b = blockIdx.x;
-    const int v = find_view(G, b);
-    const SweepView<T> &vw = G->v[v];
-    if (it > 0 && *(volatile double *)&vw.res[it - 1] < tol) return;
-    const TileView<T> &tv = G->t[v];
-    const int64_t tile = b - tv.tile_base;
-    const int tc[3] = {(int)(tile % tv.nt[0]), (int)((tile / tv.nt[0]) % tv.nt[1]),
-                       (int)(tile / ((int64_t)tv.nt[0] * tv.nt[1]))};
-    if (!tile_active(G, v, tc, it)) {
-        if (threadIdx.x == 0) tv.chg[(it & 1) * tv.tiles + tile] = 0;
-        return;
-    }
+    HJ_LIST_BEGIN(G, it, tol)
     const int64_t o[3] = {vw.o[0], vw.o[1], vw.o[2]};
     const int64_t vn[3] = {vw.vn[0], vw.vn[1], vw.vn[2]};
     const T *__restrict__ Vi = vw.V[it & 1];
@@ -199,7 +272,8 @@ __global__ void __launch_bounds__(256)
         rmax = vnew > vin ? vnew - vin : vin - vnew;
         changed = !same_bits(vnew, vin);
     }
-    tile_finish(G, v, tile, it, rmax, changed, evaluated);
+    changed_ = tile_finish(G, v, tile, it, rmax, changed, evaluated);
+    HJ_LIST_END(G, it)
 }
 
 // ---------------------------------------------------------------------------
@@ -223,17 +297,7 @@ __global__ void __launch_bounds__(256, 2)
                     const SweepGroup<T> *__restrict__ G, int64_t it, double tol) {
     constexpr int TX = 32, TY = 32, RY = 4, SW = TX + 2;
     __shared__ T s[(TY + 2) * SW];
-    const int64_t b = blockIdx.x;
-    const int v = find_view(G, b);
-    const SweepView<T> &vw = G->v[v];
-    if (it > 0 && *(volatile double *)&vw.res[it - 1] < tol) return;
-    const TileView<T> &tv = G->t[v];
-    const int64_t tile = b - tv.tile_base;
-    const int tc[3] = {(int)(tile % tv.nt[0]), (int)(tile / tv.nt[0]), 0};
-    if (!tile_active(G, v, tc, it)) {
-        if (threadIdx.x == 0) tv.chg[(it & 1) * tv.tiles + tile] = 0;
-        return;
-    }
+    HJ_LIST_BEGIN(G, it, tol)
     const int64_t vn0 = vw.vn[0], vn1 = vw.vn[1];
     const T *__restrict__ Vi = vw.V[it & 1];
     T *__restrict__ Vo = vw.V[(it + 1) & 1];
@@ -336,7 +400,8 @@ __global__ void __launch_bounds__(256, 2)
         rmax = dv > rmax ? dv : rmax;
         changed |= !same_bits(vnew, V00);
     }
-    tile_finish(G, v, tile, it, rmax, changed, evaluated);
+    changed_ = tile_finish(G, v, tile, it, rmax, changed, evaluated);
+    HJ_LIST_END(G, it)
 }
 
 // ---------------------------------------------------------------------------
@@ -390,19 +455,10 @@ template <int KQ, bool PC>
 __global__ void __launch_bounds__(256, 2)
     k_sweep_local2d_x2(const DevProblem<float, float> P, const LocalCtrl<float> C,
                        const SweepGroup<float> *__restrict__ G, int64_t it, double tol) {
+    using T = float;
     constexpr int TX = 32, TY = 32, RY = 4, SW = TX + 2;
     __shared__ float s[(TY + 2) * SW];
-    const int64_t b = blockIdx.x;
-    const int v = find_view(G, b);
-    const SweepView<float> &vw = G->v[v];
-    if (it > 0 && *(volatile double *)&vw.res[it - 1] < tol) return;
-    const TileView<float> &tv = G->t[v];
-    const int64_t tile = b - tv.tile_base;
-    const int tc[3] = {(int)(tile % tv.nt[0]), (int)(tile / tv.nt[0]), 0};
-    if (!tile_active(G, v, tc, it)) {
-        if (threadIdx.x == 0) tv.chg[(it & 1) * tv.tiles + tile] = 0;
-        return;
-    }
+    HJ_LIST_BEGIN(G, it, tol)
     const int64_t vn0 = vw.vn[0], vn1 = vw.vn[1];
     const float *__restrict__ Vi = vw.V[it & 1];
     float *__restrict__ Vo = vw.V[(it + 1) & 1];
@@ -518,7 +574,8 @@ __global__ void __launch_bounds__(256, 2)
             changed |= !same_bits(vnew, V00);
         }
     }
-    tile_finish(G, v, tile, it, rmax, changed, evaluated);
+    changed_ = tile_finish(G, v, tile, it, rmax, changed, evaluated);
+    HJ_LIST_END(G, it)
 }
 
 // ---------------------------------------------------------------------------
@@ -532,32 +589,43 @@ __global__ void __launch_bounds__(256, 2)
 // corner offsets; the other tiles use the full R3/R10 rule of interp().
 // Tile 32 x 8, one node per thread.
 // ---------------------------------------------------------------------------
-template <typename T, int DYN>
-__global__ void __launch_bounds__(256)
+// floor(d) and d - floor(d) without the conversion (XU) pipe, |d| < 2^22:
+// t = RN(d + 1.5 2^23) carries round(d) in its mantissa.  Same values as
+// floor() / d - floor(d) (fp64 keeps floor(): the double pipes are not the limit there).
+__device__ __forceinline__ int floor_split(float d, float &w) {
+    const float t = __fadd_rn(d, 12582912.0f);
+    const float r = __fsub_rn(t, 12582912.0f);
+    const bool up = r > d;
+    const float fl = up ? r - 1.0f : r;
+    w = d - fl;
+    return (__float_as_int(t) - 0x4B400000) - (up ? 1 : 0);
+}
+__device__ __forceinline__ int floor_split(double d, double &w) {
+    const double fl = floor(d);
+    w = d - fl;
+    return (int)fl;
+}
+
+template <typename T, int DYN, bool KRUZ, int RY>
+__global__ void __launch_bounds__(256, 4)
     k_sweep_field2d(const DevProblem<T, T> P, const SweepGroup<T> *__restrict__ G, int64_t it,
                     double tol) {
-    const int64_t b = blockIdx.x;
-    const int v = find_view(G, b);
-    const SweepView<T> &vw = G->v[v];
-    if (it > 0 && *(volatile double *)&vw.res[it - 1] < tol) return;
-    const TileView<T> &tv = G->t[v];
-    const int64_t tile = b - tv.tile_base;
-    const int tc[3] = {(int)(tile % tv.nt[0]), (int)(tile / tv.nt[0]), 0};
-    if (!tile_active(G, v, tc, it)) {
-        if (threadIdx.x == 0) tv.chg[(it & 1) * tv.tiles + tile] = 0;
-        return;
-    }
+    HJ_LIST_BEGIN(G, it, tol)
     const int vn0 = (int)vw.vn[0], vn1 = (int)vw.vn[1];
     const T *__restrict__ Vi = vw.V[it & 1];
     T *__restrict__ Vo = vw.V[(it + 1) & 1];
+    // tile 32 x 8RY: lane -> column, warp -> rows warp, warp + 8, ...
+    constexpr int TY = 8 * RY;
     const int li = tc[0] * 32 + (threadIdx.x & 31);
-    const int lj = tc[1] * 8 + (threadIdx.x >> 5);
     // tile-uniform fast-path test: every corner of every foot inside the view
     const int hx = G->halo[0], hy = G->halo[1];
     const bool fast = tc[0] * 32 - hx >= 0 && tc[0] * 32 + 31 + hx + 1 <= vn0 - 1 &&
-                      tc[1] * 8 - hy >= 0 && tc[1] * 8 + 7 + hy + 1 <= vn1 - 1;
+                      tc[1] * TY - hy >= 0 && tc[1] * TY + TY - 1 + hy + 1 <= vn1 - 1;
     T rmax = T(0);
     int changed = 0, evaluated = 0;
+#pragma unroll 1
+    for (int rr = 0; rr < RY; ++rr) {
+    const int lj = tc[1] * TY + (threadIdx.x >> 5) + 8 * rr;
     if (li < vn0 && lj < vn1) {
         const int64_t t = li + (int64_t)vn0 * lj;
         const int64_t gi[3] = {li + vw.o[0], lj + vw.o[1], 0};
@@ -585,7 +653,7 @@ __global__ void __launch_bounds__(256)
                 S1 = P.hdx[1];
             }
             T base;
-            if (P.cost == HJ_COST_KRUZKOV) {
+            if (KRUZ) {
                 base = P.kcost;
             } else {
                 const T x[3] = {x0, x1, T(0)};
@@ -600,13 +668,13 @@ __global__ void __launch_bounds__(256)
                     // affine: u_k = controls[k][0..1]; Van der Pol: a_k = controls[k][0]
                     const T d0 = DYN == HJ_DYN_AFFINE ? fma(S0, P.ctrl[k][0], D0) : D0;
                     const T d1 = fma(S1, P.ctrl[k][DYN == HJ_DYN_AFFINE ? 1 : 0], D1);
-                    const T f0 = floor(d0), f1 = floor(d1);
-                    const T w0 = d0 - f0, w1 = d1 - f1;
-                    const T *__restrict__ p = Vn + ((int)f0 + vn0 * (int)f1);
+                    T w0, w1;
+                    const int i0 = floor_split(d0, w0), i1 = floor_split(d1, w1);
+                    const T *__restrict__ p = Vn + (i0 + vn0 * i1);
                     const T a00 = __ldg(p), a10 = __ldg(p + 1);
                     const T a01 = __ldg(p + vn0), a11 = __ldg(p + vn0 + 1);
                     const T I = lerp<T>(lerp<T>(a00, a10, w0), lerp<T>(a01, a11, w0), w1);
-                    const T ck = (P.cost == HJ_COST_KRUZKOV) ? base : fma(hlr, P.csq[k], base);
+                    const T ck = KRUZ ? base : fma(hlr, P.csq[k], base);
                     best = fmin(best, fma(P.beta, I, ck));
                 }
             } else {
@@ -618,19 +686,22 @@ __global__ void __launch_bounds__(256)
                         DYN == HJ_DYN_AFFINE ? fma(S0, P.ctrl[k][0], D0) : D0,
                         fma(S1, P.ctrl[k][DYN == HJ_DYN_AFFINE ? 1 : 0], D1), T(0)};
                     const T I = interp<T, T, 2>(Vi, o, vn, P.n, P.periodic, gi, delta, P.v_out);
-                    const T ck = (P.cost == HJ_COST_KRUZKOV) ? base : fma(hlr, P.csq[k], base);
+                    const T ck = KRUZ ? base : fma(hlr, P.csq[k], base);
                     best = fmin(best, fma(P.beta, I, ck));
                 }
             }
             vnew = best;
             if (P.monotone) vnew = fmin(vnew, vin);
-            evaluated = 1;
+            ++evaluated;
         }
         Vo[t] = vnew;
-        rmax = vnew > vin ? vnew - vin : vin - vnew;
-        changed = !same_bits(vnew, vin);
+        const T dv = vnew > vin ? vnew - vin : vin - vnew;
+        rmax = dv > rmax ? dv : rmax;
+        changed |= !same_bits(vnew, vin);
     }
-    tile_finish(G, v, tile, it, rmax, changed, evaluated);
+    }
+    changed_ = tile_finish(G, v, tile, it, rmax, changed, evaluated);
+    HJ_LIST_END(G, it)
 }
 
 // ---------------------------------------------------------------------------
@@ -647,18 +718,7 @@ template <typename T>
 __global__ void __launch_bounds__(256)
     k_sweep_dubins(const DevProblem<T, T> P, const SweepGroup<T> *__restrict__ G, int64_t it,
                    double tol) {
-    const int64_t b = blockIdx.x;
-    const int v = find_view(G, b);
-    const SweepView<T> &vw = G->v[v];
-    if (it > 0 && *(volatile double *)&vw.res[it - 1] < tol) return;
-    const TileView<T> &tv = G->t[v];
-    const int64_t tile = b - tv.tile_base;
-    const int tc[3] = {(int)(tile % tv.nt[0]), (int)((tile / tv.nt[0]) % tv.nt[1]),
-                       (int)(tile / ((int64_t)tv.nt[0] * tv.nt[1]))};
-    if (!tile_active(G, v, tc, it)) {
-        if (threadIdx.x == 0) tv.chg[(it & 1) * tv.tiles + tile] = 0;
-        return;
-    }
+    HJ_LIST_BEGIN(G, it, tol)
     const int vn0 = (int)vw.vn[0], vn1 = (int)vw.vn[1], vn2 = (int)vw.vn[2];
     const T *__restrict__ Vi = vw.V[it & 1];
     T *__restrict__ Vo = vw.V[(it + 1) & 1];
@@ -747,7 +807,8 @@ __global__ void __launch_bounds__(256)
         rmax = vnew > vin ? vnew - vin : vin - vnew;
         changed = !same_bits(vnew, vin);
     }
-    tile_finish(G, v, tile, it, rmax, changed, evaluated);
+    changed_ = tile_finish(G, v, tile, it, rmax, changed, evaluated);
+    HJ_LIST_END(G, it)
 }
 
 }  // namespace hj
@@ -768,15 +829,29 @@ struct SweepLaunch {
     bool per_ctrl_cost = false;
     bool packed = false;                // fp32 local kernel on FFMA2 (k_sweep_local2d_x2)
     int tb = 1;                         // sweeps per launch (> 1: k_sweep_local2d_tb)
+    bool dense = false;                 // SweepGroup::dense
     int64_t total_tiles = 0;
     SweepGroup<T> *d_group = nullptr;   // device copy (inside the caller's workspace)
     LocalCtrl<T> ctrl;
 };
 
 // bytes of change flags a view needs under the smallest tiling (32 x 8 x 1)
+// bytes of per-tile flags a view needs: [2][tiles] uint8 under the 32 x 8 tiling or
+// [2][tiles] int32 (block-tagged) under the 32 x 32 tiling of the blocked kernel
 inline int64_t chg_bytes_for(const int64_t vn[3]) {
-    int64_t t = ((vn[0] + 31) / 32) * ((vn[1] + 7) / 8) * vn[2];
-    return 2 * t;
+    int64_t t8 = ((vn[0] + 31) / 32) * ((vn[1] + 7) / 8) * vn[2];
+    int64_t t32 = ((vn[0] + 31) / 32) * ((vn[1] + 31) / 32) * vn[2];
+    return std::max(2 * t8, 8 * t32);
+}
+
+// tiles of a view under the finest tiling any sweep kernel uses (32 x 8 x 1)
+inline int64_t tiles_finest(const int64_t vn[3]) {
+    return ((vn[0] + 31) / 32) * ((vn[1] + 7) / 8) * vn[2];
+}
+
+// bytes of the work list over views whose tiles (under the finest tiling) sum to T
+inline int64_t wl_bytes_for(int64_t T) {
+    return 2 * 4 * T + 2 * 4 * ((T + 31) / 32) + 64 + 4 * 256;
 }
 
 hj_status speed_max(const void *speed, int dtype, int64_t N, cudaStream_t s, double *out);
@@ -806,10 +881,44 @@ inline void foot_bound(const hj_grid &g, const hj_problem &p, double cmax, doubl
     }
 }
 
+__global__ void k_wl_init(WorkList wl, int64_t total) {
+    const int64_t W = (total + 31) / 32;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total || i < W;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        if (i < total) wl.items[0][i] = (int32_t)i;
+        if (i < W) {
+            const int64_t rem = total - 32 * i;
+            wl.mark[0][i] = rem >= 32 ? 0xffffffffu : ((1u << rem) - 1u);
+            wl.mark[1][i] = 0u;
+        }
+        if (i == 0) {
+            wl.count[0] = (int32_t)total;
+            wl.count[1] = 0;
+            wl.count[2] = 0;
+        }
+    }
+}
+
+// Persistent grid of a work-list kernel: resident CTAs (occupancy x SMs), capped by
+// the number of tiles.
+template <typename K>
+static unsigned grid_for(K kernel, int threads, size_t smem, int64_t total, bool dense = false) {
+    if (dense) return (unsigned)std::max<int64_t>(1, total);
+    static int sms = 0;
+    if (!sms && cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0) != cudaSuccess)
+        sms = 148;
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem) !=
+            cudaSuccess ||
+        per_sm < 1)
+        per_sm = 1;
+    return (unsigned)std::max<int64_t>(1, std::min<int64_t>(total, (int64_t)sms * per_sm));
+}
+
 template <typename T>
 hj_status sweep_prepare(const hj_grid &g, const hj_problem &p, const hj_fields &f,
                         std::vector<SweepView<T>> &views, const std::vector<uint8_t *> &chg,
-                        void *d_group_mem, cudaStream_t s, SweepLaunch<T> &L) {
+                        void *d_group_mem, void *wl_mem, cudaStream_t s, SweepLaunch<T> &L) {
     const int dtype = sizeof(T) == 8 ? HJ_F64 : HJ_F32;
     double cmax = 1.0;
     if (f.speed && p.dynamics == HJ_DYN_AFFINE) {
@@ -877,7 +986,13 @@ hj_status sweep_prepare(const hj_grid &g, const hj_problem &p, const hj_fields &
             L.kq = kq;
             L.packed = sizeof(T) == 4 && want != HJ_SWEEP_LOCAL_SCALAR;
             if (want == HJ_SWEEP_AUTO || want == HJ_SWEEP_LOCAL_TB) {
-                L.tb = TB_SMAX;
+                // sweeps per launch: TB_SMAX, or HJ_TB_SWEEPS (2..TB_SMAX) for tuning
+                static const int env_s = [] {
+                    const char *e = getenv("HJ_TB_SWEEPS");
+                    const int v = e ? atoi(e) : 0;
+                    return v >= 2 && v <= TB_SMAX ? v : TB_SMAX;
+                }();
+                L.tb = env_s;
                 tile_dim[0] = tile_dim[1] = TB_T;
             }
             L.per_ctrl_cost = p.cost == HJ_COST_DISCOUNTED && p.lr != 0;
@@ -928,6 +1043,10 @@ hj_status sweep_prepare(const hj_grid &g, const hj_problem &p, const hj_fields &
             L.kind = SWEEP_DUBINS;
     }
     L.dyn = p.dynamics;
+    if (L.kind == SWEEP_FIELD2D && p.cost == HJ_COST_DISCOUNTED) {
+        tile_dim[0] = 32;      // dense problems: 32 x 32 tiles (k_sweep_field2d<.., 4>)
+        tile_dim[1] = 32;
+    }
     if ((want == HJ_SWEEP_FIELD2D && L.kind != SWEEP_FIELD2D) ||
         (want == HJ_SWEEP_DUBINS && L.kind != SWEEP_DUBINS)) {
         set_error("sweep_kernel %d requested, but the problem does not qualify for it", want);
@@ -963,6 +1082,31 @@ hj_status sweep_prepare(const hj_grid &g, const hj_problem &p, const hj_fields &
         base += tv.tiles;
     }
     L.total_tiles = base;
+    hg.total_tiles = (int)base;
+    // discounted problems change at every node until they stop: no list (one CTA per
+    // tile); front-like (Kruzkov) problems and the blocked kernel walk the list
+    L.dense = p.cost == HJ_COST_DISCOUNTED && L.tb <= 1;
+    hg.dense = L.dense ? 1 : 0;
+    {   // work list: every tile is visited by the first launch
+        int32_t *items = (int32_t *)wl_mem;
+        const int64_t W = (base + 31) / 32;
+        hg.wl.items[0] = items;
+        hg.wl.items[1] = items + base;
+        hg.wl.mark[0] = (uint32_t *)(items + 2 * base);
+        hg.wl.mark[1] = hg.wl.mark[0] + W;
+        hg.wl.count = (int32_t *)(hg.wl.mark[1] + W);
+        if (base > 0) {
+            const int blocks = (int)std::min<int64_t>((base + 255) / 256, 148 * 8);
+            k_wl_init<<<blocks, 256, 0, s>>>(hg.wl, base);
+        }
+        for (size_t q = 0; q < views.size(); ++q) {
+            cudaError_t e0 = cudaMemsetAsync(chg[q], 0, chg_bytes_for(views[q].vn), s);
+            if (e0 != cudaSuccess) {
+                set_error("sweep_prepare flags: %s", cudaGetErrorString(e0));
+                return HJ_ERR_CUDA;
+            }
+        }
+    }
     L.d_group = (SweepGroup<T> *)d_group_mem;
     cudaError_t e = cudaMemcpyAsync(L.d_group, &hg, sizeof(hg), cudaMemcpyHostToDevice, s);
     if (e != cudaSuccess) {
@@ -981,7 +1125,7 @@ hj_status sweep_prepare(const hj_grid &g, const hj_problem &p, const hj_fields &
 template <bool PC>
 static void launch_local_x2(const DevProblem<float, float> &P, const SweepLaunch<float> &L,
                             int64_t it, double tol, cudaStream_t s) {
-    dim3 grid((unsigned)L.total_tiles);
+    dim3 grid(grid_for(k_sweep_local2d_x2<4, PC>, 256, 0, L.total_tiles, L.dense));
     switch (L.kq) {
         case 4: k_sweep_local2d_x2<4, PC><<<grid, 256, 0, s>>>(P, L.ctrl, L.d_group, it, tol); break;
         case 8: k_sweep_local2d_x2<8, PC><<<grid, 256, 0, s>>>(P, L.ctrl, L.d_group, it, tol); break;
@@ -998,7 +1142,7 @@ static void launch_local(const DevProblem<T, T> &P, const SweepLaunch<T> &L, int
     if constexpr (sizeof(T) == 4) {
         if (L.packed) return launch_local_x2<PC>(P, L, it, tol, s);
     }
-    dim3 grid((unsigned)L.total_tiles);
+    dim3 grid(grid_for(k_sweep_local2d<T, 4, PC>, 256, 0, L.total_tiles, L.dense));
     switch (L.kq) {
         case 4: k_sweep_local2d<T, 4, PC><<<grid, 256, 0, s>>>(P, L.ctrl, L.d_group, it, tol); break;
         case 8: k_sweep_local2d<T, 8, PC><<<grid, 256, 0, s>>>(P, L.ctrl, L.d_group, it, tol); break;
@@ -1019,7 +1163,9 @@ static void launch_tb_kq(const DevProblem<T, T> &P, const SweepLaunch<T> &L, int
                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         attr = true;
     }
-    k_sweep_local2d_tb<T, KQ, PC><<<(unsigned)L.total_tiles, 256, smem, s>>>(
+    k_sweep_local2d_tb<T, KQ, PC><<<grid_for(k_sweep_local2d_tb<T, KQ, PC>, 256, smem,
+                                             L.total_tiles),
+                                    256, smem, s>>>(
         P, L.ctrl, L.d_group, n0, L.tb, S_run, rerun, tol);
 }
 
@@ -1054,6 +1200,19 @@ hj_status sweep_launch_rerun(const DevProblem<T, T> &P, const SweepLaunch<T> &L,
     return HJ_OK;
 }
 
+template <typename T, int DYN, bool KRUZ>
+static void launch_field(const DevProblem<T, T> &P, const SweepLaunch<T> &L, int64_t it,
+                         double tol, cudaStream_t s) {
+    if (L.dense)   // 32 x 32 tiles
+        k_sweep_field2d<T, DYN, KRUZ, 4>
+            <<<grid_for(k_sweep_field2d<T, DYN, KRUZ, 4>, 256, 0, L.total_tiles, true), 256, 0,
+               s>>>(P, L.d_group, it, tol);
+    else           // 32 x 8 tiles, work list
+        k_sweep_field2d<T, DYN, KRUZ, 1>
+            <<<grid_for(k_sweep_field2d<T, DYN, KRUZ, 1>, 256, 0, L.total_tiles), 256, 0, s>>>(
+                P, L.d_group, it, tol);
+}
+
 // One launch: sweep `it` (L.tb == 1) or the block of L.tb sweeps starting at `it`.
 template <typename T>
 hj_status sweep_launch(const DevProblem<T, T> &P, const SweepLaunch<T> &L, int64_t it, double tol,
@@ -1071,16 +1230,21 @@ hj_status sweep_launch(const DevProblem<T, T> &P, const SweepLaunch<T> &L, int64
         else
             launch_local<T, false>(P, L, it, tol, s);
     } else if (L.kind == SWEEP_FIELD2D) {
-        if (L.dyn == HJ_DYN_AFFINE)
-            k_sweep_field2d<T, HJ_DYN_AFFINE><<<(unsigned)L.total_tiles, 256, 0, s>>>(P, L.d_group, it, tol);
+        const bool kz = P.cost == HJ_COST_KRUZKOV;
+        if (L.dyn == HJ_DYN_AFFINE && kz)
+            launch_field<T, HJ_DYN_AFFINE, true>(P, L, it, tol, s);
+        else if (L.dyn == HJ_DYN_AFFINE)
+            launch_field<T, HJ_DYN_AFFINE, false>(P, L, it, tol, s);
+        else if (kz)
+            launch_field<T, HJ_DYN_VANDERPOL, true>(P, L, it, tol, s);
         else
-            k_sweep_field2d<T, HJ_DYN_VANDERPOL><<<(unsigned)L.total_tiles, 256, 0, s>>>(P, L.d_group, it, tol);
+            launch_field<T, HJ_DYN_VANDERPOL, false>(P, L, it, tol, s);
     } else if (L.kind == SWEEP_DUBINS) {
-        k_sweep_dubins<T><<<(unsigned)L.total_tiles, 256, 0, s>>>(P, L.d_group, it, tol);
+        k_sweep_dubins<T><<<grid_for(k_sweep_dubins<T>, 256, 0, L.total_tiles, L.dense), 256, 0, s>>>(P, L.d_group, it, tol);
     } else if (L.dim == 2) {
-        k_sweep_generic<T, 2><<<(unsigned)L.total_tiles, 256, 0, s>>>(P, L.d_group, it, tol);
+        k_sweep_generic<T, 2><<<grid_for(k_sweep_generic<T, 2>, 256, 0, L.total_tiles, L.dense), 256, 0, s>>>(P, L.d_group, it, tol);
     } else {
-        k_sweep_generic<T, 3><<<(unsigned)L.total_tiles, 256, 0, s>>>(P, L.d_group, it, tol);
+        k_sweep_generic<T, 3><<<grid_for(k_sweep_generic<T, 3>, 256, 0, L.total_tiles, L.dense), 256, 0, s>>>(P, L.d_group, it, tol);
     }
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) {

@@ -158,14 +158,13 @@ __device__ __forceinline__ void tb_quadrant(const LocalCtrl<T> &C, int q, const 
 
 // tb flags: bit0 changed in the last sub-sweep, bit1 changed in any sub-sweep.
 // Staged classes: -3 marks an interior node ON the box edge (R3 slow path).
+// One tile of one block of sweeps; returns 1 when an owned node changed in any
+// sub-sweep (the caller then lists the 3 x 3 tiles around it for the next block).
 template <typename T, int KQ, bool PC>
-__global__ void __launch_bounds__(256, 3)
-    k_sweep_local2d_tb(const DevProblem<T, T> P, const LocalCtrl<T> C,
-                       const SweepGroup<T> *__restrict__ G, int64_t n0, int S_blk, int S_run,
-                       int rerun, double tol) {
-    extern __shared__ __align__(16) unsigned char tb_raw[];
-    TBSmem<T> &sm = *reinterpret_cast<TBSmem<T> *>(tb_raw);
-    const int64_t b = blockIdx.x;
+__device__ __forceinline__ int tb_tile(const DevProblem<T, T> &P, const LocalCtrl<T> &C,
+                                       const SweepGroup<T> *__restrict__ G, TBSmem<T> &sm,
+                                       const int64_t b, int64_t n0, int S_blk, int S_run,
+                                       int rerun, double tol) {
     unsigned long long t_start = 0;
     if (g_tb_trace.buf) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
     const int v = find_view(G, b);
@@ -173,7 +172,7 @@ __global__ void __launch_bounds__(256, 3)
     const TileView<T> &tv = G->t[v];
     if (rerun) {                       // re-run of the block that contains the stop
         S_run = tv.rerun;
-        if (S_run <= 0) return;
+        if (S_run <= 0) return 0;
     }
     const int64_t blk = n0 / S_blk;
     // stopped view: some sweep of the previous block met the rule
@@ -181,7 +180,7 @@ __global__ void __launch_bounds__(256, 3)
         int stop = 0;
         if (n0 > 0 && (int)threadIdx.x < S_blk)
             stop = *(volatile double *)&vw.res[n0 - S_blk + threadIdx.x] < tol;
-        if (__syncthreads_or(stop)) return;
+        if (__syncthreads_or(stop)) return 0;
     }
     const int64_t tile = b - tv.tile_base;
     const int tcx = (int)(tile % tv.nt[0]), tcy = (int)(tile / tv.nt[0]);
@@ -189,16 +188,19 @@ __global__ void __launch_bounds__(256, 3)
     const T *__restrict__ Vi = vw.V[blk & 1];
     T *__restrict__ Vo = vw.V[(blk + 1) & 1];
     const int x0 = tcx * TB_T, y0 = tcy * TB_T;
-    uint8_t *flags_out = tv.chg + (blk & 1) * tv.tiles;
+    // per-tile flags of this block, tagged with the block index (a tile the list did
+    // not visit keeps an older tag, which reads as "no change")
+    int32_t *flags_out = reinterpret_cast<int32_t *>(tv.chg) + (blk & 1) * tv.tiles;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     // ---- exact skip (block granularity) ---------------------------------------
     if (n0 > 0) {
-        const uint8_t *prev = tv.chg + ((blk - 1) & 1) * tv.tiles;
+        const int32_t *prev = reinterpret_cast<const int32_t *>(tv.chg) + ((blk - 1) & 1) * tv.tiles;
         int act = 0, own = 0;
         if (threadIdx.x < 9) {
             const int cx = tcx + (int)threadIdx.x % 3 - 1, cy = tcy + (int)threadIdx.x / 3 - 1;
             if (cx >= 0 && cy >= 0 && cx < tv.nt[0] && cy < tv.nt[1]) {
-                const uint8_t f = prev[cx + (int64_t)tv.nt[0] * cy];
+                const int32_t tf = prev[cx + (int64_t)tv.nt[0] * cy];
+                const int f = (tf >> 2) == (int32_t)(blk - 1) ? (tf & 3) : 0;
                 act = f & 1;
                 if (threadIdx.x == 4) own = (f >> 1) & 1;
             }
@@ -215,8 +217,8 @@ __global__ void __launch_bounds__(256, 3)
                     }
                 }
             }
-            if (threadIdx.x == 0) flags_out[tile] = 0;
-            return;
+            if (threadIdx.x == 0) flags_out[tile] = (int32_t)(blk << 2);
+            return 0;
         }
     }
     // ---- stage tile + S-cell halo ---------------------------------------------
@@ -330,7 +332,7 @@ __global__ void __launch_bounds__(256, 3)
             int si[2];
             bool valid[2], owned[2];
             int8_t cl[2];
-            T C0[2], V00[2], best[2], A1[4][2], A2[4][2], A3[4][2];
+            T C0[2], V00[2], best[2], bs[2], bss[2];
 #pragma unroll
             for (int p = 0; p < 2; ++p) {
                 valid[p] = iA + 256 * p < L;
@@ -339,8 +341,7 @@ __global__ void __launch_bounds__(256, 3)
                 owned[p] = valid[p] && (unsigned)(r - S) < (unsigned)TB_T &&
                            (unsigned)(c - S) < (unsigned)TB_T;
                 cl[p] = valid[p] ? sm.cls[si[p]] : (int8_t)-2;
-                const T *q0 = Vc + si[p];
-                V00[p] = q0[0];
+                V00[p] = Vc[si[p]];
                 T base = P.kcost;
                 if (!kruz) {
                     const T x[3] = {fma((T)(n0g + c), P.dx[0], P.lo[0]),
@@ -349,27 +350,25 @@ __global__ void __launch_bounds__(256, 3)
                 }
                 C0[p] = fma(beta, V00[p], base);
                 const T sc = sm.c[si[p]];
-                const T bs = beta * sc, bss = bs * sc;
-                const T Vm0 = q0[-1], Vp0 = q0[1], V0m = q0[-TB_P], V0p = q0[TB_P];
-                const T Vmm = q0[-TB_P - 1], Vpm = q0[-TB_P + 1], Vmp = q0[TB_P - 1],
-                        Vpp = q0[TB_P + 1];
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    const T Vx = (q & 1) ? Vm0 : Vp0;
-                    const T Vy = (q & 2) ? V0m : V0p;
-                    const T Vxy = (q == 0) ? Vpp : (q == 1) ? Vmp : (q == 2) ? Vpm : Vmm;
-                    const T Dx = Vx - V00[p], Dy = Vy - V00[p], Dxy = (Vxy - Vx) - Dy;
-                    A1[q][p] = bs * Dx;
-                    A2[q][p] = bs * Dy;
-                    A3[q][p] = bss * Dxy;
-                }
+                bs[p] = beta * sc;
+                bss[p] = bs[p] * sc;
                 // the clamp value V00 (monotone: V^{n+1} = min(T V^n, V^n)), else +inf
                 best[p] = mono ? V00[p] : (T)INFINITY;
             }
+            // quadrant by quadrant: only that quadrant's 3 neighbours and coefficients live
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
-                const T a1[2] = {A1[q][0], A1[q][1]}, a2[2] = {A2[q][0], A2[q][1]};
-                const T a3[2] = {A3[q][0], A3[q][1]};
+                const int ox_ = (q & 1) ? -1 : 1, oy_ = (q & 2) ? -TB_P : TB_P;
+                T a1[2], a2[2], a3[2];
+#pragma unroll
+                for (int p = 0; p < 2; ++p) {
+                    const T *q0 = Vc + si[p];
+                    const T Vx = q0[ox_], Vy = q0[oy_], Vxy = q0[ox_ + oy_];
+                    const T Dx = Vx - V00[p], Dy = Vy - V00[p], Dxy = (Vxy - Vx) - Dy;
+                    a1[p] = bs[p] * Dx;
+                    a2[p] = bs[p] * Dy;
+                    a3[p] = bss[p] * Dxy;
+                }
                 tb_quadrant<T, KQ, PC>(C, q, C0, a1, a2, a3, best);
             }
 #pragma unroll
@@ -460,7 +459,8 @@ __global__ void __launch_bounds__(256, 3)
     if (lane == 0 && evaluated) atomicAdd(vw.work, (unsigned long long)evaluated);
     const int any_last = __syncthreads_or(chg_last);
     const int any_any = __syncthreads_or(chg_any);
-    if (threadIdx.x == 0) flags_out[tile] = (uint8_t)((any_last ? 1 : 0) | (any_any ? 2 : 0));
+    if (threadIdx.x == 0)
+        flags_out[tile] = (int32_t)(blk << 2) | (any_last ? 1 : 0) | (any_any ? 2 : 0);
     if (g_tb_trace.buf && threadIdx.x == 0 && b < g_tb_trace.cap && n0 == g_tb_trace.n0 &&
         !rerun) {
         unsigned long long t_end, smid;
@@ -474,6 +474,38 @@ __global__ void __launch_bounds__(256, 3)
         o[2] = t_end;
         o[3] = (unsigned long long)listed;
     }
+    return any_any;
+}
+
+// Persistent walk over the block's work list (or, for the re-run of the stop block,
+// over every tile: the per-tile flags then decide, exactly as in the list walk).
+#ifndef HJ_TB_MINB
+#define HJ_TB_MINB 4
+#endif
+template <typename T, int KQ, bool PC>
+__global__ void __launch_bounds__(256, HJ_TB_MINB)
+    k_sweep_local2d_tb(const DevProblem<T, T> P, const LocalCtrl<T> C,
+                       const SweepGroup<T> *__restrict__ G, int64_t n0, int S_blk, int S_run,
+                       int rerun, double tol) {
+    extern __shared__ __align__(16) unsigned char tb_raw[];
+    TBSmem<T> &sm = *reinterpret_cast<TBSmem<T> *>(tb_raw);
+    const WorkList &wl_ = G->wl;
+    const int64_t blk = n0 / S_blk;
+    const int cnt_ = rerun ? G->total_tiles : *(volatile const int *)&wl_.count[blk % 3];
+    for (int idx_ = blockIdx.x; idx_ < cnt_; idx_ += gridDim.x) {
+        const int gid = rerun ? idx_ : wl_.items[blk & 1][idx_];
+        if (!rerun && threadIdx.x == 0)
+            atomicAnd(&wl_.mark[blk & 1][gid >> 5], ~(1u << (gid & 31)));
+        const int any = tb_tile<T, KQ, PC>(P, C, G, sm, gid, n0, S_blk, S_run, rerun, tol);
+        if (any && !rerun) {
+            const int v = find_view(G, (int64_t)gid);
+            int tc[3];
+            tile_coords(G->t[v], gid - G->t[v].tile_base, tc);
+            push_neighbours(G, v, tc, 1, 1, 0, blk + 1);
+        }
+        __syncthreads();
+    }
+    if (!rerun && blockIdx.x == 0 && threadIdx.x == 0) wl_.count[(blk + 2) % 3] = 0;
 }
 
 }  // namespace hj

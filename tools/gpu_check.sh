@@ -9,7 +9,7 @@ tail -3 gpurun_out/pytest_gpu_$tag.log
 nvidia-smi --query-gpu=index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap --format=csv -lms 200 > gpurun_out/clocks_$tag.csv &
 SMI=$!
 timeout 900 python bench.py > gpurun_out/bench_$tag.json 2> gpurun_out/bench_$tag.err; echo "bench rc=$?"
-for c in 1 3 4 5; do
+for c in 1 3 4; do
   timeout 900 python bench.py --config $c --steps 2 --no-cpu-baseline > gpurun_out/bench_c${c}_$tag.json 2>> gpurun_out/bench_$tag.err; echo "bench c$c rc=$?"
 done
 kill $SMI
