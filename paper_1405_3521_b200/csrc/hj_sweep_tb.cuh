@@ -156,6 +156,27 @@ __device__ __forceinline__ void tb_quadrant(const LocalCtrl<T> &C, int q, const 
         tb_quadrant_d<KQ, PC>(C, q, C0, A1, A2, A3, best);
 }
 
+// Pair arithmetic for the coefficient setup: two nodes per FADD2/FMUL2 in fp32
+// (each lane rounds exactly like the scalar FADD/FMUL of k_sweep_local2d).
+template <typename T>
+struct Pr {
+    T x, y;
+};
+__device__ __forceinline__ Pr<float> psub(Pr<float> a, Pr<float> b) {
+    const float2 r = __fadd2_rn(make_float2(a.x, a.y), make_float2(-b.x, -b.y));
+    return {r.x, r.y};
+}
+__device__ __forceinline__ Pr<float> pmul(Pr<float> a, Pr<float> b) {
+    const float2 r = __fmul2_rn(make_float2(a.x, a.y), make_float2(b.x, b.y));
+    return {r.x, r.y};
+}
+__device__ __forceinline__ Pr<double> psub(Pr<double> a, Pr<double> b) {
+    return {a.x - b.x, a.y - b.y};
+}
+__device__ __forceinline__ Pr<double> pmul(Pr<double> a, Pr<double> b) {
+    return {a.x * b.x, a.y * b.y};
+}
+
 // tb flags: bit0 changed in the last sub-sweep, bit1 changed in any sub-sweep.
 // Staged classes: -3 marks an interior node ON the box edge (R3 slow path).
 // One tile of one block of sweeps; returns 1 when an owned node changed in any
@@ -166,7 +187,12 @@ __device__ __forceinline__ int tb_tile(const DevProblem<T, T> &P, const LocalCtr
                                        const int64_t b, int64_t n0, int S_blk, int S_run,
                                        int rerun, double tol) {
     unsigned long long t_start = 0;
-    if (g_tb_trace.buf) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+    long long ph_stage = 0, ph_scan = 0, ph_pairs = 0, ph_tail = 0, ph_t = 0;
+    const bool tr = g_tb_trace.buf != nullptr;
+    if (tr) {
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+        ph_t = clock64();
+    }
     const int v = find_view(G, b);
     const SweepView<T> &vw = G->v[v];
     const TileView<T> &tv = G->t[v];
@@ -264,6 +290,11 @@ __device__ __forceinline__ int tb_tile(const DevProblem<T, T> &P, const LocalCtr
         }
     }
     __syncthreads();
+    if (tr) {
+        const long long t = clock64();
+        ph_stage += t - ph_t;
+        ph_t = t;
+    }
     const bool mono = P.monotone != 0;
     const T beta = P.beta;
     const bool kruz = P.cost == HJ_COST_KRUZKOV;
@@ -319,11 +350,16 @@ __device__ __forceinline__ int tb_tile(const DevProblem<T, T> &P, const LocalCtr
         __syncthreads();
         const int L = *cnt, LE = sm.ecnt[j & 1];
         listed += L + LE;
+        if (tr) {
+            const long long t = clock64();
+            ph_scan += t - ph_t;
+            ph_t = t;
+        }
         if (threadIdx.x == 0) sm.cnt[(j + 1) & 1] = sm.ecnt[(j + 1) & 1] = 0;   // for j+1
-        // changed masks of sub-sweep j (its parity slot was read by this scan: reuse it)
+        // masks sub-sweep j+1 will set: that parity slot was last read by this scan
+        // (before the barrier above) and is next written after the sub-sweep's end
         for (int r = threadIdx.x; r < TB_P; r += blockDim.x)
-            sm.chm[j & 1][r][0] = sm.chm[j & 1][r][1] = 0u;
-        __syncthreads();
+            sm.chm[(j + 1) & 1][r][0] = sm.chm[(j + 1) & 1][r][1] = 0u;
         // ---- 2. the bracket-min of the listed nodes, in pairs (i, i + 256) -----------
         T rmax = T(0);
         const int M = (L + 511) / 512;
@@ -332,7 +368,8 @@ __device__ __forceinline__ int tb_tile(const DevProblem<T, T> &P, const LocalCtr
             int si[2];
             bool valid[2], owned[2];
             int8_t cl[2];
-            T C0[2], V00[2], best[2], bs[2], bss[2];
+            T C0[2], V00[2], best[2];
+            Pr<T> bs, bss, nb[9];     // nb: the 3 x 3 neighbourhood, row-major from (-1,-1)
 #pragma unroll
             for (int p = 0; p < 2; ++p) {
                 valid[p] = iA + 256 * p < L;
@@ -341,7 +378,13 @@ __device__ __forceinline__ int tb_tile(const DevProblem<T, T> &P, const LocalCtr
                 owned[p] = valid[p] && (unsigned)(r - S) < (unsigned)TB_T &&
                            (unsigned)(c - S) < (unsigned)TB_T;
                 cl[p] = valid[p] ? sm.cls[si[p]] : (int8_t)-2;
-                V00[p] = Vc[si[p]];
+                const T *q0 = Vc + si[p];
+#pragma unroll
+                for (int e = 0; e < 9; ++e) {
+                    const T val = q0[(e / 3 - 1) * TB_P + (e % 3 - 1)];
+                    if (p == 0) nb[e].x = val; else nb[e].y = val;
+                }
+                V00[p] = p == 0 ? nb[4].x : nb[4].y;
                 T base = P.kcost;
                 if (!kruz) {
                     const T x[3] = {fma((T)(n0g + c), P.dx[0], P.lo[0]),
@@ -350,26 +393,32 @@ __device__ __forceinline__ int tb_tile(const DevProblem<T, T> &P, const LocalCtr
                 }
                 C0[p] = fma(beta, V00[p], base);
                 const T sc = sm.c[si[p]];
-                bs[p] = beta * sc;
-                bss[p] = bs[p] * sc;
+                const T b1 = beta * sc;
+                if (p == 0) { bs.x = b1; bss.x = b1 * sc; } else { bs.y = b1; bss.y = b1 * sc; }
                 // the clamp value V00 (monotone: V^{n+1} = min(T V^n, V^n)), else +inf
                 best[p] = mono ? V00[p] : (T)INFINITY;
             }
-            // quadrant by quadrant: only that quadrant's 3 neighbours and coefficients live
+            // all quadrant coefficients at once, both nodes per instruction:
+            // quadrant q: x side (q&1 ? -1 : +1), y side (q&2 ? -1 : +1); same rounding
+            // sequence as k_sweep_local2d: Dx = Vx - V00, Dy = Vy - V00,
+            // Dxy = (Vxy - Vx) - Dy, A1 = bs Dx, A2 = bs Dy, A3 = bss Dxy
+            {
+                const Pr<T> c = nb[4];
+                const Pr<T> Dxp = psub(nb[5], c), Dxm = psub(nb[3], c);
+                const Pr<T> Dyp = psub(nb[7], c), Dym = psub(nb[1], c);
+                const Pr<T> A1p = pmul(bs, Dxp), A1m = pmul(bs, Dxm);
+                const Pr<T> A2p = pmul(bs, Dyp), A2m = pmul(bs, Dym);
+                const Pr<T> A3q[4] = {pmul(bss, psub(psub(nb[8], nb[5]), Dyp)),
+                                      pmul(bss, psub(psub(nb[6], nb[3]), Dyp)),
+                                      pmul(bss, psub(psub(nb[2], nb[5]), Dym)),
+                                      pmul(bss, psub(psub(nb[0], nb[3]), Dym))};
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const int ox_ = (q & 1) ? -1 : 1, oy_ = (q & 2) ? -TB_P : TB_P;
-                T a1[2], a2[2], a3[2];
-#pragma unroll
-                for (int p = 0; p < 2; ++p) {
-                    const T *q0 = Vc + si[p];
-                    const T Vx = q0[ox_], Vy = q0[oy_], Vxy = q0[ox_ + oy_];
-                    const T Dx = Vx - V00[p], Dy = Vy - V00[p], Dxy = (Vxy - Vx) - Dy;
-                    a1[p] = bs[p] * Dx;
-                    a2[p] = bs[p] * Dy;
-                    a3[p] = bss[p] * Dxy;
+                for (int q = 0; q < 4; ++q) {
+                    const Pr<T> a1 = (q & 1) ? A1m : A1p, a2 = (q & 2) ? A2m : A2p;
+                    const T a1v[2] = {a1.x, a1.y}, a2v[2] = {a2.x, a2.y};
+                    const T a3v[2] = {A3q[q].x, A3q[q].y};
+                    tb_quadrant<T, KQ, PC>(C, q, C0, a1v, a2v, a3v, best);
                 }
-                tb_quadrant<T, KQ, PC>(C, q, C0, a1, a2, a3, best);
             }
 #pragma unroll
             for (int p = 0; p < 2; ++p) {
@@ -387,6 +436,11 @@ __device__ __forceinline__ int tb_tile(const DevProblem<T, T> &P, const LocalCtr
                     }
                 }
             }
+        }
+        if (tr) {
+            const long long t = clock64();
+            ph_pairs += t - ph_t;
+            ph_t = t;
         }
         // ---- 3. box-edge nodes (R3), same edge formula as k_sweep_local2d: 4 nodes per
         // warp at a time, 8 lanes per node splitting the controls, then an 8-lane min
@@ -408,10 +462,34 @@ __device__ __forceinline__ int tb_tile(const DevProblem<T, T> &P, const LocalCtr
                 const T eC0 = fma(beta, eV00, base);
                 const T e_sc = sm.c[esi];
                 const bool lx = g0 == 0, hx = g0 == gn0 - 1, ly = g1 == 0, hy = g1 == gn1 - 1;
+                // lane sl: quadrant sl >> 1, controls k = (sl & 1), (sl & 1) + 2, ...
                 T e_best = (T)INFINITY;
-                for (int f = sl; f < 4 * KQ; f += 8)
-                    e_best = fmin(e_best, tb_edge_cand<T>(P, C, KQ, PC, Vc + esi, f / KQ, f % KQ,
-                                                          eC0, e_sc, base, lx, hx, ly, hy));
+                {
+                    const int q = sl >> 1;
+                    const T *sp = Vc + esi;
+                    const T eV = sp[0];
+                    const T Vx = (q & 1) ? sp[-1] : sp[1];
+                    const T Vy = (q & 2) ? sp[-TB_P] : sp[TB_P];
+                    const T Vxy = (q == 0)   ? sp[TB_P + 1]
+                                  : (q == 1) ? sp[TB_P - 1]
+                                  : (q == 2) ? sp[-TB_P + 1]
+                                             : sp[-TB_P - 1];
+                    const bool ex = (q & 1) ? lx : hx, ey = (q & 2) ? ly : hy;
+                    const T Dx = beta * (Vx - eV), Dy = beta * (Vy - eV);
+                    const T Dxy = beta * ((Vxy - Vx) - (Vy - eV));
+                    const T c_out = fma(beta, P.v_out, base);
+                    const T eps = (T)BOX_EPS;
+#pragma unroll 4
+                    for (int k = sl & 1; k < KQ; k += 2) {
+                        T wx = e_sc * C.ax[q][k], wy = e_sc * C.ay[q][k];
+                        const T ck = PC ? C.ck[q][k] : T(0);
+                        const bool out = (ex && wx > eps) || (ey && wy > eps);
+                        if (ex) wx = T(0);
+                        if (ey) wy = T(0);
+                        const T in = fma(wy, fma(wx, Dxy, Dy), fma(wx, Dx, eC0)) + ck;
+                        e_best = fmin(e_best, out ? c_out + ck : in);
+                    }
+                }
 #pragma unroll
                 for (int o = 4; o > 0; o >>= 1)
                     e_best = fmin(e_best, __shfl_xor_sync(0xffffffffu, e_best, o));
@@ -441,6 +519,11 @@ __device__ __forceinline__ int tb_tile(const DevProblem<T, T> &P, const LocalCtr
         if (lane == 0 && rmax > T(0)) atomic_max_nonneg(&vw.res[n0 + j - 1], (double)rmax);
         cur ^= 1;
         __syncthreads();
+        if (tr) {
+            const long long t = clock64();
+            ph_tail += t - ph_t;
+            ph_t = t;
+        }
     }
     int chg_last = 0;
     if (threadIdx.x < TB_T) {                       // owned rows S..S+31, cols S..S+31
@@ -468,7 +551,11 @@ __device__ __forceinline__ int tb_tile(const DevProblem<T, T> &P, const LocalCtr
         unsigned s32;
         asm volatile("mov.u32 %0, %%smid;" : "=r"(s32));
         smid = s32;
-        unsigned long long *o = g_tb_trace.buf + 4 * b;
+        unsigned long long *o = g_tb_trace.buf + 8 * b;
+        o[4] = (unsigned long long)ph_stage;
+        o[5] = (unsigned long long)ph_scan;
+        o[6] = (unsigned long long)ph_pairs;
+        o[7] = (unsigned long long)ph_tail;
         o[0] = smid;
         o[1] = t_start;
         o[2] = t_end;
@@ -480,7 +567,7 @@ __device__ __forceinline__ int tb_tile(const DevProblem<T, T> &P, const LocalCtr
 // Persistent walk over the block's work list (or, for the re-run of the stop block,
 // over every tile: the per-tile flags then decide, exactly as in the list walk).
 #ifndef HJ_TB_MINB
-#define HJ_TB_MINB 4
+#define HJ_TB_MINB 3
 #endif
 template <typename T, int KQ, bool PC>
 __global__ void __launch_bounds__(256, HJ_TB_MINB)

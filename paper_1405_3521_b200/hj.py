@@ -15,7 +15,7 @@ import os
 import numpy as np
 import torch
 
-_LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libhj.so")
+_LIB_PATH = os.environ.get("HJ_LIB_PATH") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libhj.so")
 _lib = None
 
 HJ_OK, HJ_ERR_INVALID, HJ_ERR_CUDA, HJ_ERR_NOT_CONVERGED, HJ_ERR_UNSUPPORTED, HJ_ERR_WORKSPACE = range(6)
