@@ -52,8 +52,10 @@ struct TileView {          // per-view tiling, filled by sweep_prepare
 // and zeroes count[(n+2)%3]; every visited tile clears its own mark bit.
 struct WorkList {
     int32_t *items[2];
-    int32_t *count;       // [3]
+    int32_t *count;       // [4]: the ring [0..2] and the live-tile count [3]
     uint32_t *mark[2];    // bitmaps over global tile ids
+    int32_t *live;        // tiles holding at least one interior node (the only ones that
+                          // can ever change: targets keep g, ghosts keep v_out)
 };
 
 template <typename T>
@@ -154,9 +156,9 @@ __device__ __forceinline__ void push_neighbours(const SweepGroup<T> *__restrict_
 #define HJ_LIST_BEGIN(G, it, tol)                                                          \
     const WorkList &wl_ = (G)->wl;                                                         \
     const bool dense_ = (G)->dense != 0;                                                   \
-    const int cnt_ = dense_ ? (G)->total_tiles : *(volatile const int *)&wl_.count[(it) % 3]; \
+    const int cnt_ = *(volatile const int *)&wl_.count[dense_ ? 3 : (it) % 3];              \
     for (int idx_ = blockIdx.x; idx_ < cnt_; idx_ += gridDim.x) {                          \
-        const int gid_ = dense_ ? idx_ : wl_.items[(it) & 1][idx_];                        \
+        const int gid_ = dense_ ? wl_.live[idx_] : wl_.items[(it) & 1][idx_];              \
         const int v = find_view(G, gid_);                                                  \
         if (!dense_ && threadIdx.x == 0)                                                   \
             atomicAnd(&wl_.mark[(it) & 1][gid_ >> 5], ~(1u << (gid_ & 31)));                \
@@ -851,7 +853,7 @@ inline int64_t tiles_finest(const int64_t vn[3]) {
 
 // bytes of the work list over views whose tiles (under the finest tiling) sum to T
 inline int64_t wl_bytes_for(int64_t T) {
-    return 2 * 4 * T + 2 * 4 * ((T + 31) / 32) + 64 + 4 * 256;
+    return 3 * 4 * T + 2 * 4 * ((T + 31) / 32) + 64 + 4 * 256;
 }
 
 hj_status speed_max(const void *speed, int dtype, int64_t N, cudaStream_t s, double *out);
@@ -881,21 +883,30 @@ inline void foot_bound(const hj_grid &g, const hj_problem &p, double cmax, doubl
     }
 }
 
-__global__ void k_wl_init(WorkList wl, int64_t total) {
-    const int64_t W = (total + 31) / 32;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total || i < W;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        if (i < total) wl.items[0][i] = (int32_t)i;
-        if (i < W) {
-            const int64_t rem = total - 32 * i;
-            wl.mark[0][i] = rem >= 32 ? 0xffffffffu : ((1u << rem) - 1u);
-            wl.mark[1][i] = 0u;
-        }
-        if (i == 0) {
-            wl.count[0] = (int32_t)total;
-            wl.count[1] = 0;
-            wl.count[2] = 0;
-        }
+// Initial work list: every tile with an interior node (class -1) — one CTA per tile.
+// The first launch visits exactly these; dense mode visits them at every sweep.
+template <typename T>
+__global__ void k_wl_live(const SweepGroup<T> *__restrict__ G) {
+    const int gid = blockIdx.x;
+    const int v = find_view(G, gid);
+    const SweepView<T> &vw = G->v[v];
+    const TileView<T> &tv = G->t[v];
+    int tc[3];
+    tile_coords(tv, gid - tv.tile_base, tc);
+    const int TX = G->tile_dim[0], TY = G->tile_dim[1], TZ = G->tile_dim[2];
+    int any = 0;
+    for (int e = threadIdx.x; e < TX * TY * TZ && !any; e += blockDim.x) {
+        const int64_t i = (int64_t)tc[0] * TX + e % TX, j = (int64_t)tc[1] * TY + (e / TX) % TY;
+        const int64_t k = (int64_t)tc[2] * TZ + e / (TX * TY);
+        if (i < vw.vn[0] && j < vw.vn[1] && k < vw.vn[2])
+            any = vw.cls[i + vw.vn[0] * (j + vw.vn[1] * k)] == -1;
+    }
+    if (__syncthreads_or(any) && threadIdx.x == 0) {
+        const WorkList &wl = G->wl;
+        const int pos = atomicAdd(&wl.count[3], 1);
+        wl.live[pos] = gid;
+        wl.items[0][atomicAdd(&wl.count[0], 1)] = gid;
+        atomicOr(&wl.mark[0][gid >> 5], 1u << (gid & 31));
     }
 }
 
@@ -903,7 +914,7 @@ __global__ void k_wl_init(WorkList wl, int64_t total) {
 // the number of tiles.
 template <typename K>
 static unsigned grid_for(K kernel, int threads, size_t smem, int64_t total, bool dense = false) {
-    if (dense) return (unsigned)std::max<int64_t>(1, total);
+    (void)dense;   // dense mode walks the live list too (persistent grid)
     static int sms = 0;
     if (!sms && cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0) != cudaSuccess)
         sms = 148;
@@ -1087,17 +1098,19 @@ hj_status sweep_prepare(const hj_grid &g, const hj_problem &p, const hj_fields &
     // tile); front-like (Kruzkov) problems and the blocked kernel walk the list
     L.dense = p.cost == HJ_COST_DISCOUNTED && L.tb <= 1;
     hg.dense = L.dense ? 1 : 0;
-    {   // work list: every tile is visited by the first launch
+    {   // work lists (filled by k_wl_live after the group upload below)
         int32_t *items = (int32_t *)wl_mem;
         const int64_t W = (base + 31) / 32;
         hg.wl.items[0] = items;
         hg.wl.items[1] = items + base;
-        hg.wl.mark[0] = (uint32_t *)(items + 2 * base);
+        hg.wl.live = items + 2 * base;
+        hg.wl.mark[0] = (uint32_t *)(items + 3 * base);
         hg.wl.mark[1] = hg.wl.mark[0] + W;
         hg.wl.count = (int32_t *)(hg.wl.mark[1] + W);
-        if (base > 0) {
-            const int blocks = (int)std::min<int64_t>((base + 255) / 256, 148 * 8);
-            k_wl_init<<<blocks, 256, 0, s>>>(hg.wl, base);
+        cudaError_t e1 = cudaMemsetAsync(hg.wl.mark[0], 0, (2 * W + 4) * sizeof(uint32_t), s);
+        if (e1 != cudaSuccess) {
+            set_error("sweep_prepare list: %s", cudaGetErrorString(e1));
+            return HJ_ERR_CUDA;
         }
         for (size_t q = 0; q < views.size(); ++q) {
             cudaError_t e0 = cudaMemsetAsync(chg[q], 0, chg_bytes_for(views[q].vn), s);
@@ -1113,6 +1126,7 @@ hj_status sweep_prepare(const hj_grid &g, const hj_problem &p, const hj_fields &
         set_error("sweep_prepare upload: %s", cudaGetErrorString(e));
         return HJ_ERR_CUDA;
     }
+    if (base > 0) k_wl_live<T><<<(unsigned)base, 128, 0, s>>>(L.d_group);
     // the host struct must outlive the async copy
     e = cudaStreamSynchronize(s);
     if (e != cudaSuccess) {

@@ -20,3 +20,8 @@ ncu --metrics gpu__time_duration.sum,launch__grid_size --clock-control none --cs
     --log-file gpurun_out/launches_$tag.csv python tools/prof_step.py 2 > gpurun_out/ncu_launch_$tag.log 2>&1
 echo "ncu rc=$?"
 python tools/launch_stats.py gpurun_out/launches_$tag.csv | head -20
+# the largest config (16385^2, 32 sub-domains): one timed step after the required warm-ups
+if [ "${WITH_C5:-0}" = "1" ]; then
+  timeout 2400 python bench.py --config 5 --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/bench_c5_$tag.json 2>> gpurun_out/bench_$tag.err; echo "bench c5 rc=$?"
+  cut -c1-600 gpurun_out/bench_c5_$tag.json
+fi

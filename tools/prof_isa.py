@@ -1,0 +1,26 @@
+"""One whole ISA pass (coarse solve, labels, partitioned fine solve) of a config, with
+stage times and per-sub-domain iteration counts: python tools/prof_isa.py CONFIG [REPS]"""
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+import hj_workloads as W  # noqa: E402
+from paper_1405_3521_b200 import hj, pipeline  # noqa: E402
+
+idx = int(sys.argv[1]) if len(sys.argv) > 1 else 2
+reps = int(sys.argv[2]) if len(sys.argv) > 2 else 1
+cfg = W.make(idx)
+fine = hj.DeviceProblem(cfg.fine, cfg.dtype)
+coarse = hj.DeviceProblem(cfg.coarse, cfg.dtype)
+for r in range(reps):
+    t0 = time.perf_counter()
+    res = pipeline.run_isa(cfg, cfg.dtype, fine=fine, coarse=coarse)
+    torch.cuda.synchronize()
+    reps_ = [x for x in res["reports"] if x]
+    print(f"config {idx}: wall {1e3 * (time.perf_counter() - t0):.1f} ms  stages "
+          f"{ {k: round(v, 2) for k, v in res['timings'].items()} }  sweeps per sub-domain "
+          f"{[x['iterations'] for x in reps_]}  box nodes {[p.box_nodes for p in res['plan']][:8]}...  "
+          f"evaluated {sum(x['evaluated_updates'] for x in reps_):.3e}", flush=True)
