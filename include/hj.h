@@ -82,16 +82,17 @@ enum {
 enum { HJ_COST_KRUZKOV = 0, HJ_COST_DISCOUNTED = 1 };
 
 /* Sweep kernels (all compute the same Jacobi sweep).  AUTO picks, in
- * order: LOCAL_TB when the problem qualifies for the local kernels (2-D, f = c(x) u_a,
- * every foot within one cell, no periodic axis): 8 sweeps per launch, temporally
- * blocked in shared memory, FFMA2-packed for fp32 — bit-identical iterates to the
+ * order: LOCAL_COOP when the problem qualifies for the local kernels (2-D, f = c(x) u_a,
+ * every foot within one cell, no periodic axis): the whole iteration in one cooperative
+ * launch over node-level dirty 8x8 mini-tiles (LOCAL_TB: 8 sweeps per launch, temporally
+ * blocked in shared memory) — FFMA2-packed for fp32, bit-identical iterates to the
  * one-sweep LOCAL_PACKED (fp32 only) / LOCAL_SCALAR kernels; FIELD2D for any other 2-D affine / Van der Pol problem without
  * periodic axes; DUBINS for Dubins dynamics whose heading step is <= 1 cell; GENERIC
  * otherwise.  The two LOCAL kernels give bit-identical iterates; the others evaluate
  * the same bracket in other operation orders (equal up to rounding). */
 enum { HJ_SWEEP_AUTO = 0, HJ_SWEEP_GENERIC = 1, HJ_SWEEP_LOCAL_SCALAR = 2,
        HJ_SWEEP_LOCAL_PACKED = 3, HJ_SWEEP_FIELD2D = 4, HJ_SWEEP_DUBINS = 5,
-       HJ_SWEEP_LOCAL_TB = 6 };
+       HJ_SWEEP_LOCAL_TB = 6, HJ_SWEEP_LOCAL_COOP = 7 };
 
 typedef struct {
     int32_t dim;            /* 2 or 3                                          */

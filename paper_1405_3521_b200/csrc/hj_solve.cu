@@ -191,6 +191,37 @@ template <typename T>
 static hj_status iterate(const DevProblem<T, T> &P, SweepLaunch<T> &L, int nv,
                          double *res_base, int64_t res_stride, double tol, int64_t max_iter,
                          cudaStream_t s, IterResult &out) {
+    if (L.coop) {   // the whole iteration in one cooperative launch
+        out.iters.assign(nv, max_iter);
+        out.resid.assign(nv, INFINITY);
+        out.converged.assign(nv, 0);
+        out.buf.assign(nv, 0);
+        cudaEvent_t c0, c1;
+        HJ_CUDA(cudaEventCreate(&c0));
+        HJ_CUDA(cudaEventCreate(&c1));
+        HJ_CUDA(cudaEventRecord(c0, s));
+        std::vector<int64_t> stop;
+        hj_status st = sweep_coop(P, L, max_iter, tol, s, stop);
+        if (st != HJ_OK) return st;
+        HJ_CUDA(cudaEventRecord(c1, s));
+        std::vector<double> last(nv, INFINITY);
+        for (int v = 0; v < nv; ++v)
+            if (stop[v] >= 1)
+                HJ_CUDA(cudaMemcpyAsync(&last[v], res_base + v * res_stride + stop[v] - 1,
+                                        sizeof(double), cudaMemcpyDeviceToHost, s));
+        HJ_CUDA(cudaStreamSynchronize(s));
+        HJ_CUDA(cudaEventElapsedTime(&out.ms, c0, c1));
+        cudaEventDestroy(c0);
+        cudaEventDestroy(c1);
+        for (int v = 0; v < nv; ++v) {
+            out.iters[v] = stop[v];
+            out.resid[v] = last[v];
+            out.converged[v] = last[v] < tol;
+            out.buf[v] = (int)(stop[v] & 1);
+        }
+        out.launches = 2;
+        return HJ_OK;
+    }
     const int S = std::max(1, L.tb);
     const int64_t B = S > 1 ? 4 * S : 16;          // sweeps per read-back batch
     double *pin = pinned_scratch((size_t)2 * nv * B);

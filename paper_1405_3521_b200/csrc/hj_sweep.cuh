@@ -815,6 +815,7 @@ __global__ void __launch_bounds__(256)
 
 }  // namespace hj
 #include "hj_sweep_tb.cuh"
+#include "hj_sweep_coop.cuh"
 namespace hj {
 
 // ---------------------------------------------------------------------------
@@ -831,6 +832,10 @@ struct SweepLaunch {
     bool per_ctrl_cost = false;
     bool packed = false;                // fp32 local kernel on FFMA2 (k_sweep_local2d_x2)
     int tb = 1;                         // sweeps per launch (> 1: k_sweep_local2d_tb)
+    bool coop = false;                  // whole iteration in k_sweep_local2d_coop
+    void *wl_mem = nullptr;             // work-list / cooperative-state region
+    std::vector<int64_t> vn0, vn1;      // view extents (cooperative mini-tiling)
+    int64_t gn0 = 0, gn1 = 0;           // grid extents
     bool dense = false;                 // SweepGroup::dense
     int64_t total_tiles = 0;
     SweepGroup<T> *d_group = nullptr;   // device copy (inside the caller's workspace)
@@ -851,9 +856,13 @@ inline int64_t tiles_finest(const int64_t vn[3]) {
     return ((vn[0] + 31) / 32) * ((vn[1] + 7) / 8) * vn[2];
 }
 
-// bytes of the work list over views whose tiles (under the finest tiling) sum to T
+// bytes of the work list over views whose tiles (under the finest tiling) sum to T;
+// the cooperative kernel's mini-tile state (8 x 8: <= 4 per 32 x 8 tile, 40 B each)
+// shares the same region, so the larger of the two is reserved
 inline int64_t wl_bytes_for(int64_t T) {
-    return 3 * 4 * T + 2 * 4 * ((T + 31) / 32) + 64 + 4 * 256;
+    const int64_t lists = 3 * 4 * T + 2 * 4 * ((T + 31) / 32) + 64 + 4 * 256;
+    const int64_t coop = 4 * T * (4 * 8 + 2 * 4) + 16 * 256 + 8 * HJ_MAX_SUBDOMAINS;
+    return std::max(lists, coop);
 }
 
 hj_status speed_max(const void *speed, int dtype, int64_t N, cudaStream_t s, double *out);
@@ -946,7 +955,7 @@ hj_status sweep_prepare(const hj_grid &g, const hj_problem &p, const hj_fields &
             if (p.A[d][e] != 0) iso = false;
     }
     const int want = p.sweep_kernel;
-    if (want < HJ_SWEEP_AUTO || want > HJ_SWEEP_LOCAL_TB) {
+    if (want < HJ_SWEEP_AUTO || want > HJ_SWEEP_LOCAL_COOP) {
         set_error("unknown sweep_kernel %d", want);
         return HJ_ERR_INVALID;
     }
@@ -957,7 +966,8 @@ hj_status sweep_prepare(const hj_grid &g, const hj_problem &p, const hj_fields &
     const bool local = iso && H[0] <= 1 + 1e-6 && H[1] <= 1 + 1e-6 && !g.periodic[0] &&
                        !g.periodic[1] &&
                        (want == HJ_SWEEP_AUTO || want == HJ_SWEEP_LOCAL_SCALAR ||
-                        want == HJ_SWEEP_LOCAL_PACKED || want == HJ_SWEEP_LOCAL_TB);
+                        want == HJ_SWEEP_LOCAL_PACKED || want == HJ_SWEEP_LOCAL_TB ||
+                        want == HJ_SWEEP_LOCAL_COOP);
     L.kind = SWEEP_GENERIC;
     int tile_dim[3] = {32, 8, 1};
     if (local) {
@@ -996,7 +1006,9 @@ hj_status sweep_prepare(const hj_grid &g, const hj_problem &p, const hj_fields &
             L.kind = SWEEP_LOCAL2D;
             L.kq = kq;
             L.packed = sizeof(T) == 4 && want != HJ_SWEEP_LOCAL_SCALAR;
-            if (want == HJ_SWEEP_AUTO || want == HJ_SWEEP_LOCAL_TB) {
+            if (want == HJ_SWEEP_AUTO || want == HJ_SWEEP_LOCAL_COOP) {
+                L.coop = true;
+            } else if (want == HJ_SWEEP_LOCAL_TB) {
                 // sweeps per launch: TB_SMAX, or HJ_TB_SWEEPS (2..TB_SMAX) for tuning
                 static const int env_s = [] {
                     const char *e = getenv("HJ_TB_SWEEPS");
@@ -1045,7 +1057,8 @@ hj_status sweep_prepare(const hj_grid &g, const hj_problem &p, const hj_fields &
         }
     }
     if (L.kind == SWEEP_GENERIC && want != HJ_SWEEP_GENERIC && want != HJ_SWEEP_LOCAL_SCALAR &&
-        want != HJ_SWEEP_LOCAL_PACKED && want != HJ_SWEEP_LOCAL_TB) {
+        want != HJ_SWEEP_LOCAL_PACKED && want != HJ_SWEEP_LOCAL_TB &&
+        want != HJ_SWEEP_LOCAL_COOP) {
         if (g.dim == 2 && (p.dynamics == HJ_DYN_AFFINE || p.dynamics == HJ_DYN_VANDERPOL) &&
             !g.periodic[0] && !g.periodic[1] && (want == HJ_SWEEP_AUTO || want == HJ_SWEEP_FIELD2D))
             L.kind = SWEEP_FIELD2D;
@@ -1064,7 +1077,7 @@ hj_status sweep_prepare(const hj_grid &g, const hj_problem &p, const hj_fields &
         return HJ_ERR_UNSUPPORTED;
     }
     if ((want == HJ_SWEEP_LOCAL_SCALAR || want == HJ_SWEEP_LOCAL_PACKED ||
-         want == HJ_SWEEP_LOCAL_TB) && L.kind != SWEEP_LOCAL2D) {
+         want == HJ_SWEEP_LOCAL_TB || want == HJ_SWEEP_LOCAL_COOP) && L.kind != SWEEP_LOCAL2D) {
         set_error("sweep_kernel %d requested, but the problem does not qualify for the local "
                   "kernel (2-D, f = c(x) u_a, foot within one cell, no periodic axis)", want);
         return HJ_ERR_UNSUPPORTED;
@@ -1107,7 +1120,15 @@ hj_status sweep_prepare(const hj_grid &g, const hj_problem &p, const hj_fields &
         hg.wl.mark[0] = (uint32_t *)(items + 3 * base);
         hg.wl.mark[1] = hg.wl.mark[0] + W;
         hg.wl.count = (int32_t *)(hg.wl.mark[1] + W);
-        cudaError_t e1 = cudaMemsetAsync(hg.wl.mark[0], 0, (2 * W + 4) * sizeof(uint32_t), s);
+        L.wl_mem = wl_mem;
+        for (size_t q = 0; q < views.size(); ++q) {
+            L.vn0.push_back(views[q].vn[0]);
+            L.vn1.push_back(views[q].vn[1]);
+        }
+        L.gn0 = g.n[0];
+        L.gn1 = g.dim > 1 ? g.n[1] : 1;
+        cudaError_t e1 = L.coop ? cudaSuccess
+                                : cudaMemsetAsync(hg.wl.mark[0], 0, (2 * W + 4) * sizeof(uint32_t), s);
         if (e1 != cudaSuccess) {
             set_error("sweep_prepare list: %s", cudaGetErrorString(e1));
             return HJ_ERR_CUDA;
@@ -1126,7 +1147,7 @@ hj_status sweep_prepare(const hj_grid &g, const hj_problem &p, const hj_fields &
         set_error("sweep_prepare upload: %s", cudaGetErrorString(e));
         return HJ_ERR_CUDA;
     }
-    if (base > 0) k_wl_live<T><<<(unsigned)base, 128, 0, s>>>(L.d_group);
+    if (base > 0 && !L.coop) k_wl_live<T><<<(unsigned)base, 128, 0, s>>>(L.d_group);
     // the host struct must outlive the async copy
     e = cudaStreamSynchronize(s);
     if (e != cudaSuccess) {
@@ -1211,6 +1232,87 @@ hj_status sweep_launch_rerun(const DevProblem<T, T> &P, const SweepLaunch<T> &L,
         set_error("sweep re-run launch failed: %s", cudaGetErrorString(e));
         return HJ_ERR_CUDA;
     }
+    return HJ_OK;
+}
+
+// The whole iteration of the local class in one cooperative launch (hj_sweep_coop.cuh).
+// stop[v] (host, out) = iterations performed by view v.
+template <typename T, int KQ, bool PC>
+static hj_status launch_coop_kq(const DevProblem<T, T> &P, const SweepLaunch<T> &L,
+                                const CoopState &S, int64_t max_iter, double tol,
+                                cudaStream_t s) {
+    static int grid = 0;
+    if (!grid) {
+        int sms = 148, per_sm = 0;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sweep_local2d_coop<T, KQ, PC>,
+                                                          256, 0) != cudaSuccess ||
+            per_sm < 1)
+            per_sm = 1;
+        grid = sms * per_sm;
+    }
+    const SweepGroup<T> *g = L.d_group;
+    void *args[] = {(void *)&P, (void *)&L.ctrl, (void *)&g, (void *)&S, (void *)&max_iter,
+                    (void *)&tol};
+    cudaError_t e = cudaLaunchCooperativeKernel((void *)k_sweep_local2d_coop<T, KQ, PC>,
+                                                dim3(grid), dim3(256), args, 0, s);
+    if (e != cudaSuccess) {
+        set_error("cooperative sweep launch failed: %s", cudaGetErrorString(e));
+        return HJ_ERR_CUDA;
+    }
+    return HJ_OK;
+}
+
+template <typename T>
+hj_status sweep_coop(const DevProblem<T, T> &P, const SweepLaunch<T> &L, int64_t max_iter,
+                     double tol, cudaStream_t s, std::vector<int64_t> &stop) {
+    const int nv = (int)L.vn0.size();
+    CoopState S;
+    memset(&S, 0, sizeof(S));
+    S.n_views = nv;
+    int64_t tot = 0;
+    for (int v = 0; v < nv; ++v) {
+        S.mt_base[v] = tot;
+        S.mt0[v] = (int32_t)((L.vn0[v] + 7) / 8);
+        S.mt1[v] = (int32_t)((L.vn1[v] + 7) / 8);
+        tot += (int64_t)S.mt0[v] * S.mt1[v];
+    }
+    S.mt_base[nv] = tot;
+    S.total = tot;
+    Carver c(L.wl_mem, (size_t)1 << 62);
+    S.imask = (unsigned long long *)c.take(8 * tot);
+    S.emask = (unsigned long long *)c.take(8 * tot);
+    S.dmask[0] = (unsigned long long *)c.take(8 * tot);
+    S.dmask[1] = (unsigned long long *)c.take(8 * tot);
+    S.items[0] = (int32_t *)c.take(4 * tot);
+    S.items[1] = (int32_t *)c.take(4 * tot);
+    S.count = (int32_t *)c.take(16);
+    S.stop = (int64_t *)c.take(8 * HJ_MAX_SUBDOMAINS);
+    HJ_CUDA(cudaMemsetAsync(S.count, 0, 16, s));
+    if (tot > 0) {
+        const int blocks = (int)std::min<int64_t>((tot + 255) / 256, 148 * 8);
+        k_coop_masks<T><<<blocks, 256, 0, s>>>(L.d_group, S, L.gn0, L.gn1);
+        HJ_CUDA(cudaGetLastError());
+    }
+    hj_status st = HJ_OK;
+    switch (L.kq) {
+        case 4: st = L.per_ctrl_cost ? launch_coop_kq<T, 4, true>(P, L, S, max_iter, tol, s)
+                                     : launch_coop_kq<T, 4, false>(P, L, S, max_iter, tol, s); break;
+        case 8: st = L.per_ctrl_cost ? launch_coop_kq<T, 8, true>(P, L, S, max_iter, tol, s)
+                                     : launch_coop_kq<T, 8, false>(P, L, S, max_iter, tol, s); break;
+        case 12: st = L.per_ctrl_cost ? launch_coop_kq<T, 12, true>(P, L, S, max_iter, tol, s)
+                                      : launch_coop_kq<T, 12, false>(P, L, S, max_iter, tol, s); break;
+        case 16: st = L.per_ctrl_cost ? launch_coop_kq<T, 16, true>(P, L, S, max_iter, tol, s)
+                                      : launch_coop_kq<T, 16, false>(P, L, S, max_iter, tol, s); break;
+        case 24: st = L.per_ctrl_cost ? launch_coop_kq<T, 24, true>(P, L, S, max_iter, tol, s)
+                                      : launch_coop_kq<T, 24, false>(P, L, S, max_iter, tol, s); break;
+        default: st = L.per_ctrl_cost ? launch_coop_kq<T, 32, true>(P, L, S, max_iter, tol, s)
+                                      : launch_coop_kq<T, 32, false>(P, L, S, max_iter, tol, s); break;
+    }
+    if (st != HJ_OK) return st;
+    stop.assign(nv, max_iter);
+    HJ_CUDA(cudaMemcpyAsync(stop.data(), S.stop, nv * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    HJ_CUDA(cudaStreamSynchronize(s));
     return HJ_OK;
 }
 

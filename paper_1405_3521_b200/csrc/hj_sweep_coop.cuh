@@ -1,0 +1,459 @@
+// hj_sweep_coop.cuh — the whole value iteration of the local 2-D class in ONE
+// cooperative launch (PAPER.md eq. (SL), (Tdef) line 238-245, stopping rule
+// line 341-345 / reading R6).
+//
+// Problem class: the one k_sweep_local2d handles (2-D, f = c(x) u_a, every foot within
+// one cell).  Work unit: an 8 x 8 "mini-tile" of a view plus a 64-bit mask of its nodes
+// whose T(V) can change in this sweep (a node of their 3 x 3 neighbourhood changed in
+// the previous one).  Every sweep the resident grid walks the list of mini-tiles with a
+// nonzero mask, a warp per mini-tile: it stages the 10 x 10 block of V^n around it in
+// shared memory, evaluates the listed nodes two per lane (FFMA2, the same per-node
+// arithmetic as k_sweep_local2d: bit-identical iterates), writes V^{n+1}, and ORs the
+// 3 x 3 dilation of its changed nodes into the masks of the 9 surrounding mini-tiles
+// for sweep n+1 — a mini-tile whose mask was empty is appended to the next list.  Then
+// one grid-wide barrier; every CTA reads the per-view residuals of sweep n and applies
+// the stopping rule itself (identical decisions everywhere), so the host never waits
+// per sweep.  No halo is recomputed, no tile is visited whose nodes cannot change, and
+// the node-level work is spread over all SMs every sweep.
+//
+// Nodes not recomputed hold the same value in both buffers (they did not change in the
+// previous sweep either), so nothing is copied; the final iterate of view v is in
+// V[stop_v & 1], stop_v = the first n with res[n-1] < tol (or max_iter).
+#pragma once
+
+#include <cooperative_groups.h>
+
+namespace hj {
+
+struct CoopState {
+    int64_t mt_base[HJ_MAX_SUBDOMAINS + 1];   // first global mini-tile id of each view
+    int32_t mt0[HJ_MAX_SUBDOMAINS], mt1[HJ_MAX_SUBDOMAINS];
+    unsigned long long *imask;      // [total] fast interior nodes (class -1)
+    unsigned long long *emask;      // [total] interior nodes on the box edge (class -3)
+    unsigned long long *dmask[2];   // [total] nodes to evaluate in sweep n (parity n)
+    int32_t *items[2];              // [total] mini-tiles with a nonzero mask (parity n)
+    int32_t *count;                 // [3] ring: sweep n reads count[n % 3]
+    int64_t *stop;                  // [n_views] iterations performed (output)
+    int n_views;
+    int64_t total;
+};
+
+__device__ __forceinline__ int coop_view(const CoopState &S, int64_t gid) {
+    int v = 0;
+    while (v + 1 < S.n_views && S.mt_base[v + 1] <= gid) ++v;
+    return v;
+}
+
+// classes of the mini-tiles of every view: one thread per mini-tile
+template <typename T>
+__global__ void k_coop_masks(const SweepGroup<T> *__restrict__ G, CoopState S, int64_t gn0,
+                             int64_t gn1) {
+    for (int64_t gid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; gid < S.total;
+         gid += (int64_t)gridDim.x * blockDim.x) {
+        const int v = coop_view(S, gid);
+        const SweepView<T> &vw = G->v[v];
+        const int64_t mt = gid - S.mt_base[v];
+        const int mx = (int)(mt % S.mt0[v]), my = (int)(mt / S.mt0[v]);
+        unsigned long long im = 0, em = 0;
+        for (int b = 0; b < 64; ++b) {
+            const int64_t li = (int64_t)mx * 8 + (b & 7), lj = (int64_t)my * 8 + (b >> 3);
+            if (li >= vw.vn[0] || lj >= vw.vn[1]) continue;
+            if (vw.cls[li + vw.vn[0] * lj] != -1) continue;
+            const int64_t g0 = li + vw.o[0], g1 = lj + vw.o[1];
+            if (g0 == 0 || g1 == 0 || g0 == gn0 - 1 || g1 == gn1 - 1)
+                em |= 1ull << b;
+            else
+                im |= 1ull << b;
+        }
+        S.imask[gid] = im;
+        S.emask[gid] = em;
+        S.dmask[0][gid] = im | em;     // sweep 0 evaluates every interior node
+        S.dmask[1][gid] = 0;
+    }
+}
+
+// the 3 x 3 dilation of an 8 x 8 change mask (bit = 8 row + col), restricted to the
+// mini-tile at offset (dx, dy) in {-1, 0, 1}^2
+__device__ __forceinline__ unsigned long long coop_spread(unsigned long long cm, int dx, int dy) {
+    const unsigned long long C0 = 0x0101010101010101ull, C7 = 0x8080808080808080ull;
+    const unsigned long long h = cm | ((cm << 1) & ~C0) | ((cm >> 1) & ~C7);
+    unsigned long long x;
+    if (dx == 0) {
+        x = h;                                       // columns stay
+    } else if (dx == 1) {
+        x = (cm & C7) >> 7;                          // our column 7 -> their column 0
+    } else {
+        x = (cm & C0) << 7;                          // our column 0 -> their column 7
+    }
+    const unsigned long long v = x | (x << 8) | (x >> 8);   // rows +-1
+    if (dy == 0) return v;
+    if (dy == 1) return (x >> 56) & 0xffull;                 // our row 7 -> their row 0
+    return (x & 0xffull) << 56;                              // our row 0 -> their row 7
+}
+
+// Phase B of one mini-tile: the listed nodes of block b (10 x 10, V^n staged), speeds
+// sp[64] (staged), classes masks di (interior) / de (box edge).  Writes V^{n+1} and
+// returns, per lane, the changed-node bits, the residual and the evaluated count.
+template <typename T, int KQ, bool PC>
+__device__ __forceinline__ void coop_eval(const DevProblem<T, T> &P, const LocalCtrl<T> &C,
+                                          const SweepView<T> &vw, const T *__restrict__ b,
+                                          const T *__restrict__ spd, int8_t *lstw,
+                                          unsigned long long di, unsigned long long de,
+                                          int64_t x0, int64_t y0, T *__restrict__ Vo,
+                                          T &rmax_out, unsigned long long &cm_out,
+                                          int &evald_out) {
+    constexpr int BP = 10;
+    const int lane = threadIdx.x & 31;
+    const bool mono = P.monotone != 0;
+    const bool kruz = P.cost == HJ_COST_KRUZKOV;
+    const T beta = P.beta, v_out = P.v_out;
+    const int64_t gn0 = P.n[0], gn1 = P.n[1];
+    const int64_t vn0 = vw.vn[0];
+    // compact the interior nodes: lane l takes bits l and l+32
+    const unsigned lt = (1u << lane) - 1u;
+    const unsigned dlo = (unsigned)di, dhi = (unsigned)(di >> 32);
+    const int plo = __popc(dlo), nI = plo + __popc(dhi);
+    if ((dlo >> lane) & 1u) lstw[__popc(dlo & lt)] = (int8_t)lane;
+    if ((dhi >> lane) & 1u) lstw[plo + __popc(dhi & lt)] = (int8_t)(32 + lane);
+    __syncwarp();
+            T rmax = T(0);
+    unsigned long long cm = 0;             // changed nodes (bit = local index)
+    int evald = 0;
+    if (nI > 0) {
+    int loc[2];
+    bool valid[2];
+    T C0[2], V00[2], best[2];
+    Pr<T> bs, bss, nb[9];
+#pragma unroll
+    for (int p = 0; p < 2; ++p) {
+        valid[p] = lane + 32 * p < nI;
+        loc[p] = valid[p] ? (int)lstw[lane + 32 * p] : 0;
+        const int r = loc[p] >> 3, c = loc[p] & 7;
+        const T *q0 = b + (r + 1) * BP + (c + 1);
+#pragma unroll
+        for (int e = 0; e < 9; ++e) {
+            const T val = q0[(e / 3 - 1) * BP + (e % 3 - 1)];
+            if (p == 0) nb[e].x = val; else nb[e].y = val;
+        }
+        V00[p] = p == 0 ? nb[4].x : nb[4].y;
+        const int64_t g0 = x0 + c + vw.o[0], g1 = y0 + r + vw.o[1];
+        T base = P.kcost;
+        if (!kruz) {
+            const T x[3] = {fma((T)g0, P.dx[0], P.lo[0]), fma((T)g1, P.dx[1], P.lo[1]),
+                            T(0)};
+            base = P.h * cost_state(P, x);
+        }
+        C0[p] = fma(beta, V00[p], base);
+        const T sc = spd[loc[p]];
+        const T b1 = beta * sc;
+        if (p == 0) { bs.x = b1; bss.x = b1 * sc; } else { bs.y = b1; bss.y = b1 * sc; }
+        best[p] = mono ? V00[p] : (T)INFINITY;
+    }
+    {   // quadrant coefficients, both nodes per instruction (k_sweep_local2d order)
+        const Pr<T> c = nb[4];
+        const Pr<T> Dxp = psub(nb[5], c), Dxm = psub(nb[3], c);
+        const Pr<T> Dyp = psub(nb[7], c), Dym = psub(nb[1], c);
+        const Pr<T> A1p = pmul(bs, Dxp), A1m = pmul(bs, Dxm);
+        const Pr<T> A2p = pmul(bs, Dyp), A2m = pmul(bs, Dym);
+        const Pr<T> A3q[4] = {pmul(bss, psub(psub(nb[8], nb[5]), Dyp)),
+                              pmul(bss, psub(psub(nb[6], nb[3]), Dyp)),
+                              pmul(bss, psub(psub(nb[2], nb[5]), Dym)),
+                              pmul(bss, psub(psub(nb[0], nb[3]), Dym))};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const Pr<T> a1 = (q & 1) ? A1m : A1p, a2 = (q & 2) ? A2m : A2p;
+            const T a1v[2] = {a1.x, a1.y}, a2v[2] = {a2.x, a2.y};
+            const T a3v[2] = {A3q[q].x, A3q[q].y};
+            tb_quadrant<T, KQ, PC>(C, q, C0, a1v, a2v, a3v, best);
+        }
+    }
+#pragma unroll
+    for (int p = 0; p < 2; ++p) {
+        if (!valid[p]) continue;
+        const int r = loc[p] >> 3, c = loc[p] & 7;
+        const T vnew = best[p];
+        Vo[(x0 + c) + vn0 * (y0 + r)] = vnew;
+        ++evald;
+        if (!same_bits(vnew, V00[p])) {
+            cm |= 1ull << loc[p];
+            const T dv = vnew > V00[p] ? vnew - V00[p] : V00[p] - vnew;
+            rmax = dv > rmax ? dv : rmax;
+        }
+    }
+    }
+    // box-edge nodes (R3): 4 at a time, 8 lanes per node (2 per quadrant)
+    const int nE = __popcll(de);
+    if (nE > 0) {
+    const int sg = lane >> 3, sl = lane & 7;
+    unsigned long long rest = de;
+    for (int e0 = 0; e0 < nE; e0 += 4) {
+        // the sg-th remaining set bit
+        unsigned long long mm = rest;
+        for (int s = 0; s < sg && mm; ++s) mm &= mm - 1;
+        const bool ok = mm != 0ull;
+        const int loc = ok ? __ffsll((long long)mm) - 1 : 0;
+        for (int s = 0; s < 4 && rest; ++s) rest &= rest - 1;
+        const int r = loc >> 3, c = loc & 7;
+        const T *sp = b + (r + 1) * BP + (c + 1);
+        const int64_t g0 = x0 + c + vw.o[0], g1 = y0 + r + vw.o[1];
+        T base = P.kcost;
+        if (!kruz) {
+            const T x[3] = {fma((T)g0, P.dx[0], P.lo[0]), fma((T)g1, P.dx[1], P.lo[1]),
+                            T(0)};
+            base = P.h * cost_state(P, x);
+        }
+        const T eV00 = sp[0];
+        const T eC0 = fma(beta, eV00, base);
+        const T e_sc = spd[loc];
+        const bool lx = g0 == 0, hx = g0 == gn0 - 1, ly = g1 == 0, hy = g1 == gn1 - 1;
+        T e_best = (T)INFINITY;
+        {
+            const int qd = sl >> 1;
+            const T Vx = (qd & 1) ? sp[-1] : sp[1];
+            const T Vy = (qd & 2) ? sp[-BP] : sp[BP];
+            const T Vxy = (qd == 0)   ? sp[BP + 1]
+                          : (qd == 1) ? sp[BP - 1]
+                          : (qd == 2) ? sp[-BP + 1]
+                                      : sp[-BP - 1];
+            const bool ex = (qd & 1) ? lx : hx, ey = (qd & 2) ? ly : hy;
+            const T Dx = beta * (Vx - eV00), Dy = beta * (Vy - eV00);
+            const T Dxy = beta * ((Vxy - Vx) - (Vy - eV00));
+            const T c_out = fma(beta, v_out, base);
+            const T eps = (T)BOX_EPS;
+#pragma unroll 4
+            for (int k = sl & 1; k < KQ; k += 2) {
+                T wx = e_sc * C.ax[qd][k], wy = e_sc * C.ay[qd][k];
+                const T ck = PC ? C.ck[qd][k] : T(0);
+                const bool out = (ex && wx > eps) || (ey && wy > eps);
+                if (ex) wx = T(0);
+                if (ey) wy = T(0);
+                const T in = fma(wy, fma(wx, Dxy, Dy), fma(wx, Dx, eC0)) + ck;
+                e_best = fmin(e_best, out ? c_out + ck : in);
+            }
+        }
+#pragma unroll
+        for (int o = 4; o > 0; o >>= 1)
+            e_best = fmin(e_best, __shfl_xor_sync(0xffffffffu, e_best, o));
+        if (ok && sl == 0) {
+            const T vnew = mono ? fmin(e_best, eV00) : e_best;
+            Vo[(x0 + c) + vn0 * (y0 + r)] = vnew;
+            ++evald;
+            if (!same_bits(vnew, eV00)) {
+                cm |= 1ull << loc;
+                const T dv = vnew > eV00 ? vnew - eV00 : eV00 - vnew;
+                rmax = dv > rmax ? dv : rmax;
+            }
+        }
+    }
+    }
+    rmax_out = rmax;
+    cm_out = cm;
+    evald_out = evald;
+}
+
+template <typename T, int KQ, bool PC>
+__global__ void __launch_bounds__(256, 2)
+    k_sweep_local2d_coop(const DevProblem<T, T> P, const LocalCtrl<T> C,
+                         const SweepGroup<T> *__restrict__ G, const CoopState S,
+                         int64_t max_iter, double tol) {
+    namespace cg = cooperative_groups;
+    cg::grid_group grid = cg::this_grid();
+    constexpr int BP = 10;                         // staged block pitch
+    __shared__ T blk[8][2][BP * BP];
+    __shared__ T spd[8][2][64];
+    __shared__ int8_t lst[8][2][64];
+    __shared__ int32_t qgid[256];
+    __shared__ unsigned long long qmask[256];
+    __shared__ int wcnt[8], qn;
+    __shared__ double cres[8][HJ_MAX_SUBDOMAINS];
+    __shared__ unsigned long long cwork[8][HJ_MAX_SUBDOMAINS];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t gwarp = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
+    const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    const bool mono = P.monotone != 0;
+    const bool kruz = P.cost == HJ_COST_KRUZKOV;
+    const T beta = P.beta, v_out = P.v_out;
+    const int64_t gn0 = P.n[0], gn1 = P.n[1];
+    unsigned stopped = 0;                          // bit v: view v met the rule
+    int64_t stop_at[HJ_MAX_SUBDOMAINS];
+    for (int v = 0; v < HJ_MAX_SUBDOMAINS; ++v) stop_at[v] = max_iter;
+    const unsigned all = S.n_views >= 32 ? 0xffffffffu : ((1u << S.n_views) - 1u);
+    int64_t n = 0;
+    const bool tr = g_tb_trace.buf != nullptr && blockIdx.x == 0 && threadIdx.x == 0;
+    unsigned long long t_a = 0, t_b = 0;
+    for (; n < max_iter && stopped != all; ++n) {
+        if (tr) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_a));
+        for (int v = lane; v < HJ_MAX_SUBDOMAINS; v += 32) {
+            cres[warp][v] = 0.0;
+            cwork[warp][v] = 0ull;
+        }
+        unsigned long long *dcur = S.dmask[n & 1], *dnext = S.dmask[(n + 1) & 1];
+        // CTA c owns the mini-tiles c, c + G, c + 2G, ... (strided: the active ones spread
+        // over all CTAs).  Chunks of 256 candidates: load their masks, compact the nonzero
+        // ones in shared memory, then the warps take two per iteration.
+        const int64_t per_cta = (S.total - blockIdx.x + gridDim.x - 1) / gridDim.x;
+        for (int64_t ch = 0; ch < per_cta; ch += 256) {
+        {
+            const int64_t k = ch + threadIdx.x;
+            const int64_t g = blockIdx.x + k * (int64_t)gridDim.x;
+            const unsigned long long m = k < per_cta ? dcur[g] : 0ull;
+            const unsigned bal = __ballot_sync(0xffffffffu, m != 0ull);
+            if (lane == 0) wcnt[warp] = __popc(bal);
+            __syncthreads();
+            int base_i = 0;
+            for (int w = 0; w < warp; ++w) base_i += wcnt[w];
+            if (m) {
+                const int pos = base_i + __popc(bal & ((1u << lane) - 1u));
+                qgid[pos] = (int32_t)g;
+                qmask[pos] = m;
+                dcur[g] = 0ull;                    // consumed
+            }
+            if (threadIdx.x == 0) {
+                int t = 0;
+                for (int w = 0; w < 8; ++w) t += wcnt[w];
+                qn = t;
+            }
+            __syncthreads();
+        }
+        const int cnt = qn;
+        // two mini-tiles per warp iteration: every global load of both (masks, the
+        // 10 x 10 blocks of V^n, the speeds) is issued before any is used, and the mask
+        // updates of both go out together
+        for (int it = warp; it < cnt; it += 16) {
+            int64_t gid[2];
+            gid[0] = qgid[it];
+            gid[1] = it + 8 < cnt ? (int64_t)qgid[it + 8] : (int64_t)-1;
+            int vv[2], mxy[2][2];
+            int64_t x0[2], y0[2];
+            unsigned long long dd[2], im[2], em[2];
+#pragma unroll
+            for (int s2 = 0; s2 < 2; ++s2) {
+                const int64_t g = gid[s2] < 0 ? gid[0] : gid[s2];
+                vv[s2] = coop_view(S, g);
+                const int64_t mt = g - S.mt_base[vv[s2]];
+                mxy[s2][0] = (int)(mt % S.mt0[vv[s2]]);
+                mxy[s2][1] = (int)(mt / S.mt0[vv[s2]]);
+                x0[s2] = (int64_t)mxy[s2][0] * 8;
+                y0[s2] = (int64_t)mxy[s2][1] * 8;
+                dd[s2] = gid[s2] >= 0 ? qmask[s2 ? it + 8 : it] : 0ull;
+                im[s2] = S.imask[g];
+                em[s2] = S.emask[g];
+            }
+            // staged V^n blocks and speeds, loads first
+            T ld[2][4], lsp[2][2];
+#pragma unroll
+            for (int s2 = 0; s2 < 2; ++s2) {
+                const SweepView<T> &vw = G->v[vv[s2]];
+                const int64_t vn0 = vw.vn[0], vn1 = vw.vn[1];
+                const T *__restrict__ Vi = vw.V[n & 1];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const int e = lane + 32 * k;
+                    const int64_t li = x0[s2] - 1 + e % BP, lj = y0[s2] - 1 + e / BP;
+                    ld[s2][k] = (e < BP * BP && li >= 0 && lj >= 0 && li < vn0 && lj < vn1)
+                                    ? Vi[li + vn0 * lj]
+                                    : v_out;
+                }
+#pragma unroll
+                for (int k = 0; k < 2; ++k) {
+                    const int e = lane + 32 * k;
+                    const int64_t li = x0[s2] + (e & 7), lj = y0[s2] + (e >> 3);
+                    lsp[s2][k] = (P.speed && li < vn0 && lj < vn1)
+                                     ? P.speed[(li + vw.o[0]) + gn0 * (lj + vw.o[1])]
+                                     : T(1);
+                }
+            }
+#pragma unroll
+            for (int s2 = 0; s2 < 2; ++s2) {
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    if (lane + 32 * k < BP * BP) blk[warp][s2][lane + 32 * k] = ld[s2][k];
+                spd[warp][s2][lane] = lsp[s2][0];
+                spd[warp][s2][lane + 32] = lsp[s2][1];
+            }
+            __syncwarp();
+            unsigned long long cmv[2] = {0ull, 0ull};
+#pragma unroll 1
+            for (int s2 = 0; s2 < 2; ++s2) {
+                const int v = vv[s2];
+                if (gid[s2] < 0 || ((stopped >> v) & 1u)) continue;
+                const SweepView<T> &vw = G->v[v];
+                T rmax;
+                unsigned long long cm;
+                int evald;
+                coop_eval<T, KQ, PC>(P, C, vw, blk[warp][s2], spd[warp][s2], lst[warp][s2],
+                                     dd[s2] & im[s2], dd[s2] & em[s2], x0[s2], y0[s2],
+                                     vw.V[(n + 1) & 1], rmax, cm, evald);
+                cm = ((unsigned long long)__reduce_or_sync(0xffffffffu, (unsigned)(cm >> 32)) << 32) |
+                     (unsigned long long)__reduce_or_sync(0xffffffffu, (unsigned)cm);
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    const T other = __shfl_xor_sync(0xffffffffu, rmax, o);
+                    rmax = other > rmax ? other : rmax;
+                }
+                evald = __reduce_add_sync(0xffffffffu, evald);
+                if (lane == 0) {
+                    cres[warp][v] = fmax(cres[warp][v], (double)rmax);
+                    cwork[warp][v] += (unsigned long long)evald;
+                }
+                cmv[s2] = cm;
+            }
+            // sweep n+1: the 3 x 3 dilation of the changed nodes into the 9 mini-tiles
+            // around each item (lanes 0-8: item 0, lanes 16-24: item 1)
+            {
+                const int s2 = lane >> 4, l9 = lane & 15;
+                const unsigned long long cm = cmv[s2];
+                if (cm && l9 < 9) {
+                    const int v = vv[s2];
+                    const int dx = l9 % 3 - 1, dy = l9 / 3 - 1;
+                    const int nx = mxy[s2][0] + dx, ny = mxy[s2][1] + dy;
+                    if (nx >= 0 && ny >= 0 && nx < S.mt0[v] && ny < S.mt1[v]) {
+                        const unsigned long long bits = coop_spread(cm, dx, dy);
+                        if (bits) {   // fire and forget: the scan finds it next sweep
+                            const int64_t nid = S.mt_base[v] + nx + (int64_t)S.mt0[v] * ny;
+                            atomicOr(&dnext[nid], bits);
+                        }
+                    }
+                }
+            }
+            __syncwarp();
+        }
+        __syncthreads();                           // the queue is reused by the next chunk
+        }
+        // per-CTA residual / work of this sweep, one atomic per view
+        __syncthreads();
+        if (threadIdx.x < (unsigned)S.n_views) {
+            const int v = threadIdx.x;
+            double m = 0.0;
+            unsigned long long w = 0;
+            for (int k = 0; k < 8; ++k) {
+                m = fmax(m, cres[k][v]);
+                w += cwork[k][v];
+            }
+            if (m > 0.0) atomic_max_nonneg(&G->v[v].res[n], m);
+            if (w) atomicAdd(G->v[v].work, w);
+        }
+        if (tr) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_b));
+        grid.sync();
+        if (tr && 4 * n + 3 < 4 * g_tb_trace.cap) {
+            unsigned long long t_c;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_c));
+            g_tb_trace.buf[4 * n] = t_a;
+            g_tb_trace.buf[4 * n + 1] = t_b;
+            g_tb_trace.buf[4 * n + 2] = t_c;
+            g_tb_trace.buf[4 * n + 3] = 0ull;
+        }
+        // the stopping rule, applied identically by every thread
+        for (int v = 0; v < S.n_views; ++v) {
+            if ((stopped >> v) & 1u) continue;
+            if (*(volatile const double *)&G->v[v].res[n] < tol) {
+                stopped |= 1u << v;
+                stop_at[v] = n + 1;
+            }
+        }
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0)
+        for (int v = 0; v < S.n_views; ++v) S.stop[v] = stop_at[v];
+}
+
+}  // namespace hj

@@ -33,6 +33,7 @@ namespace hj {
 constexpr int TB_T = 32;      // owned tile edge
 constexpr int TB_SMAX = 8;    // sub-sweeps per launch (max)
 constexpr int TB_P = TB_T + 2 * TB_SMAX;   // staged pitch (48)
+constexpr int TB_WSEG = 6 * (TB_P - 2);    // rows per warp (<= 6) x columns (<= 46)
 
 // Optional per-CTA trace (profiling aid, off unless hj_debug_set_trace was called):
 // [blockIdx] = {smid, start ns, end ns, computed nodes}.
@@ -47,15 +48,15 @@ template <typename T>
 struct TBSmem {
     T V[2][TB_P * TB_P];
     T c[TB_P * TB_P];           // speed c(x) (1 if none)
-    int16_t list[TB_P * TB_P];  // compacted dirty interior nodes of the sub-sweep
-    int16_t elist[4 * TB_P];    // compacted dirty box-edge nodes (R3 path)
+    int16_t list[8][TB_WSEG];   // dirty interior nodes, one segment per warp (its rows)
+    int16_t elist[8][128];      // dirty box-edge nodes (R3 path), one segment per warp
+    int wcnt[2][8], wecnt[2][8];  // segment lengths (parity of the sub-sweep)
     int8_t cls[TB_P * TB_P];    // -2 ghost / outside the view, -1 interior, -3 interior
                                 // on the box edge, >= 0 target
     // row bitmasks (bit c of word [r] = column c; the region is <= 48 < 64 wide)
     unsigned long long imask[TB_P];    // fast interior nodes (class -1)
     unsigned long long emask[TB_P];    // interior nodes on the box edge (class -3)
     unsigned int chm[2][TB_P][2];      // changed in the sub-sweep of that parity
-    int cnt[2], ecnt[2];
 };
 
 template <typename T>
@@ -300,7 +301,6 @@ __device__ __forceinline__ int tb_tile(const DevProblem<T, T> &P, const LocalCtr
     const bool kruz = P.cost == HJ_COST_KRUZKOV;
     int evaluated = 0, listed = 0, chg_any = 0;
     int cur = 0;
-    if (threadIdx.x == 0) sm.cnt[1] = sm.ecnt[1] = 0;
     for (int j = 1; j <= S; ++j) {
         const T *__restrict__ Vc = sm.V[cur];
         T *__restrict__ Vn = sm.V[cur ^ 1];
@@ -309,53 +309,56 @@ __device__ __forceinline__ int tb_tile(const DevProblem<T, T> &P, const LocalCtr
         // of its 3x3 neighbourhood changed in sub-sweep j-1 (chg == j-1; all at j = 1).
         // Nodes not recomputed keep their value in BOTH buffers (they did not change in
         // j-1 either), so nothing is copied.
-        int *cnt = &sm.cnt[j & 1];
         {
+            // warp w scans rows lo+w, lo+w+8, ... into its own segment: no atomics
             const unsigned (*pm)[2] = sm.chm[(j - 1) & 1];
-            const unsigned long long cols =
-                ((hi >= 63 ? ~0ull : ((1ull << (hi + 1)) - 1))) & ~((1ull << lo) - 1);
+            const unsigned clo = (lo >= 32 ? 0u : (~0u << lo)) &
+                                 (hi >= 31 ? ~0u : ((1u << (hi + 1)) - 1u));
+            const unsigned chi = (lo <= 32 ? ~0u : (~0u << (lo - 32))) &
+                                 (hi >= 63 ? ~0u : (hi < 32 ? 0u : ((1u << (hi - 31)) - 1u)));
+            const unsigned lt = (1u << lane) - 1u;
+            int16_t *seg = sm.list[warp];
+            int16_t *eseg = sm.elist[warp];
+            int n = 0, ne = 0;
             for (int r = lo + warp; r <= hi; r += 8) {
-                auto row = [&](int rr) -> unsigned long long {
-                    return (unsigned long long)pm[rr][0] | ((unsigned long long)pm[rr][1] << 32);
-                };
-                unsigned long long m = row(r - 1) | row(r) | row(r + 1);
-                m = (m | (m << 1) | (m >> 1)) & cols;
-                const unsigned long long dI = m & sm.imask[r], dE = m & sm.emask[r];
-                if (dI) {
-                    int base_i = 0;
-                    if (lane == 0) base_i = atomicAdd(cnt, __popcll(dI));
-                    base_i = __shfl_sync(0xffffffffu, base_i, 0);
-#pragma unroll
-                    for (int h = 0; h < 2; ++h) {
-                        const int c = lane + 32 * h;
-                        if ((dI >> c) & 1ull)
-                            sm.list[base_i + __popcll(dI & ((1ull << c) - 1))] =
-                                (int16_t)(r * TB_P + c);
-                    }
-                }
-                if (dE) {
-                    int base_i = 0;
-                    if (lane == 0) base_i = atomicAdd(&sm.ecnt[j & 1], __popcll(dE));
-                    base_i = __shfl_sync(0xffffffffu, base_i, 0);
-#pragma unroll
-                    for (int h = 0; h < 2; ++h) {
-                        const int c = lane + 32 * h;
-                        if ((dE >> c) & 1ull)
-                            sm.elist[base_i + __popcll(dE & ((1ull << c) - 1))] =
-                                (int16_t)(r * TB_P + c);
-                    }
-                }
+                const unsigned mlo = pm[r - 1][0] | pm[r][0] | pm[r + 1][0];
+                const unsigned mhi = pm[r - 1][1] | pm[r][1] | pm[r + 1][1];
+                const unsigned dlo = (mlo | (mlo << 1) | (mlo >> 1) | (mhi << 31)) & clo;
+                const unsigned dhi = (mhi | (mhi << 1) | (mhi >> 1) | (mlo >> 31)) & chi;
+                const unsigned long long im = sm.imask[r], em = sm.emask[r];
+                const unsigned ilo = dlo & (unsigned)im, ihi = dhi & (unsigned)(im >> 32);
+                const unsigned elo = dlo & (unsigned)em, ehi = dhi & (unsigned)(em >> 32);
+                const int pil = __popc(ilo), pel = __popc(elo);
+                if ((ilo >> lane) & 1u) seg[n + __popc(ilo & lt)] = (int16_t)(r * TB_P + lane);
+                if ((ihi >> lane) & 1u)
+                    seg[n + pil + __popc(ihi & lt)] = (int16_t)(r * TB_P + 32 + lane);
+                if ((elo >> lane) & 1u) eseg[ne + __popc(elo & lt)] = (int16_t)(r * TB_P + lane);
+                if ((ehi >> lane) & 1u)
+                    eseg[ne + pel + __popc(ehi & lt)] = (int16_t)(r * TB_P + 32 + lane);
+                n += pil + __popc(ihi);
+                ne += pel + __popc(ehi);
+            }
+            if (lane == 0) {
+                sm.wcnt[j & 1][warp] = n;
+                sm.wecnt[j & 1][warp] = ne;
             }
         }
         __syncthreads();
-        const int L = *cnt, LE = sm.ecnt[j & 1];
+        // segment offsets of the interior list (every thread, 8 entries)
+        int off[9];
+        off[0] = 0;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) off[w + 1] = off[w] + sm.wcnt[j & 1][w];
+        int LE = 0;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) LE += sm.wecnt[j & 1][w];
+        const int L = off[8];
         listed += L + LE;
         if (tr) {
             const long long t = clock64();
             ph_scan += t - ph_t;
             ph_t = t;
         }
-        if (threadIdx.x == 0) sm.cnt[(j + 1) & 1] = sm.ecnt[(j + 1) & 1] = 0;   // for j+1
         // masks sub-sweep j+1 will set: that parity slot was last read by this scan
         // (before the barrier above) and is next written after the sub-sweep's end
         for (int r = threadIdx.x; r < TB_P; r += blockDim.x)
@@ -373,7 +376,15 @@ __device__ __forceinline__ int tb_tile(const DevProblem<T, T> &P, const LocalCtr
 #pragma unroll
             for (int p = 0; p < 2; ++p) {
                 valid[p] = iA + 256 * p < L;
-                si[p] = valid[p] ? (int)sm.list[iA + 256 * p] : (S + 1) * TB_P + S + 1;
+                int sidx = (S + 1) * TB_P + S + 1;
+                if (valid[p]) {
+                    const int i = iA + 256 * p;
+                    int w = 0;
+#pragma unroll
+                    for (int u = 1; u < 8; ++u) w += i >= off[u];
+                    sidx = sm.list[w][i - off[w]];
+                }
+                si[p] = sidx;
                 const int r = si[p] / TB_P, c = si[p] - (si[p] / TB_P) * TB_P;
                 owned[p] = valid[p] && (unsigned)(r - S) < (unsigned)TB_T &&
                            (unsigned)(c - S) < (unsigned)TB_T;
@@ -442,6 +453,10 @@ __device__ __forceinline__ int tb_tile(const DevProblem<T, T> &P, const LocalCtr
             ph_pairs += t - ph_t;
             ph_t = t;
         }
+        int eoff[9];
+        eoff[0] = 0;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) eoff[w + 1] = eoff[w] + sm.wecnt[j & 1][w];
         // ---- 3. box-edge nodes (R3), same edge formula as k_sweep_local2d: 4 nodes per
         // warp at a time, 8 lanes per node splitting the controls, then an 8-lane min
         {
@@ -449,7 +464,13 @@ __device__ __forceinline__ int tb_tile(const DevProblem<T, T> &P, const LocalCtr
             for (int e0 = 4 * warp; e0 < LE; e0 += 32) {
                 const int e = e0 + sg;
                 const bool ok = e < LE;
-                const int esi = ok ? (int)sm.elist[e] : (S + 1) * TB_P + S + 1;
+                int esi = (S + 1) * TB_P + S + 1;
+                if (ok) {
+                    int w = 0;
+#pragma unroll
+                    for (int u = 1; u < 8; ++u) w += e >= eoff[u];
+                    esi = sm.elist[w][e - eoff[w]];
+                }
                 const int sr = esi / TB_P, scol = esi - sr * TB_P;
                 const int64_t g0 = n0g + scol, g1 = n1g + sr;
                 T base = P.kcost;

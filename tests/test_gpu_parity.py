@@ -70,8 +70,8 @@ def test_solve_matches_oracle(idx, dtype, oracle_cache):
         assert abs(rep["iterations"] - it_o) <= max(2, it_o // 10)   # fp32 residual noise
 
 
-KERNELS = {1: ("generic", "field2d", "local_scalar", "local_packed", "local_tb"),
-           2: ("generic", "field2d", "local_scalar", "local_packed", "local_tb"),
+KERNELS = {1: ("generic", "field2d", "local_scalar", "local_packed", "local_tb", "local_coop"),
+           2: ("generic", "field2d", "local_scalar", "local_packed", "local_tb", "local_coop"),
            3: ("generic", "field2d"), 4: ("generic", "dubins"), 5: ("generic", "field2d")}
 
 
@@ -100,20 +100,22 @@ def test_sweep_kernels_match_oracle(idx, dtype, oracle_cache):
     if "local_packed" in out:
         assert torch.equal(out["local_scalar"][0], out["local_packed"][0])
         assert out["local_scalar"][1] == out["local_packed"][1]
-    if "local_tb" in out:               # 8 sweeps per launch, same iterates bit for bit
-        assert torch.equal(out["local_scalar"][0], out["local_tb"][0])
-        assert out["local_scalar"][1] == out["local_tb"][1]
+    for k in ("local_tb", "local_coop"):   # blocked / cooperative: same iterates bit for bit
+        if k in out:
+            assert torch.equal(out["local_scalar"][0], out[k][0]), k
+            assert out["local_scalar"][1] == out[k][1], k
 
 
 @pytest.mark.parametrize("max_iter", [1, 5, 8, 13, 16])
-def test_local_tb_stops_inside_a_block(max_iter):
+@pytest.mark.parametrize("kernel", ["local_tb", "local_coop"])
+def test_local_tb_stops_inside_a_block(max_iter, kernel):
     """The temporally blocked kernel (8 sweeps per launch) must return exactly the
     iterate the one-sweep kernel returns, whatever sweep the stop lands on: a tol the
     iteration meets at sweep n* re-runs n*'s block with n* - 8 floor((n*-1)/8) sweeps;
     max_iter cut-offs inside a block end the last block early."""
     cfg = _cfg(2)
     ref = hj.DeviceProblem(cfg.fine, "f32", sweep_kernel="local_packed")
-    tb = hj.DeviceProblem(cfg.fine, "f32", sweep_kernel="local_tb")
+    tb = hj.DeviceProblem(cfg.fine, "f32", sweep_kernel=kernel)
     V1, r1 = hj.hj_solve(ref, max_iter=max_iter, allow_not_converged=True)
     V2, r2 = hj.hj_solve(tb, max_iter=max_iter, allow_not_converged=True)
     assert torch.equal(V1, V2) and r1["iterations"] == r2["iterations"] == max_iter

@@ -1,0 +1,36 @@
+"""Per-sweep timeline of the cooperative local kernel (block 0's view):
+python tools/coop_trace.py [CONFIG] — items, block-0 item phase, barrier wait, per sweep."""
+import ctypes
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import hj_workloads as W  # noqa: E402
+from paper_1405_3521_b200 import hj  # noqa: E402
+
+idx = int(sys.argv[1]) if len(sys.argv) > 1 else 2
+cfg = W.make(idx)
+dp = hj.DeviceProblem(cfg.fine, "f32", sweep_kernel="local_coop")
+cap = 1 << 16
+buf = torch.zeros(4 * cap, dtype=torch.int64, device="cuda")
+L = hj.lib()
+L.hj_debug_set_trace.argtypes = [ctypes.c_void_p, ctypes.c_longlong, ctypes.c_longlong]
+hj.hj_solve(dp)
+L.hj_debug_set_trace(buf.data_ptr(), cap, -1)
+V, rep = hj.hj_solve(dp)
+torch.cuda.synchronize()
+L.hj_debug_set_trace(None, 0, 0)
+t = buf.view(-1, 4).cpu().numpy()[: rep["iterations"]].astype(np.float64)
+items = t[:, 3]
+work = (t[:, 1] - t[:, 0]) / 1e3
+sync = (t[:, 2] - t[:, 1]) / 1e3
+gap = (t[1:, 0] - t[:-1, 2]) / 1e3
+print(f"sweeps {len(t)}  total {(t[-1, 2] - t[0, 0]) / 1e6:.2f} ms  device {rep['device_ms']:.2f} ms")
+for name, x in (("items", items), ("block0 work us", work), ("sync us", sync), ("post-sync us", gap)):
+    print(f"{name:15s} mean {x.mean():8.2f}  med {np.median(x):8.2f}  max {x.max():8.2f}")
+for k in (0, 100, 300, 500, 700):
+    if k < len(t):
+        print(f"  sweep {k}: items {int(items[k])} work {work[k]:.1f} us sync {sync[k]:.1f} us")
