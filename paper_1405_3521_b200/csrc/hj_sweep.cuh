@@ -1246,7 +1246,7 @@ static hj_status launch_coop_kq(const DevProblem<T, T> &P, const SweepLaunch<T> 
         int sms = 148, per_sm = 0;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
         if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sweep_local2d_coop<T, KQ, PC>,
-                                                          256, 0) != cudaSuccess ||
+                                                          CoopNW<T>::nw * 32, 0) != cudaSuccess ||
             per_sm < 1)
             per_sm = 1;
         grid = sms * per_sm;
@@ -1255,7 +1255,7 @@ static hj_status launch_coop_kq(const DevProblem<T, T> &P, const SweepLaunch<T> 
     void *args[] = {(void *)&P, (void *)&L.ctrl, (void *)&g, (void *)&S, (void *)&max_iter,
                     (void *)&tol};
     cudaError_t e = cudaLaunchCooperativeKernel((void *)k_sweep_local2d_coop<T, KQ, PC>,
-                                                dim3(grid), dim3(256), args, 0, s);
+                                                dim3(grid), dim3(CoopNW<T>::nw * 32), args, 0, s);
     if (e != cudaSuccess) {
         set_error("cooperative sweep launch failed: %s", cudaGetErrorString(e));
         return HJ_ERR_CUDA;

@@ -251,22 +251,31 @@ __device__ __forceinline__ void coop_eval(const DevProblem<T, T> &P, const Local
     evald_out = evald;
 }
 
+// warps per CTA: fp32 one 512-thread CTA per SM (fewer barrier arrivals); fp64 (its
+// staged blocks are twice the size) two 256-thread CTAs per SM
+template <typename T>
+struct CoopNW {
+    static constexpr int nw = sizeof(T) == 4 ? 16 : 8;
+    static constexpr int minb = sizeof(T) == 4 ? 1 : 2;
+};
+
 template <typename T, int KQ, bool PC>
-__global__ void __launch_bounds__(256, 2)
+__global__ void __launch_bounds__(CoopNW<T>::nw * 32, CoopNW<T>::minb)
     k_sweep_local2d_coop(const DevProblem<T, T> P, const LocalCtrl<T> C,
                          const SweepGroup<T> *__restrict__ G, const CoopState S,
                          int64_t max_iter, double tol) {
     namespace cg = cooperative_groups;
     cg::grid_group grid = cg::this_grid();
+    constexpr int COOP_NW = CoopNW<T>::nw;
     constexpr int BP = 10;                         // staged block pitch
-    __shared__ T blk[8][2][BP * BP];
-    __shared__ T spd[8][2][64];
-    __shared__ int8_t lst[8][2][64];
-    __shared__ int32_t qgid[256];
-    __shared__ unsigned long long qmask[256];
-    __shared__ int wcnt[8], qn;
-    __shared__ double cres[8][HJ_MAX_SUBDOMAINS];
-    __shared__ unsigned long long cwork[8][HJ_MAX_SUBDOMAINS];
+    __shared__ T blk[COOP_NW][2][BP * BP];
+    __shared__ T spd[COOP_NW][2][64];
+    __shared__ int8_t lst[COOP_NW][2][64];
+    __shared__ int32_t qgid[COOP_NW * 32];
+    __shared__ unsigned long long qmask[COOP_NW * 32];
+    __shared__ int wcnt[COOP_NW], qn;
+    __shared__ unsigned long long cres[HJ_MAX_SUBDOMAINS];    // per-CTA max (fp64 bits >= 0)
+    __shared__ unsigned long long cwork[HJ_MAX_SUBDOMAINS];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t gwarp = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
     const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
@@ -283,16 +292,17 @@ __global__ void __launch_bounds__(256, 2)
     unsigned long long t_a = 0, t_b = 0;
     for (; n < max_iter && stopped != all; ++n) {
         if (tr) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_a));
-        for (int v = lane; v < HJ_MAX_SUBDOMAINS; v += 32) {
-            cres[warp][v] = 0.0;
-            cwork[warp][v] = 0ull;
+        if (threadIdx.x < HJ_MAX_SUBDOMAINS) {
+            cres[threadIdx.x] = 0ull;
+            cwork[threadIdx.x] = 0ull;
         }
+        __syncthreads();
         unsigned long long *dcur = S.dmask[n & 1], *dnext = S.dmask[(n + 1) & 1];
         // CTA c owns the mini-tiles c, c + G, c + 2G, ... (strided: the active ones spread
         // over all CTAs).  Chunks of 256 candidates: load their masks, compact the nonzero
         // ones in shared memory, then the warps take two per iteration.
         const int64_t per_cta = (S.total - blockIdx.x + gridDim.x - 1) / gridDim.x;
-        for (int64_t ch = 0; ch < per_cta; ch += 256) {
+        for (int64_t ch = 0; ch < per_cta; ch += COOP_NW * 32) {
         {
             const int64_t k = ch + threadIdx.x;
             const int64_t g = blockIdx.x + k * (int64_t)gridDim.x;
@@ -310,7 +320,7 @@ __global__ void __launch_bounds__(256, 2)
             }
             if (threadIdx.x == 0) {
                 int t = 0;
-                for (int w = 0; w < 8; ++w) t += wcnt[w];
+                for (int w = 0; w < COOP_NW; ++w) t += wcnt[w];
                 qn = t;
             }
             __syncthreads();
@@ -319,10 +329,10 @@ __global__ void __launch_bounds__(256, 2)
         // two mini-tiles per warp iteration: every global load of both (masks, the
         // 10 x 10 blocks of V^n, the speeds) is issued before any is used, and the mask
         // updates of both go out together
-        for (int it = warp; it < cnt; it += 16) {
+        for (int it = warp; it < cnt; it += 2 * COOP_NW) {
             int64_t gid[2];
             gid[0] = qgid[it];
-            gid[1] = it + 8 < cnt ? (int64_t)qgid[it + 8] : (int64_t)-1;
+            gid[1] = it + COOP_NW < cnt ? (int64_t)qgid[it + COOP_NW] : (int64_t)-1;
             int vv[2], mxy[2][2];
             int64_t x0[2], y0[2];
             unsigned long long dd[2], im[2], em[2];
@@ -335,7 +345,7 @@ __global__ void __launch_bounds__(256, 2)
                 mxy[s2][1] = (int)(mt / S.mt0[vv[s2]]);
                 x0[s2] = (int64_t)mxy[s2][0] * 8;
                 y0[s2] = (int64_t)mxy[s2][1] * 8;
-                dd[s2] = gid[s2] >= 0 ? qmask[s2 ? it + 8 : it] : 0ull;
+                dd[s2] = gid[s2] >= 0 ? qmask[s2 ? it + COOP_NW : it] : 0ull;
                 im[s2] = S.imask[g];
                 em[s2] = S.emask[g];
             }
@@ -393,8 +403,9 @@ __global__ void __launch_bounds__(256, 2)
                 }
                 evald = __reduce_add_sync(0xffffffffu, evald);
                 if (lane == 0) {
-                    cres[warp][v] = fmax(cres[warp][v], (double)rmax);
-                    cwork[warp][v] += (unsigned long long)evald;
+                    if (rmax > T(0))
+                        atomicMax(&cres[v], (unsigned long long)__double_as_longlong((double)rmax));
+                    atomicAdd(&cwork[v], (unsigned long long)evald);
                 }
                 cmv[s2] = cm;
             }
@@ -424,12 +435,8 @@ __global__ void __launch_bounds__(256, 2)
         __syncthreads();
         if (threadIdx.x < (unsigned)S.n_views) {
             const int v = threadIdx.x;
-            double m = 0.0;
-            unsigned long long w = 0;
-            for (int k = 0; k < 8; ++k) {
-                m = fmax(m, cres[k][v]);
-                w += cwork[k][v];
-            }
+            const double m = __longlong_as_double((long long)cres[v]);
+            const unsigned long long w = cwork[v];
             if (m > 0.0) atomic_max_nonneg(&G->v[v].res[n], m);
             if (w) atomicAdd(G->v[v].work, w);
         }
