@@ -30,8 +30,8 @@
  *  - "device" pointers must be CUDA device (or managed) memory on the current
  *    device; "host" pointers are ordinary host memory.  Callers pass workspaces
  *    sized by the *_bytes / plan queries and own every buffer; the library's only
- *    own allocations are a 1.5 KB stream-ordered scratch inside hj_partition_plan
- *    (freed before it returns) and a small pinned host staging buffer per thread.  All device work is enqueued on
+ *    own allocations are a < 2 KB device scratch per device and thread (kept for the
+ *    process, allocated on first use) and a small pinned host staging buffer per thread.  All device work is enqueued on
  *    `stream` (a cudaStream_t, NULL = legacy default stream).
  *  - Value dtype: HJ_F32 or HJ_F64 selects the storage and arithmetic type of V
  *    and of the node fields speed/g.  Feedback and labelling decisions are
@@ -86,13 +86,15 @@ enum { HJ_COST_KRUZKOV = 0, HJ_COST_DISCOUNTED = 1 };
  * every foot within one cell, no periodic axis): the whole iteration in one cooperative
  * launch over node-level dirty 8x8 mini-tiles (LOCAL_TB: 8 sweeps per launch, temporally
  * blocked in shared memory) — FFMA2-packed for fp32, bit-identical iterates to the
- * one-sweep LOCAL_PACKED (fp32 only) / LOCAL_SCALAR kernels; FIELD2D for any other 2-D affine / Van der Pol problem without
- * periodic axes; DUBINS for Dubins dynamics whose heading step is <= 1 cell; GENERIC
+ * one-sweep LOCAL_PACKED (fp32 only) / LOCAL_SCALAR kernels; FIELD_COOP for any other 2-D
+ * affine / Van der Pol problem whose feet stay within one cell (the same cooperative
+ * scheme, the foot's cell picked by the signs of its offsets); FIELD2D for the other 2-D
+ * affine / Van der Pol problems without periodic axes; DUBINS for Dubins dynamics whose heading step is <= 1 cell; GENERIC
  * otherwise.  The two LOCAL kernels give bit-identical iterates; the others evaluate
  * the same bracket in other operation orders (equal up to rounding). */
 enum { HJ_SWEEP_AUTO = 0, HJ_SWEEP_GENERIC = 1, HJ_SWEEP_LOCAL_SCALAR = 2,
        HJ_SWEEP_LOCAL_PACKED = 3, HJ_SWEEP_FIELD2D = 4, HJ_SWEEP_DUBINS = 5,
-       HJ_SWEEP_LOCAL_TB = 6, HJ_SWEEP_LOCAL_COOP = 7 };
+       HJ_SWEEP_LOCAL_TB = 6, HJ_SWEEP_LOCAL_COOP = 7, HJ_SWEEP_FIELD_COOP = 8 };
 
 typedef struct {
     int32_t dim;            /* 2 or 3                                          */

@@ -148,8 +148,12 @@ __global__ void k_absmax(const T *__restrict__ x, int64_t N, unsigned long long 
 hj_status speed_max(const void *speed, int dtype, int64_t N, cudaStream_t s, double *out) {
     double *pin = pinned_scratch(1);
     HJ_CHECK(pin != nullptr, "cudaMallocHost failed");
-    unsigned long long *d;
-    HJ_CUDA(cudaMallocAsync(&d, sizeof(*d), s));
+    static thread_local unsigned long long *scratch[64] = {nullptr};   // per device, kept
+    int dev = 0;
+    HJ_CUDA(cudaGetDevice(&dev));
+    HJ_CHECK(dev >= 0 && dev < 64, "device index out of range");
+    if (!scratch[dev]) HJ_CUDA(cudaMalloc(&scratch[dev], sizeof(unsigned long long)));
+    unsigned long long *d = scratch[dev];
     HJ_CUDA(cudaMemsetAsync(d, 0, sizeof(*d), s));
     int blocks = (int)std::min<int64_t>((N + 255) / 256, 148 * 8);
     if (dtype == HJ_F64)
@@ -157,7 +161,6 @@ hj_status speed_max(const void *speed, int dtype, int64_t N, cudaStream_t s, dou
     else
         k_absmax<float><<<blocks, 256, 0, s>>>((const float *)speed, N, d);
     HJ_CUDA(cudaMemcpyAsync(pin, d, sizeof(double), cudaMemcpyDeviceToHost, s));
-    HJ_CUDA(cudaFreeAsync(d, s));
     HJ_CUDA(cudaStreamSynchronize(s));
     *out = pin[0];
     return HJ_OK;
@@ -622,10 +625,16 @@ hj_status hj_partition_plan(const hj_grid *grid, const uint32_t *fine_mask, int3
     HJ_CHECK(max_iter >= 1, "max_iter must be >= 1");
     cudaStream_t s = (cudaStream_t)stream;
     int64_t N = grid_nodes(*grid);
-    int *d_bb;
-    unsigned long long *d_cnt;
-    HJ_CUDA(cudaMallocAsync(&d_bb, sizeof(int) * 6 * HJ_MAX_SUBDOMAINS, s));
-    HJ_CUDA(cudaMallocAsync(&d_cnt, sizeof(unsigned long long) * HJ_MAX_SUBDOMAINS, s));
+    // a small device scratch kept for the process (one per device), not a per-call malloc
+    static thread_local void *scratch[64] = {nullptr};
+    int dev = 0;
+    HJ_CUDA(cudaGetDevice(&dev));
+    HJ_CHECK(dev >= 0 && dev < 64, "device index out of range");
+    if (!scratch[dev])
+        HJ_CUDA(cudaMalloc(&scratch[dev], sizeof(int) * 6 * HJ_MAX_SUBDOMAINS +
+                                              sizeof(unsigned long long) * HJ_MAX_SUBDOMAINS));
+    int *d_bb = (int *)scratch[dev];
+    unsigned long long *d_cnt = (unsigned long long *)(d_bb + 6 * HJ_MAX_SUBDOMAINS);
     k_fill_int<<<1, 6 * HJ_MAX_SUBDOMAINS, 0, s>>>(d_bb, 6 * HJ_MAX_SUBDOMAINS, 0x7fffffff, -1);
     HJ_CUDA(cudaMemsetAsync(d_cnt, 0, sizeof(unsigned long long) * HJ_MAX_SUBDOMAINS, s));
     int blocks = (int)std::min<int64_t>((N + 255) / 256, 148 * 8);
@@ -635,8 +644,6 @@ hj_status hj_partition_plan(const hj_grid *grid, const uint32_t *fine_mask, int3
     unsigned long long hcnt[HJ_MAX_SUBDOMAINS];
     HJ_CUDA(cudaMemcpyAsync(hbb, d_bb, sizeof(hbb), cudaMemcpyDeviceToHost, s));
     HJ_CUDA(cudaMemcpyAsync(hcnt, d_cnt, sizeof(hcnt), cudaMemcpyDeviceToHost, s));
-    HJ_CUDA(cudaFreeAsync(d_bb, s));
-    HJ_CUDA(cudaFreeAsync(d_cnt, s));
     HJ_CUDA(cudaStreamSynchronize(s));
     HJ_CUDA(cudaGetLastError());
     for (int k = 0; k < m; ++k) {

@@ -955,7 +955,7 @@ hj_status sweep_prepare(const hj_grid &g, const hj_problem &p, const hj_fields &
             if (p.A[d][e] != 0) iso = false;
     }
     const int want = p.sweep_kernel;
-    if (want < HJ_SWEEP_AUTO || want > HJ_SWEEP_LOCAL_COOP) {
+    if (want < HJ_SWEEP_AUTO || want > HJ_SWEEP_FIELD_COOP) {
         set_error("unknown sweep_kernel %d", want);
         return HJ_ERR_INVALID;
     }
@@ -1058,15 +1058,24 @@ hj_status sweep_prepare(const hj_grid &g, const hj_problem &p, const hj_fields &
     }
     if (L.kind == SWEEP_GENERIC && want != HJ_SWEEP_GENERIC && want != HJ_SWEEP_LOCAL_SCALAR &&
         want != HJ_SWEEP_LOCAL_PACKED && want != HJ_SWEEP_LOCAL_TB &&
-        want != HJ_SWEEP_LOCAL_COOP) {
+        want != HJ_SWEEP_LOCAL_COOP) {   // (FIELD_COOP: decided with FIELD2D)
         if (g.dim == 2 && (p.dynamics == HJ_DYN_AFFINE || p.dynamics == HJ_DYN_VANDERPOL) &&
-            !g.periodic[0] && !g.periodic[1] && (want == HJ_SWEEP_AUTO || want == HJ_SWEEP_FIELD2D))
+            !g.periodic[0] && !g.periodic[1] &&
+            (want == HJ_SWEEP_AUTO || want == HJ_SWEEP_FIELD2D || want == HJ_SWEEP_FIELD_COOP))
             L.kind = SWEEP_FIELD2D;
         else if (p.dynamics == HJ_DYN_DUBINS && H[2] <= 1.0 && !g.periodic[0] && !g.periodic[1] &&
                  (want == HJ_SWEEP_AUTO || want == HJ_SWEEP_DUBINS))
             L.kind = SWEEP_DUBINS;
     }
     L.dyn = p.dynamics;
+    if (L.kind == SWEEP_FIELD2D && H[0] <= 1.0 && H[1] <= 1.0 &&
+        (want == HJ_SWEEP_AUTO || want == HJ_SWEEP_FIELD_COOP))
+        L.coop = true;         // every foot within one cell: the cooperative kernel
+    if (want == HJ_SWEEP_FIELD_COOP && !(L.kind == SWEEP_FIELD2D && L.coop)) {
+        set_error("sweep_kernel %d requested, but the problem does not qualify for it "
+                  "(2-D affine / Van der Pol, feet within one cell)", want);
+        return HJ_ERR_UNSUPPORTED;
+    }
     if (L.kind == SWEEP_FIELD2D && p.cost == HJ_COST_DISCOUNTED) {
         tile_dim[0] = 32;      // dense problems: 32 x 32 tiles (k_sweep_field2d<.., 4>)
         tile_dim[1] = 32;
@@ -1237,7 +1246,7 @@ hj_status sweep_launch_rerun(const DevProblem<T, T> &P, const SweepLaunch<T> &L,
 
 // The whole iteration of the local class in one cooperative launch (hj_sweep_coop.cuh).
 // stop[v] (host, out) = iterations performed by view v.
-template <typename T, int KQ, bool PC>
+template <typename T, int KQ, bool PC, int EV = 0>
 static hj_status launch_coop_kq(const DevProblem<T, T> &P, const SweepLaunch<T> &L,
                                 const CoopState &S, int64_t max_iter, double tol,
                                 cudaStream_t s) {
@@ -1245,7 +1254,7 @@ static hj_status launch_coop_kq(const DevProblem<T, T> &P, const SweepLaunch<T> 
     if (!grid) {
         int sms = 148, per_sm = 0;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sweep_local2d_coop<T, KQ, PC>,
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sweep_local2d_coop<T, KQ, PC, EV>,
                                                           CoopNW<T>::nw * 32, 0) != cudaSuccess ||
             per_sm < 1)
             per_sm = 1;
@@ -1254,7 +1263,7 @@ static hj_status launch_coop_kq(const DevProblem<T, T> &P, const SweepLaunch<T> 
     const SweepGroup<T> *g = L.d_group;
     void *args[] = {(void *)&P, (void *)&L.ctrl, (void *)&g, (void *)&S, (void *)&max_iter,
                     (void *)&tol};
-    cudaError_t e = cudaLaunchCooperativeKernel((void *)k_sweep_local2d_coop<T, KQ, PC>,
+    cudaError_t e = cudaLaunchCooperativeKernel((void *)k_sweep_local2d_coop<T, KQ, PC, EV>,
                                                 dim3(grid), dim3(CoopNW<T>::nw * 32), args, 0, s);
     if (e != cudaSuccess) {
         set_error("cooperative sweep launch failed: %s", cudaGetErrorString(e));
@@ -1279,6 +1288,10 @@ hj_status sweep_coop(const DevProblem<T, T> &P, const SweepLaunch<T> &L, int64_t
     }
     S.mt_base[nv] = tot;
     S.total = tot;
+    // scan every mask each sweep while that is a few loads per thread of the grid;
+    // beyond, keep a list of the mini-tiles with a nonzero mask
+    S.use_list = tot > (int64_t)148 * 512 * 2 ? 1 : 0;
+    if (const char *e = getenv("HJ_COOP_LIST")) S.use_list = atoi(e) != 0;   // tests / tuning
     Carver c(L.wl_mem, (size_t)1 << 62);
     S.imask = (unsigned long long *)c.take(8 * tot);
     S.emask = (unsigned long long *)c.take(8 * tot);
@@ -1295,7 +1308,11 @@ hj_status sweep_coop(const DevProblem<T, T> &P, const SweepLaunch<T> &L, int64_t
         HJ_CUDA(cudaGetLastError());
     }
     hj_status st = HJ_OK;
-    switch (L.kq) {
+    if (L.kind == SWEEP_FIELD2D) {
+        st = L.dyn == HJ_DYN_AFFINE
+                 ? launch_coop_kq<T, 4, false, HJ_DYN_AFFINE + 1>(P, L, S, max_iter, tol, s)
+                 : launch_coop_kq<T, 4, false, HJ_DYN_VANDERPOL + 1>(P, L, S, max_iter, tol, s);
+    } else switch (L.kq) {
         case 4: st = L.per_ctrl_cost ? launch_coop_kq<T, 4, true>(P, L, S, max_iter, tol, s)
                                      : launch_coop_kq<T, 4, false>(P, L, S, max_iter, tol, s); break;
         case 8: st = L.per_ctrl_cost ? launch_coop_kq<T, 8, true>(P, L, S, max_iter, tol, s)

@@ -34,6 +34,7 @@ struct CoopState {
     int32_t *items[2];              // [total] mini-tiles with a nonzero mask (parity n)
     int32_t *count;                 // [3] ring: sweep n reads count[n % 3]
     int64_t *stop;                  // [n_views] iterations performed (output)
+    int use_list;                   // 1: walk items/count (many mini-tiles); 0: scan all
     int n_views;
     int64_t total;
 };
@@ -69,6 +70,7 @@ __global__ void k_coop_masks(const SweepGroup<T> *__restrict__ G, CoopState S, i
         S.emask[gid] = em;
         S.dmask[0][gid] = im | em;     // sweep 0 evaluates every interior node
         S.dmask[1][gid] = 0;
+        if (S.use_list && (im | em)) S.items[0][atomicAdd(&S.count[0], 1)] = (int32_t)gid;
     }
 }
 
@@ -251,6 +253,117 @@ __device__ __forceinline__ void coop_eval(const DevProblem<T, T> &P, const Local
     evald_out = evald;
 }
 
+// Phase B for the FIELD class with every foot within one cell (|delta_d| <= 1, e.g. the
+// Zermelo drift of config 3): per control the foot's cell is the quadrant given by the
+// signs of its offsets, so the bilinear interpolant is
+//   V00 + |d0| D0(s0) + |d1| (D1(s1) + |d0| D01(s0,s1))
+// with the node's 4 one-sided and 4 cross differences (prescaled by beta) selected by
+// sign — no floor, no index arithmetic.  Box-edge nodes (class -3) take the general R3
+// interpolation (interp()) on the global V^n, as k_sweep_field2d's slow path.
+template <typename T, int DYN>
+__device__ __forceinline__ void coop_eval_field(const DevProblem<T, T> &P, const SweepView<T> &vw,
+                                                const T *__restrict__ Vi, const T *__restrict__ b,
+                                                const T *__restrict__ spd, int8_t *lstw,
+                                                unsigned long long di, unsigned long long de,
+                                                int64_t x0, int64_t y0, T *__restrict__ Vo,
+                                                T &rmax_out, unsigned long long &cm_out,
+                                                int &evald_out) {
+    constexpr int BP = 10;
+    const int lane = threadIdx.x & 31;
+    const bool mono = P.monotone != 0;
+    const bool kruz = P.cost == HJ_COST_KRUZKOV;
+    const T beta = P.beta;
+    const int64_t vn0 = vw.vn[0];
+    const T hlr = P.h * P.lr;
+    // every listed node (interior and box edge) is one lane-slot: lane l takes the l-th
+    // and (l+32)-th set bit of di | de
+    const unsigned long long dall = di | de;
+    const unsigned lt = (1u << lane) - 1u;
+    const unsigned dlo = (unsigned)dall, dhi = (unsigned)(dall >> 32);
+    const int plo = __popc(dlo), nN = plo + __popc(dhi);
+    if ((dlo >> lane) & 1u) lstw[__popc(dlo & lt)] = (int8_t)lane;
+    if ((dhi >> lane) & 1u) lstw[plo + __popc(dhi & lt)] = (int8_t)(32 + lane);
+    __syncwarp();
+    T rmax = T(0);
+    unsigned long long cm = 0;
+    int evald = 0;
+#pragma unroll 1
+    for (int p = 0; p < 2; ++p) {
+        const int slot = lane + 32 * p;
+        if (slot >= nN) continue;
+        const int loc = lstw[slot];
+        const int r = loc >> 3, c = loc & 7;
+        const T *q0 = b + (r + 1) * BP + (c + 1);
+        const T V00 = q0[0];
+        const int64_t gi[3] = {x0 + c + vw.o[0], y0 + r + vw.o[1], 0};
+        const T xx0 = fma((T)gi[0], P.dx[0], P.lo[0]), xx1 = fma((T)gi[1], P.dx[1], P.lo[1]);
+        T D0, D1, S0, S1;
+        if (DYN == HJ_DYN_AFFINE) {
+            const T cs = spd[loc];
+            D0 = P.hdx[0] * fma(P.A[0], xx0, fma(P.A[1], xx1, P.b[0]));
+            D1 = P.hdx[1] * fma(P.A[3], xx0, fma(P.A[4], xx1, P.b[1]));
+            S0 = P.hdx[0] * cs;
+            S1 = P.hdx[1] * cs;
+        } else {
+            D0 = P.hdx[0] * xx1;
+            D1 = P.hdx[1] * fma(P.vdp_mu * (T(1) - xx0 * xx0), xx1, -xx0);
+            S0 = T(0);
+            S1 = P.hdx[1];
+        }
+        T base = P.kcost;
+        if (!kruz) {
+            const T x[3] = {xx0, xx1, T(0)};
+            base = P.h * cost_state(P, x);
+        }
+        T best = mono ? V00 : (T)INFINITY;
+        if ((di >> loc) & 1ull) {
+            // one-sided and cross differences, prescaled by beta
+            const T Vp0 = q0[1], Vm0 = q0[-1], V0p = q0[BP], V0m = q0[-BP];
+            const T Dxp = beta * (Vp0 - V00), Dxm = beta * (Vm0 - V00);
+            const T Dyp = beta * (V0p - V00), Dym = beta * (V0m - V00);
+            const T X00 = beta * ((q0[BP + 1] - Vp0) - (V0p - V00));    // +x +y
+            const T X10 = beta * ((q0[BP - 1] - Vm0) - (V0p - V00));    // -x +y
+            const T X01 = beta * ((q0[-BP + 1] - Vp0) - (V0m - V00));   // +x -y
+            const T X11 = beta * ((q0[-BP - 1] - Vm0) - (V0m - V00));   // -x -y
+            const T C0 = fma(beta, V00, base);
+#pragma unroll 4
+            for (int k = 0; k < P.K; ++k) {
+                const T d0 = DYN == HJ_DYN_AFFINE ? fma(S0, P.ctrl[k][0], D0) : D0;
+                const T d1 = fma(S1, P.ctrl[k][DYN == HJ_DYN_AFFINE ? 1 : 0], D1);
+                const bool nx = d0 < T(0), ny = d1 < T(0);
+                const T A1 = nx ? Dxm : Dxp, A2 = ny ? Dym : Dyp;
+                const T A3 = ny ? (nx ? X11 : X01) : (nx ? X10 : X00);
+                const T w0 = fabs(d0), w1 = fabs(d1);
+                const T ck = kruz ? C0 : C0 + hlr * P.csq[k];
+                best = fmin(best, fma(w1, fma(w0, A3, A2), fma(w0, A1, ck)));
+            }
+        } else {   // box edge (R3): the general interpolation on the global V^n
+            const int64_t o[3] = {vw.o[0], vw.o[1], 0};
+            const int64_t vn[3] = {vw.vn[0], vw.vn[1], 1};
+            T eb = (T)INFINITY;
+#pragma unroll 1
+            for (int k = 0; k < P.K; ++k) {
+                const T delta[3] = {DYN == HJ_DYN_AFFINE ? fma(S0, P.ctrl[k][0], D0) : D0,
+                                    fma(S1, P.ctrl[k][DYN == HJ_DYN_AFFINE ? 1 : 0], D1), T(0)};
+                const T I = interp<T, T, 2>(Vi, o, vn, P.n, P.periodic, gi, delta, P.v_out);
+                const T ck = kruz ? base : fma(hlr, P.csq[k], base);
+                eb = fmin(eb, fma(beta, I, ck));
+            }
+            best = mono ? fmin(eb, V00) : eb;
+        }
+        Vo[(x0 + c) + vn0 * (y0 + r)] = best;
+        ++evald;
+        if (!same_bits(best, V00)) {
+            cm |= 1ull << loc;
+            const T dv = best > V00 ? best - V00 : V00 - best;
+            rmax = dv > rmax ? dv : rmax;
+        }
+    }
+    rmax_out = rmax;
+    cm_out = cm;
+    evald_out = evald;
+}
+
 // warps per CTA: fp32 one 512-thread CTA per SM (fewer barrier arrivals); fp64 (its
 // staged blocks are twice the size) two 256-thread CTAs per SM
 template <typename T>
@@ -259,7 +372,9 @@ struct CoopNW {
     static constexpr int minb = sizeof(T) == 4 ? 1 : 2;
 };
 
-template <typename T, int KQ, bool PC>
+// EV: 0 = local class (LocalCtrl, FFMA2 quadrants), HJ_DYN_AFFINE + 1 / HJ_DYN_VANDERPOL + 1
+// = field class with feet within one cell
+template <typename T, int KQ, bool PC, int EV = 0>
 __global__ void __launch_bounds__(CoopNW<T>::nw * 32, CoopNW<T>::minb)
     k_sweep_local2d_coop(const DevProblem<T, T> P, const LocalCtrl<T> C,
                          const SweepGroup<T> *__restrict__ G, const CoopState S,
@@ -301,11 +416,16 @@ __global__ void __launch_bounds__(CoopNW<T>::nw * 32, CoopNW<T>::minb)
         // CTA c owns the mini-tiles c, c + G, c + 2G, ... (strided: the active ones spread
         // over all CTAs).  Chunks of 256 candidates: load their masks, compact the nonzero
         // ones in shared memory, then the warps take two per iteration.
-        const int64_t per_cta = (S.total - blockIdx.x + gridDim.x - 1) / gridDim.x;
+        // (list mode: the candidates are the listed mini-tiles of this sweep instead)
+        const int64_t ncand =
+            S.use_list ? (int64_t)*(volatile const int32_t *)&S.count[n % 3] : S.total;
+        const int32_t *litems = S.items[n & 1];
+        const int64_t per_cta = ncand > blockIdx.x ? (ncand - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
         for (int64_t ch = 0; ch < per_cta; ch += COOP_NW * 32) {
         {
             const int64_t k = ch + threadIdx.x;
-            const int64_t g = blockIdx.x + k * (int64_t)gridDim.x;
+            const int64_t idx = blockIdx.x + k * (int64_t)gridDim.x;
+            const int64_t g = k < per_cta ? (S.use_list ? (int64_t)litems[idx] : idx) : 0;
             const unsigned long long m = k < per_cta ? dcur[g] : 0ull;
             const unsigned bal = __ballot_sync(0xffffffffu, m != 0ull);
             if (lane == 0) wcnt[warp] = __popc(bal);
@@ -391,9 +511,15 @@ __global__ void __launch_bounds__(CoopNW<T>::nw * 32, CoopNW<T>::minb)
                 T rmax;
                 unsigned long long cm;
                 int evald;
-                coop_eval<T, KQ, PC>(P, C, vw, blk[warp][s2], spd[warp][s2], lst[warp][s2],
-                                     dd[s2] & im[s2], dd[s2] & em[s2], x0[s2], y0[s2],
-                                     vw.V[(n + 1) & 1], rmax, cm, evald);
+                if constexpr (EV == 0)
+                    coop_eval<T, KQ, PC>(P, C, vw, blk[warp][s2], spd[warp][s2], lst[warp][s2],
+                                         dd[s2] & im[s2], dd[s2] & em[s2], x0[s2], y0[s2],
+                                         vw.V[(n + 1) & 1], rmax, cm, evald);
+                else
+                    coop_eval_field<T, EV - 1>(P, vw, vw.V[n & 1], blk[warp][s2], spd[warp][s2],
+                                               lst[warp][s2], dd[s2] & im[s2], dd[s2] & em[s2],
+                                               x0[s2], y0[s2], vw.V[(n + 1) & 1], rmax, cm,
+                                               evald);
                 cm = ((unsigned long long)__reduce_or_sync(0xffffffffu, (unsigned)(cm >> 32)) << 32) |
                      (unsigned long long)__reduce_or_sync(0xffffffffu, (unsigned)cm);
 #pragma unroll
@@ -420,9 +546,16 @@ __global__ void __launch_bounds__(CoopNW<T>::nw * 32, CoopNW<T>::minb)
                     const int nx = mxy[s2][0] + dx, ny = mxy[s2][1] + dy;
                     if (nx >= 0 && ny >= 0 && nx < S.mt0[v] && ny < S.mt1[v]) {
                         const unsigned long long bits = coop_spread(cm, dx, dy);
-                        if (bits) {   // fire and forget: the scan finds it next sweep
+                        if (bits) {
                             const int64_t nid = S.mt_base[v] + nx + (int64_t)S.mt0[v] * ny;
-                            atomicOr(&dnext[nid], bits);
+                            if (S.use_list) {    // a mask that was empty: list the mini-tile
+                                const unsigned long long old = atomicOr(&dnext[nid], bits);
+                                if (old == 0ull)
+                                    S.items[(n + 1) & 1][atomicAdd(&S.count[(n + 1) % 3], 1)] =
+                                        (int32_t)nid;
+                            } else {             // fire and forget: the scan finds it
+                                atomicOr(&dnext[nid], bits);
+                            }
                         }
                     }
                 }
@@ -440,6 +573,7 @@ __global__ void __launch_bounds__(CoopNW<T>::nw * 32, CoopNW<T>::minb)
             if (m > 0.0) atomic_max_nonneg(&G->v[v].res[n], m);
             if (w) atomicAdd(G->v[v].work, w);
         }
+        if (S.use_list && blockIdx.x == 0 && threadIdx.x == 0) S.count[(n + 2) % 3] = 0;
         if (tr) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_b));
         grid.sync();
         if (tr && 4 * n + 3 < 4 * g_tb_trace.cap) {

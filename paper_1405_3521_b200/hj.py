@@ -77,7 +77,8 @@ EXPORTS = ["hj_last_error", "hj_version", "hj_solve_workspace_bytes", "hj_solve"
 
 # hj.h HJ_SWEEP_*
 SWEEP_KERNELS = {"auto": 0, "generic": 1, "local_scalar": 2, "local_packed": 3, "field2d": 4,
-                 "dubins": 5, "local_tb": 6, "local_coop": 7}
+                 "dubins": 5, "local_tb": 6, "local_coop": 7,
+                 "field_coop": 8}
 
 
 def lib():
@@ -165,8 +166,12 @@ class DeviceProblem:
     """hj_grid / hj_problem structs plus the problem's node fields on the device."""
 
     def __init__(self, prob, dtype="f32", device="cuda", piece=None, speed=None, g=None,
-                 sweep_kernel="auto"):
+                 sweep_kernel="auto", reuse_buffers=False):
         self.prob = prob
+        # reuse_buffers: outputs and workspaces are cached on this object and reused by
+        # the next call (no allocator traffic in a timed loop; results alias)
+        self.reuse = reuse_buffers
+        self._bufs = {}
         self.dtype = dtype
         self.grid = make_grid(prob.grid)
         self.cprob = make_problem(prob)
@@ -186,6 +191,17 @@ class DeviceProblem:
         self.device = device
 
 
+def _buf(dp, name, numel, dtype):
+    """A device tensor for `name`: fresh, or the cached one when dp.reuse_buffers."""
+    if not getattr(dp, "reuse", False):
+        return torch.empty(numel, dtype=dtype, device=dp.device)
+    t = dp._bufs.get(name)
+    if t is None or t.numel() < numel or t.dtype != dtype:
+        t = torch.empty(numel, dtype=dtype, device=dp.device)
+        dp._bufs[name] = t
+    return t[:numel]
+
+
 def hj_version() -> str:
     return lib().hj_version().decode()
 
@@ -198,10 +214,10 @@ def hj_solve(dp: DeviceProblem, tol=None, max_iter=None, V=None, workspace=None,
     max_iter = prob.max_iter if max_iter is None else max_iter
     L = lib()
     if V is None:
-        V = torch.empty(dp.N, dtype=_torch_dtype(dp.dtype), device=dp.device)
+        V = _buf(dp, "V", dp.N, _torch_dtype(dp.dtype))
     need = L.hj_solve_workspace_bytes(ctypes.byref(dp.grid), _code(dp.dtype), max_iter)
     if workspace is None or workspace.numel() < need:
-        workspace = torch.empty(need, dtype=torch.uint8, device=dp.device)
+        workspace = _buf(dp, "ws", need, torch.uint8)
     rep = hj_report()
     st = L.hj_solve(ctypes.byref(dp.grid), ctypes.byref(dp.cprob), ctypes.byref(dp.fields),
                     _code(dp.dtype), V.data_ptr(), float(tol), int(max_iter), workspace.data_ptr(),
@@ -224,11 +240,11 @@ def hj_label_subdomains(coarse: DeviceProblem, Vc, n_max, fine: DeviceProblem, r
                         stream=None):
     Nc, Nf = coarse.N, fine.N
     dev = coarse.device
-    label = torch.empty(Nc, dtype=torch.int32, device=dev)
-    margin = torch.empty(Nc, dtype=torch.float64, device=dev)
-    geo = torch.empty(Nc, dtype=torch.float64, device=dev)
-    steps = torch.empty(Nc, dtype=torch.int32, device=dev)
-    mask = torch.empty(Nf, dtype=torch.int32, device=dev)   # uint32 bits
+    label = _buf(coarse, "label", Nc, torch.int32)
+    margin = _buf(coarse, "margin", Nc, torch.float64)
+    geo = _buf(coarse, "geo", Nc, torch.float64)
+    steps = _buf(coarse, "steps", Nc, torch.int32)
+    mask = _buf(fine, "mask", Nf, torch.int32)   # uint32 bits
     r = (ctypes.c_int32 * 3)(*[int(ratio[d]) if d < len(ratio) else 1 for d in range(3)])
     _check(lib().hj_label_subdomains(
         ctypes.byref(coarse.grid), ctypes.byref(coarse.cprob), ctypes.byref(coarse.fields),
@@ -262,9 +278,9 @@ def hj_solve_partitioned(fine: DeviceProblem, mask, m, plan, ws_bytes, solve_set
     max_iter = prob.max_iter if max_iter is None else max_iter
     solve_set = ((1 << m) - 1) if solve_set is None else solve_set
     if Vbar is None:
-        Vbar = torch.empty(fine.N, dtype=_torch_dtype(fine.dtype), device=fine.device)
+        Vbar = _buf(fine, "Vbar", fine.N, _torch_dtype(fine.dtype))
     if workspace is None or workspace.numel() < ws_bytes:
-        workspace = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=fine.device)
+        workspace = _buf(fine, "pws", max(ws_bytes, 1), torch.uint8)
     reps = (hj_report * m)()
     _check(lib().hj_solve_partitioned(
         ctypes.byref(fine.grid), ctypes.byref(fine.cprob), ctypes.byref(fine.fields),

@@ -72,7 +72,8 @@ def test_solve_matches_oracle(idx, dtype, oracle_cache):
 
 KERNELS = {1: ("generic", "field2d", "local_scalar", "local_packed", "local_tb", "local_coop"),
            2: ("generic", "field2d", "local_scalar", "local_packed", "local_tb", "local_coop"),
-           3: ("generic", "field2d"), 4: ("generic", "dubins"), 5: ("generic", "field2d")}
+           3: ("generic", "field2d", "field_coop"), 4: ("generic", "dubins"),
+           5: ("generic", "field2d")}
 
 
 @pytest.mark.parametrize("idx", [1, 2, 3, 4, 5])
@@ -131,6 +132,23 @@ def test_local_tb_stops_inside_a_block(max_iter, kernel):
         Vb, rb = hj.hj_solve(tb, tol=tol, allow_not_converged=True)
         assert ra["iterations"] == rb["iterations"], (n, ra["iterations"], rb["iterations"])
         assert torch.equal(Va, Vb)
+
+
+@pytest.mark.parametrize("idx,kernel", [(1, "local_coop"), (2, "local_coop"), (3, "field_coop")])
+def test_coop_list_mode_matches_scan_mode(idx, kernel, oracle_cache, monkeypatch):
+    """The cooperative kernels enumerate the active mini-tiles by scanning every mask
+    (small grids) or by a device list (large grids): both must give the same iterates,
+    bit for bit, and match the oracle."""
+    cfg = _cfg(idx)
+    Vo, it_o, _ = _oracle_solve(oracle_cache, idx)
+    out = []
+    for mode in ("0", "1"):
+        monkeypatch.setenv("HJ_COOP_LIST", mode)
+        V, rep = hj.hj_solve(hj.DeviceProblem(cfg.fine, "f32", sweep_kernel=kernel),
+                             tol=max(cfg.fine.tol, 1e-7))
+        out.append((V.cpu(), rep["iterations"]))
+        assert np.abs(V.double().cpu().numpy() - Vo).max() <= TOL["f32"]
+    assert torch.equal(out[0][0], out[1][0]) and out[0][1] == out[1][1]
 
 
 def test_local_kernel_refuses_nonlocal_problem():
