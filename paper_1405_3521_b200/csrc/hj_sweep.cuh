@@ -834,7 +834,7 @@ struct SweepLaunch {
     int tb = 1;                         // sweeps per launch (> 1: k_sweep_local2d_tb)
     bool coop = false;                  // whole iteration in k_sweep_local2d_coop
     void *wl_mem = nullptr;             // work-list / cooperative-state region
-    std::vector<int64_t> vn0, vn1;      // view extents (cooperative mini-tiling)
+    std::vector<int64_t> vn0, vn1, vn2; // view extents (cooperative mini-tiling)
     int64_t gn0 = 0, gn1 = 0;           // grid extents
     bool dense = false;                 // SweepGroup::dense
     int64_t total_tiles = 0;
@@ -955,7 +955,7 @@ hj_status sweep_prepare(const hj_grid &g, const hj_problem &p, const hj_fields &
             if (p.A[d][e] != 0) iso = false;
     }
     const int want = p.sweep_kernel;
-    if (want < HJ_SWEEP_AUTO || want > HJ_SWEEP_FIELD_COOP) {
+    if (want < HJ_SWEEP_AUTO || want > HJ_SWEEP_DUBINS_COOP) {
         set_error("unknown sweep_kernel %d", want);
         return HJ_ERR_INVALID;
     }
@@ -1064,13 +1064,22 @@ hj_status sweep_prepare(const hj_grid &g, const hj_problem &p, const hj_fields &
             (want == HJ_SWEEP_AUTO || want == HJ_SWEEP_FIELD2D || want == HJ_SWEEP_FIELD_COOP))
             L.kind = SWEEP_FIELD2D;
         else if (p.dynamics == HJ_DYN_DUBINS && H[2] <= 1.0 && !g.periodic[0] && !g.periodic[1] &&
-                 (want == HJ_SWEEP_AUTO || want == HJ_SWEEP_DUBINS))
+                 (want == HJ_SWEEP_AUTO || want == HJ_SWEEP_DUBINS ||
+                  want == HJ_SWEEP_DUBINS_COOP))
             L.kind = SWEEP_DUBINS;
     }
     L.dyn = p.dynamics;
     if (L.kind == SWEEP_FIELD2D && H[0] <= 1.0 && H[1] <= 1.0 &&
         (want == HJ_SWEEP_AUTO || want == HJ_SWEEP_FIELD_COOP))
         L.coop = true;         // every foot within one cell: the cooperative kernel
+    if (L.kind == SWEEP_DUBINS && H[0] <= 1.0 && H[1] <= 1.0 &&
+        (want == HJ_SWEEP_AUTO || want == HJ_SWEEP_DUBINS_COOP))
+        L.coop = true;         // (x, y) feet within one cell: the cooperative kernel
+    if (want == HJ_SWEEP_DUBINS_COOP && !(L.kind == SWEEP_DUBINS && L.coop)) {
+        set_error("sweep_kernel %d requested, but the problem does not qualify for it "
+                  "(Dubins, feet within one cell)", want);
+        return HJ_ERR_UNSUPPORTED;
+    }
     if (want == HJ_SWEEP_FIELD_COOP && !(L.kind == SWEEP_FIELD2D && L.coop)) {
         set_error("sweep_kernel %d requested, but the problem does not qualify for it "
                   "(2-D affine / Van der Pol, feet within one cell)", want);
@@ -1133,6 +1142,7 @@ hj_status sweep_prepare(const hj_grid &g, const hj_problem &p, const hj_fields &
         for (size_t q = 0; q < views.size(); ++q) {
             L.vn0.push_back(views[q].vn[0]);
             L.vn1.push_back(views[q].vn[1]);
+            L.vn2.push_back(views[q].vn[2]);
         }
         L.gn0 = g.n[0];
         L.gn1 = g.dim > 1 ? g.n[1] : 1;
@@ -1280,11 +1290,13 @@ hj_status sweep_coop(const DevProblem<T, T> &P, const SweepLaunch<T> &L, int64_t
     memset(&S, 0, sizeof(S));
     S.n_views = nv;
     int64_t tot = 0;
+    S.dubins = L.kind == SWEEP_DUBINS ? 1 : 0;
     for (int v = 0; v < nv; ++v) {
         S.mt_base[v] = tot;
         S.mt0[v] = (int32_t)((L.vn0[v] + 7) / 8);
         S.mt1[v] = (int32_t)((L.vn1[v] + 7) / 8);
-        tot += (int64_t)S.mt0[v] * S.mt1[v];
+        S.mt2[v] = (int32_t)L.vn2[v];
+        tot += (int64_t)S.mt0[v] * S.mt1[v] * S.mt2[v];
     }
     S.mt_base[nv] = tot;
     S.total = tot;
@@ -1308,7 +1320,9 @@ hj_status sweep_coop(const DevProblem<T, T> &P, const SweepLaunch<T> &L, int64_t
         HJ_CUDA(cudaGetLastError());
     }
     hj_status st = HJ_OK;
-    if (L.kind == SWEEP_FIELD2D) {
+    if (L.kind == SWEEP_DUBINS) {
+        st = launch_coop_kq<T, 4, false, 3>(P, L, S, max_iter, tol, s);
+    } else if (L.kind == SWEEP_FIELD2D) {
         st = L.dyn == HJ_DYN_AFFINE
                  ? launch_coop_kq<T, 4, false, HJ_DYN_AFFINE + 1>(P, L, S, max_iter, tol, s)
                  : launch_coop_kq<T, 4, false, HJ_DYN_VANDERPOL + 1>(P, L, S, max_iter, tol, s);

@@ -27,7 +27,7 @@ namespace hj {
 
 struct CoopState {
     int64_t mt_base[HJ_MAX_SUBDOMAINS + 1];   // first global mini-tile id of each view
-    int32_t mt0[HJ_MAX_SUBDOMAINS], mt1[HJ_MAX_SUBDOMAINS];
+    int32_t mt0[HJ_MAX_SUBDOMAINS], mt1[HJ_MAX_SUBDOMAINS], mt2[HJ_MAX_SUBDOMAINS];
     unsigned long long *imask;      // [total] fast interior nodes (class -1)
     unsigned long long *emask;      // [total] interior nodes on the box edge (class -3)
     unsigned long long *dmask[2];   // [total] nodes to evaluate in sweep n (parity n)
@@ -35,6 +35,7 @@ struct CoopState {
     int32_t *count;                 // [3] ring: sweep n reads count[n % 3]
     int64_t *stop;                  // [n_views] iterations performed (output)
     int use_list;                   // 1: walk items/count (many mini-tiles); 0: scan all
+    int dubins;                     // 3-D Dubins views: 8 x 8 mini-tiles per heading plane
     int n_views;
     int64_t total;
 };
@@ -54,15 +55,17 @@ __global__ void k_coop_masks(const SweepGroup<T> *__restrict__ G, CoopState S, i
         const int v = coop_view(S, gid);
         const SweepView<T> &vw = G->v[v];
         const int64_t mt = gid - S.mt_base[v];
-        const int mx = (int)(mt % S.mt0[v]), my = (int)(mt / S.mt0[v]);
+        const int mx = (int)(mt % S.mt0[v]);
+        const int my = (int)((mt / S.mt0[v]) % S.mt1[v]);
+        const int mz = (int)(mt / ((int64_t)S.mt0[v] * S.mt1[v]));
         unsigned long long im = 0, em = 0;
         for (int b = 0; b < 64; ++b) {
             const int64_t li = (int64_t)mx * 8 + (b & 7), lj = (int64_t)my * 8 + (b >> 3);
             if (li >= vw.vn[0] || lj >= vw.vn[1]) continue;
-            if (vw.cls[li + vw.vn[0] * lj] != -1) continue;
+            if (vw.cls[li + vw.vn[0] * (lj + vw.vn[1] * mz)] != -1) continue;
             const int64_t g0 = li + vw.o[0], g1 = lj + vw.o[1];
-            if (g0 == 0 || g1 == 0 || g0 == gn0 - 1 || g1 == gn1 - 1)
-                em |= 1ull << b;
+            if (!S.dubins && (g0 == 0 || g1 == 0 || g0 == gn0 - 1 || g1 == gn1 - 1))
+                em |= 1ull << b;   // (Dubins nodes apply the box rule themselves)
             else
                 im |= 1ull << b;
         }
@@ -364,6 +367,101 @@ __device__ __forceinline__ void coop_eval_field(const DevProblem<T, T> &P, const
     evald_out = evald;
 }
 
+// Phase B for the Dubins car (config 4): the listed nodes of one 8 x 8 mini-tile of
+// heading plane z, with the 10 x 10 blocks of planes z-1, z, z+1 staged (b[0..299]).
+// Same arithmetic as k_sweep_dubins: the (x, y) foot h v (cos th, sin th) is the same
+// for all controls (box rule R3 once per node), three bilinear interpolants, then per
+// control I0 + |d_k| (I+-1 - I0).
+template <typename T>
+__device__ __forceinline__ void coop_eval_dubins(const DevProblem<T, T> &P, const SweepView<T> &vw,
+                                                 const T *__restrict__ b, int8_t *lstw,
+                                                 unsigned long long di, int64_t x0, int64_t y0,
+                                                 int64_t z, T d0, T d1, T *__restrict__ Vo,
+                                                 T &rmax_out, unsigned long long &cm_out,
+                                                 int &evald_out) {
+    constexpr int BP = 10;
+    const int lane = threadIdx.x & 31;
+    const bool mono = P.monotone != 0;
+    const bool kruz = P.cost == HJ_COST_KRUZKOV;
+    const T beta = P.beta;
+    const int64_t vn0 = vw.vn[0], vn1 = vw.vn[1];
+    const T hlr = P.h * P.lr;
+    const unsigned lt = (1u << lane) - 1u;
+    const unsigned dlo = (unsigned)di, dhi = (unsigned)(di >> 32);
+    const int plo = __popc(dlo), nN = plo + __popc(dhi);
+    if ((dlo >> lane) & 1u) lstw[__popc(dlo & lt)] = (int8_t)lane;
+    if ((dhi >> lane) & 1u) lstw[plo + __popc(dhi & lt)] = (int8_t)(32 + lane);
+    __syncwarp();
+    T rmax = T(0);
+    unsigned long long cm = 0;
+    int evald = 0;
+    const T hw = P.hdx[2] * P.dub_w;
+#pragma unroll 1
+    for (int p = 0; p < 2; ++p) {
+        const int slot = lane + 32 * p;
+        if (slot >= nN) continue;
+        const int loc = lstw[slot];
+        const int r = loc >> 3, c = loc & 7;
+        const int64_t gi0 = x0 + c + vw.o[0], gi1 = y0 + r + vw.o[1];
+        const T *q0 = b + BP * BP + (r + 1) * BP + (c + 1);   // plane z, the node
+        const T V00 = q0[0];
+        T base = P.kcost;
+        if (!kruz) {
+            const T x[3] = {fma((T)gi0, P.dx[0], P.lo[0]), fma((T)gi1, P.dx[1], P.lo[1]),
+                            fma((T)(z + vw.o[2]), P.dx[2], P.lo[2])};
+            base = P.h * cost_state(P, x);
+        }
+        const T lo0 = -(T)gi0, hi0 = (T)(P.n[0] - 1 - gi0);
+        const T lo1 = -(T)gi1, hi1 = (T)(P.n[1] - 1 - gi1);
+        const T eps = (T)BOX_EPS;
+        const bool inside = d0 >= lo0 - eps && d0 <= hi0 + eps && d1 >= lo1 - eps &&
+                            d1 <= hi1 + eps;
+        T best = (T)INFINITY;
+        if (!inside) {
+            for (int k = 0; k < P.K; ++k) {
+                const T ck = kruz ? base : fma(hlr, P.csq[k], base);
+                best = fmin(best, fma(beta, P.v_out, ck));
+            }
+        } else {
+            T x = d0 < lo0 ? lo0 : (d0 > hi0 ? hi0 : d0);
+            T y = d1 < lo1 ? lo1 : (d1 > hi1 ? hi1 : d1);
+            T fx = floor(x), fy = floor(y);
+            int64_t cx = gi0 + (int64_t)fx, cy = gi1 + (int64_t)fy;
+            T wx = x - fx, wy = y - fy;
+            if (cx > P.n[0] - 2) { cx = P.n[0] - 2; wx = T(1); }
+            if (cy > P.n[1] - 2) { cy = P.n[1] - 2; wy = T(1); }
+            const int rx = (int)(cx - gi0), ry = (int)(cy - gi1);   // in {-1, 0}
+            T I3[3];
+#pragma unroll
+            for (int s = 0; s < 3; ++s) {
+                const T *pl = b + s * BP * BP + (r + 1 + ry) * BP + (c + 1 + rx);
+                const T a = lerp<T>(pl[0], pl[1], wx);
+                const T bb = lerp<T>(pl[BP], pl[BP + 1], wx);
+                I3[s] = lerp<T>(a, bb, wy);
+            }
+            const T dM = I3[0] - I3[1], dP = I3[2] - I3[1];
+#pragma unroll 4
+            for (int k = 0; k < P.K; ++k) {
+                const T dk = hw * P.ctrl[k][0];
+                const T I = fma(fabs(dk), dk < T(0) ? dM : dP, I3[1]);
+                const T ck = kruz ? base : fma(hlr, P.csq[k], base);
+                best = fmin(best, fma(beta, I, ck));
+            }
+        }
+        if (mono) best = fmin(best, V00);
+        Vo[(x0 + c) + vn0 * ((y0 + r) + vn1 * z)] = best;
+        ++evald;
+        if (!same_bits(best, V00)) {
+            cm |= 1ull << loc;
+            const T dv = best > V00 ? best - V00 : V00 - best;
+            rmax = dv > rmax ? dv : rmax;
+        }
+    }
+    rmax_out = rmax;
+    cm_out = cm;
+    evald_out = evald;
+}
+
 // warps per CTA: fp32 one 512-thread CTA per SM (fewer barrier arrivals); fp64 (its
 // staged blocks are twice the size) two 256-thread CTAs per SM
 template <typename T>
@@ -373,7 +471,7 @@ struct CoopNW {
 };
 
 // EV: 0 = local class (LocalCtrl, FFMA2 quadrants), HJ_DYN_AFFINE + 1 / HJ_DYN_VANDERPOL + 1
-// = field class with feet within one cell
+// = field class with feet within one cell, 3 = Dubins (3-D, heading planes)
 template <typename T, int KQ, bool PC, int EV = 0>
 __global__ void __launch_bounds__(CoopNW<T>::nw * 32, CoopNW<T>::minb)
     k_sweep_local2d_coop(const DevProblem<T, T> P, const LocalCtrl<T> C,
@@ -383,8 +481,10 @@ __global__ void __launch_bounds__(CoopNW<T>::nw * 32, CoopNW<T>::minb)
     cg::grid_group grid = cg::this_grid();
     constexpr int COOP_NW = CoopNW<T>::nw;
     constexpr int BP = 10;                         // staged block pitch
-    __shared__ T blk[COOP_NW][2][BP * BP];
-    __shared__ T spd[COOP_NW][2][64];
+    constexpr int BLK = EV == 3 ? 3 * BP * BP : BP * BP;   // Dubins: planes z-1, z, z+1
+    constexpr int SPD = EV == 3 ? 1 : 64;
+    __shared__ T blk[COOP_NW][2][BLK];
+    __shared__ T spd[COOP_NW][2][SPD];
     __shared__ int8_t lst[COOP_NW][2][64];
     __shared__ int32_t qgid[COOP_NW * 32];
     __shared__ unsigned long long qmask[COOP_NW * 32];
@@ -453,7 +553,7 @@ __global__ void __launch_bounds__(CoopNW<T>::nw * 32, CoopNW<T>::minb)
             int64_t gid[2];
             gid[0] = qgid[it];
             gid[1] = it + COOP_NW < cnt ? (int64_t)qgid[it + COOP_NW] : (int64_t)-1;
-            int vv[2], mxy[2][2];
+            int vv[2], mxy[2][3];
             int64_t x0[2], y0[2];
             unsigned long long dd[2], im[2], em[2];
 #pragma unroll
@@ -462,7 +562,8 @@ __global__ void __launch_bounds__(CoopNW<T>::nw * 32, CoopNW<T>::minb)
                 vv[s2] = coop_view(S, g);
                 const int64_t mt = g - S.mt_base[vv[s2]];
                 mxy[s2][0] = (int)(mt % S.mt0[vv[s2]]);
-                mxy[s2][1] = (int)(mt / S.mt0[vv[s2]]);
+                mxy[s2][1] = (int)((mt / S.mt0[vv[s2]]) % S.mt1[vv[s2]]);
+                mxy[s2][2] = (int)(mt / ((int64_t)S.mt0[vv[s2]] * S.mt1[vv[s2]]));
                 x0[s2] = (int64_t)mxy[s2][0] * 8;
                 y0[s2] = (int64_t)mxy[s2][1] * 8;
                 dd[s2] = gid[s2] >= 0 ? qmask[s2 ? it + COOP_NW : it] : 0ull;
@@ -470,25 +571,33 @@ __global__ void __launch_bounds__(CoopNW<T>::nw * 32, CoopNW<T>::minb)
                 em[s2] = S.emask[g];
             }
             // staged V^n blocks and speeds, loads first
-            T ld[2][4], lsp[2][2];
+            constexpr int NLD = (BLK + 31) / 32;
+            T ld[2][NLD], lsp[2][2];
 #pragma unroll
             for (int s2 = 0; s2 < 2; ++s2) {
                 const SweepView<T> &vw = G->v[vv[s2]];
-                const int64_t vn0 = vw.vn[0], vn1 = vw.vn[1];
+                const int64_t vn0 = vw.vn[0], vn1 = vw.vn[1], vn2 = vw.vn[2];
                 const T *__restrict__ Vi = vw.V[n & 1];
 #pragma unroll
-                for (int k = 0; k < 4; ++k) {
+                for (int k = 0; k < NLD; ++k) {
                     const int e = lane + 32 * k;
-                    const int64_t li = x0[s2] - 1 + e % BP, lj = y0[s2] - 1 + e / BP;
-                    ld[s2][k] = (e < BP * BP && li >= 0 && lj >= 0 && li < vn0 && lj < vn1)
-                                    ? Vi[li + vn0 * lj]
+                    const int ee = e % (BP * BP);
+                    const int64_t li = x0[s2] - 1 + ee % BP, lj = y0[s2] - 1 + ee / BP;
+                    int64_t lk = 0;
+                    if (EV == 3) {                   // heading plane z-1+e/100, periodic
+                        lk = mxy[s2][2] - 1 + e / (BP * BP);
+                        if (lk < 0) lk += vn2;
+                        if (lk >= vn2) lk -= vn2;
+                    }
+                    ld[s2][k] = (e < BLK && li >= 0 && lj >= 0 && li < vn0 && lj < vn1)
+                                    ? Vi[li + vn0 * (lj + vn1 * lk)]
                                     : v_out;
                 }
 #pragma unroll
                 for (int k = 0; k < 2; ++k) {
                     const int e = lane + 32 * k;
                     const int64_t li = x0[s2] + (e & 7), lj = y0[s2] + (e >> 3);
-                    lsp[s2][k] = (P.speed && li < vn0 && lj < vn1)
+                    lsp[s2][k] = (EV != 3 && P.speed && li < vn0 && lj < vn1)
                                      ? P.speed[(li + vw.o[0]) + gn0 * (lj + vw.o[1])]
                                      : T(1);
                 }
@@ -496,10 +605,12 @@ __global__ void __launch_bounds__(CoopNW<T>::nw * 32, CoopNW<T>::minb)
 #pragma unroll
             for (int s2 = 0; s2 < 2; ++s2) {
 #pragma unroll
-                for (int k = 0; k < 4; ++k)
-                    if (lane + 32 * k < BP * BP) blk[warp][s2][lane + 32 * k] = ld[s2][k];
-                spd[warp][s2][lane] = lsp[s2][0];
-                spd[warp][s2][lane + 32] = lsp[s2][1];
+                for (int k = 0; k < NLD; ++k)
+                    if (lane + 32 * k < BLK) blk[warp][s2][lane + 32 * k] = ld[s2][k];
+                if (EV != 3) {
+                    spd[warp][s2][lane % SPD] = lsp[s2][0];
+                    spd[warp][s2][(lane + 32) % SPD] = lsp[s2][1];
+                }
             }
             __syncwarp();
             unsigned long long cmv[2] = {0ull, 0ull};
@@ -511,7 +622,15 @@ __global__ void __launch_bounds__(CoopNW<T>::nw * 32, CoopNW<T>::minb)
                 T rmax;
                 unsigned long long cm;
                 int evald;
-                if constexpr (EV == 0)
+                if constexpr (EV == 3) {
+                    const T th = fma((T)(mxy[s2][2] + vw.o[2]), P.dx[2], P.lo[2]);
+                    T sn, cn;
+                    sincos_t(th, &sn, &cn);
+                    coop_eval_dubins<T>(P, vw, blk[warp][s2], lst[warp][s2], dd[s2] & im[s2],
+                                        x0[s2], y0[s2], mxy[s2][2], P.hdx[0] * (P.dub_v * cn),
+                                        P.hdx[1] * (P.dub_v * sn), vw.V[(n + 1) & 1], rmax, cm,
+                                        evald);
+                } else if constexpr (EV == 0)
                     coop_eval<T, KQ, PC>(P, C, vw, blk[warp][s2], spd[warp][s2], lst[warp][s2],
                                          dd[s2] & im[s2], dd[s2] & em[s2], x0[s2], y0[s2],
                                          vw.V[(n + 1) & 1], rmax, cm, evald);
@@ -537,17 +656,24 @@ __global__ void __launch_bounds__(CoopNW<T>::nw * 32, CoopNW<T>::minb)
             }
             // sweep n+1: the 3 x 3 dilation of the changed nodes into the 9 mini-tiles
             // around each item (lanes 0-8: item 0, lanes 16-24: item 1)
-            {
-                const int s2 = lane >> 4, l9 = lane & 15;
+            // (Dubins: the same in-plane dilation into planes z-1, z, z+1: 27 mini-tiles,
+            // two per lane)
+#pragma unroll
+            for (int rep = 0; rep < (EV == 3 ? 2 : 1); ++rep) {
+                const int s2 = lane >> 4, l9 = (lane & 15) + 16 * rep;
                 const unsigned long long cm = cmv[s2];
-                if (cm && l9 < 9) {
+                if (cm && l9 < (EV == 3 ? 27 : 9)) {
                     const int v = vv[s2];
-                    const int dx = l9 % 3 - 1, dy = l9 / 3 - 1;
+                    const int dx = l9 % 3 - 1, dy = (l9 / 3) % 3 - 1, dz = l9 / 9 - 1;
                     const int nx = mxy[s2][0] + dx, ny = mxy[s2][1] + dy;
+                    int nz = mxy[s2][2] + (EV == 3 ? dz : 0);
+                    if (nz < 0) nz += S.mt2[v];
+                    if (nz >= S.mt2[v]) nz -= S.mt2[v];
                     if (nx >= 0 && ny >= 0 && nx < S.mt0[v] && ny < S.mt1[v]) {
                         const unsigned long long bits = coop_spread(cm, dx, dy);
                         if (bits) {
-                            const int64_t nid = S.mt_base[v] + nx + (int64_t)S.mt0[v] * ny;
+                            const int64_t nid = S.mt_base[v] + nx +
+                                                (int64_t)S.mt0[v] * (ny + (int64_t)S.mt1[v] * nz);
                             if (S.use_list) {    // a mask that was empty: list the mini-tile
                                 const unsigned long long old = atomicOr(&dnext[nid], bits);
                                 if (old == 0ull)

@@ -72,7 +72,7 @@ def test_solve_matches_oracle(idx, dtype, oracle_cache):
 
 KERNELS = {1: ("generic", "field2d", "local_scalar", "local_packed", "local_tb", "local_coop"),
            2: ("generic", "field2d", "local_scalar", "local_packed", "local_tb", "local_coop"),
-           3: ("generic", "field2d", "field_coop"), 4: ("generic", "dubins"),
+           3: ("generic", "field2d", "field_coop"), 4: ("generic", "dubins", "dubins_coop"),
            5: ("generic", "field2d")}
 
 
@@ -134,7 +134,8 @@ def test_local_tb_stops_inside_a_block(max_iter, kernel):
         assert torch.equal(Va, Vb)
 
 
-@pytest.mark.parametrize("idx,kernel", [(1, "local_coop"), (2, "local_coop"), (3, "field_coop")])
+@pytest.mark.parametrize("idx,kernel", [(1, "local_coop"), (2, "local_coop"), (3, "field_coop"),
+                                        (4, "dubins_coop")])
 def test_coop_list_mode_matches_scan_mode(idx, kernel, oracle_cache, monkeypatch):
     """The cooperative kernels enumerate the active mini-tiles by scanning every mask
     (small grids) or by a device list (large grids): both must give the same iterates,
