@@ -88,3 +88,12 @@ def test_product_has_no_cpu_fallback_and_no_oracle_import():
         if fn.endswith(".py"):
             src = open(os.path.join(pkg, fn)).read()
             assert "import oracle" not in src and "from oracle" not in src, fn
+
+
+def test_sweep_kernel_enum_matches_binding():
+    """hj.h HJ_SWEEP_* values == the names hj.py marshals (sweep_kernel="...")."""
+    from paper_1405_3521_b200 import hj
+    src = open(os.path.join(ROOT, "include", "hj.h")).read()
+    vals = {m.group(1).lower(): int(m.group(2))
+            for m in re.finditer(r"HJ_SWEEP_([A-Z0-9_]+)\s*=\s*(\d+)", src)}
+    assert vals == hj.SWEEP_KERNELS
