@@ -1260,12 +1260,16 @@ template <typename T, int KQ, bool PC, int EV = 0>
 static hj_status launch_coop_kq(const DevProblem<T, T> &P, const SweepLaunch<T> &L,
                                 const CoopState &S, int64_t max_iter, double tol,
                                 cudaStream_t s) {
+    constexpr int BLK = EV == 3 ? 300 : 100;
+    const size_t dyn = (size_t)CoopNW<T>::nw * 2 * BLK * sizeof(T);
     static int grid = 0;
     if (!grid) {
+        cudaFuncSetAttribute(k_sweep_local2d_coop<T, KQ, PC, EV>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
         int sms = 148, per_sm = 0;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
         if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sweep_local2d_coop<T, KQ, PC, EV>,
-                                                          CoopNW<T>::nw * 32, 0) != cudaSuccess ||
+                                                          CoopNW<T>::nw * 32, dyn) != cudaSuccess ||
             per_sm < 1)
             per_sm = 1;
         grid = sms * per_sm;
@@ -1274,7 +1278,7 @@ static hj_status launch_coop_kq(const DevProblem<T, T> &P, const SweepLaunch<T> 
     void *args[] = {(void *)&P, (void *)&L.ctrl, (void *)&g, (void *)&S, (void *)&max_iter,
                     (void *)&tol};
     cudaError_t e = cudaLaunchCooperativeKernel((void *)k_sweep_local2d_coop<T, KQ, PC, EV>,
-                                                dim3(grid), dim3(CoopNW<T>::nw * 32), args, 0, s);
+                                                dim3(grid), dim3(CoopNW<T>::nw * 32), args, dyn, s);
     if (e != cudaSuccess) {
         set_error("cooperative sweep launch failed: %s", cudaGetErrorString(e));
         return HJ_ERR_CUDA;

@@ -483,17 +483,17 @@ __global__ void __launch_bounds__(CoopNW<T>::nw * 32, CoopNW<T>::minb)
     constexpr int BP = 10;                         // staged block pitch
     constexpr int BLK = EV == 3 ? 3 * BP * BP : BP * BP;   // Dubins: planes z-1, z, z+1
     constexpr int SPD = EV == 3 ? 1 : 64;
-    __shared__ T blk[COOP_NW][2][BLK];
+    // the staged blocks (the largest piece) live in dynamic shared memory
+    extern __shared__ __align__(16) unsigned char coop_dyn[];
+    T(*blk)[2][BLK] = reinterpret_cast<T(*)[2][BLK]>(coop_dyn);
     __shared__ T spd[COOP_NW][2][SPD];
     __shared__ int8_t lst[COOP_NW][2][64];
     __shared__ int32_t qgid[COOP_NW * 32];
-    __shared__ unsigned long long qmask[COOP_NW * 32];
+    __shared__ unsigned long long qmask[COOP_NW * 32], qemask[COOP_NW * 32];
     __shared__ int wcnt[COOP_NW], qn;
     __shared__ unsigned long long cres[HJ_MAX_SUBDOMAINS];    // per-CTA max (fp64 bits >= 0)
     __shared__ unsigned long long cwork[HJ_MAX_SUBDOMAINS];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int64_t gwarp = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
-    const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
     const bool mono = P.monotone != 0;
     const bool kruz = P.cost == HJ_COST_KRUZKOV;
     const T beta = P.beta, v_out = P.v_out;
@@ -527,6 +527,9 @@ __global__ void __launch_bounds__(CoopNW<T>::nw * 32, CoopNW<T>::minb)
             const int64_t idx = blockIdx.x + k * (int64_t)gridDim.x;
             const int64_t g = k < per_cta ? (S.use_list ? (int64_t)litems[idx] : idx) : 0;
             const unsigned long long m = k < per_cta ? dcur[g] : 0ull;
+            // the class masks ride along with the dirty mask (one round trip for all three)
+            const unsigned long long cim = k < per_cta ? S.imask[g] : 0ull;
+            const unsigned long long cem = k < per_cta ? S.emask[g] : 0ull;
             const unsigned bal = __ballot_sync(0xffffffffu, m != 0ull);
             if (lane == 0) wcnt[warp] = __popc(bal);
             __syncthreads();
@@ -535,7 +538,8 @@ __global__ void __launch_bounds__(CoopNW<T>::nw * 32, CoopNW<T>::minb)
             if (m) {
                 const int pos = base_i + __popc(bal & ((1u << lane) - 1u));
                 qgid[pos] = (int32_t)g;
-                qmask[pos] = m;
+                qmask[pos] = m & cim;
+                qemask[pos] = m & cem;
                 dcur[g] = 0ull;                    // consumed
             }
             if (threadIdx.x == 0) {
@@ -567,8 +571,8 @@ __global__ void __launch_bounds__(CoopNW<T>::nw * 32, CoopNW<T>::minb)
                 x0[s2] = (int64_t)mxy[s2][0] * 8;
                 y0[s2] = (int64_t)mxy[s2][1] * 8;
                 dd[s2] = gid[s2] >= 0 ? qmask[s2 ? it + COOP_NW : it] : 0ull;
-                im[s2] = S.imask[g];
-                em[s2] = S.emask[g];
+                im[s2] = ~0ull;                    // (dd already restricted to the classes)
+                em[s2] = gid[s2] >= 0 ? qemask[s2 ? it + COOP_NW : it] : 0ull;
             }
             // staged V^n blocks and speeds, loads first
             constexpr int NLD = (BLK + 31) / 32;
@@ -626,17 +630,17 @@ __global__ void __launch_bounds__(CoopNW<T>::nw * 32, CoopNW<T>::minb)
                     const T th = fma((T)(mxy[s2][2] + vw.o[2]), P.dx[2], P.lo[2]);
                     T sn, cn;
                     sincos_t(th, &sn, &cn);
-                    coop_eval_dubins<T>(P, vw, blk[warp][s2], lst[warp][s2], dd[s2] & im[s2],
+                    coop_eval_dubins<T>(P, vw, blk[warp][s2], lst[warp][s2], dd[s2] | em[s2],
                                         x0[s2], y0[s2], mxy[s2][2], P.hdx[0] * (P.dub_v * cn),
                                         P.hdx[1] * (P.dub_v * sn), vw.V[(n + 1) & 1], rmax, cm,
                                         evald);
                 } else if constexpr (EV == 0)
                     coop_eval<T, KQ, PC>(P, C, vw, blk[warp][s2], spd[warp][s2], lst[warp][s2],
-                                         dd[s2] & im[s2], dd[s2] & em[s2], x0[s2], y0[s2],
+                                         dd[s2], em[s2], x0[s2], y0[s2],
                                          vw.V[(n + 1) & 1], rmax, cm, evald);
                 else
                     coop_eval_field<T, EV - 1>(P, vw, vw.V[n & 1], blk[warp][s2], spd[warp][s2],
-                                               lst[warp][s2], dd[s2] & im[s2], dd[s2] & em[s2],
+                                               lst[warp][s2], dd[s2], em[s2],
                                                x0[s2], y0[s2], vw.V[(n + 1) & 1], rmax, cm,
                                                evald);
                 cm = ((unsigned long long)__reduce_or_sync(0xffffffffu, (unsigned)(cm >> 32)) << 32) |
