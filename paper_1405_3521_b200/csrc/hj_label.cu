@@ -70,84 +70,8 @@ __global__ void k_feedback(const DevProblem<double, Ts> P, const Ts *__restrict_
     }
 }
 
-// One thread follows the discrete optimal feedback trajectory of one coarse node.
-template <typename Ts, int DIM>
-__global__ void k_label(const DevProblem<double, Ts> P, const Ts *__restrict__ V,
-                        const int8_t *__restrict__ piece, int64_t N, int64_t n_max,
-                        int32_t *label, double *margin_out, double *geo_out, int32_t *steps_out) {
-    const int64_t o[3] = {0, 0, 0};
-    const int64_t vn[3] = {P.n[0], P.n[1], P.n[2]};
-    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < N;
-         t += (int64_t)gridDim.x * blockDim.x) {
-        double g[3] = {(double)(t % P.n[0]), (double)((t / P.n[0]) % P.n[1]),
-                       (double)(t / (P.n[0] * P.n[1]))};
-        double mm = INFINITY, mg = INFINITY;
-        int lab = -1;
-        int64_t s = 0;
-        for (;; ++s) {
-            int64_t r[3] = {0, 0, 0};
-#pragma unroll
-            for (int d = 0; d < DIM; ++d) {
-                double q = g[d] + 0.5;
-                double fl = floor(q);
-                double dist = q - fl;
-                dist = fmin(dist, 1.0 - dist);
-                mg = fmin(mg, dist);
-                int64_t c = (int64_t)fl;
-                if (P.periodic[d]) {
-                    c %= P.n[d];
-                    if (c < 0) c += P.n[d];
-                } else if (c > P.n[d] - 1) {
-                    c = P.n[d] - 1;
-                }
-                r[d] = c;
-            }
-            int pc = piece[r[0] + P.n[0] * (r[1] + P.n[1] * r[2])];
-            if (pc >= 0) {
-                lab = pc;
-                break;
-            }
-            if (s >= n_max) break;
-            int a;
-            double margin;
-            min_bracket<Ts, DIM>(P, V, o, vn, g, &a, &margin);
-            mm = fmin(mm, margin);
-            double x[3] = {0, 0, 0};
-#pragma unroll
-            for (int d = 0; d < DIM; ++d) x[d] = fma(g[d], P.dx[d], P.lo[d]);
-            const int64_t zero[3] = {0, 0, 0};
-            double cs = 1.0;
-            if (P.speed && P.dyn == HJ_DYN_AFFINE)
-                cs = interp<double, Ts, DIM>(P.speed, o, vn, P.n, P.periodic, zero, g, 1.0);
-            double f[3];
-            dynamics(P, x, cs, a, f);
-            bool out = false;
-#pragma unroll
-            for (int d = 0; d < DIM; ++d) {
-                g[d] = fma(P.hdx[d], f[d], g[d]);
-                if (P.periodic[d]) {
-                    double n = (double)P.n[d];
-                    g[d] = g[d] - n * floor(g[d] / n);
-                } else {
-                    double hi = (double)(P.n[d] - 1);
-                    mg = fmin(mg, fmin(fabs(g[d]), fabs(hi - g[d])));
-                    if (g[d] < 0.0 || g[d] > hi) out = true;
-                }
-            }
-            if (out) {
-                ++s;
-                break;
-            }
-        }
-        label[t] = lab;
-        if (margin_out) margin_out[t] = mm;
-        if (geo_out) geo_out[t] = mg;
-        if (steps_out) steps_out[t] = (int32_t)s;
-    }
-}
-
-// Warp-parallel version of the same trajectory: one warp per coarse node, the
-// controls of every feedback evaluation split over the lanes (k = lane, lane+32, ...)
+// The discrete optimal feedback trajectory of one coarse node (R8), one warp per node:
+// the controls of every feedback evaluation split over the lanes (k = lane, lane+32, ...)
 // and combined exactly: smallest bracket, lowest index among equal ones, and the
 // second smallest value of the multiset (so margin = second - best is the serial
 // scan's).  Every lane then takes the same step, so the warp never diverges.
@@ -359,7 +283,7 @@ static hj_status label_impl(const hj_grid &g, const hj_problem &p, const hj_fiel
                             double *geo, int32_t *steps, cudaStream_t s) {
     auto P = make_dev_problem<double, Ts>(g, p, f);
     int64_t N = grid_nodes(g);
-    // one warp per coarse node (k_label_warp); k_label is the one-thread-per-node form
+    // one warp per coarse node
     int blocks = (int)std::min<int64_t>((N + 7) / 8, 148 * 64);
     if (g.dim == 2)
         k_label_warp<Ts, 2><<<blocks, 256, 0, s>>>(P, V, f.piece, N, n_max, label, margin, geo,

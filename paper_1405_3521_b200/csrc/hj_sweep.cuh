@@ -1,28 +1,22 @@
-// hj_sweep.cuh — one Jacobi sweep V^{n+1} = T(V^n) over a set of views
+// hj_sweep.cuh — Jacobi sweeps V^{n+1} = T(V^n) over a set of views
 // (PAPER.md eq. (SL), operator (Tdef) line 238-245, readings R1-R4).
 //
-// Work decomposition: every view (the whole grid, or the bounding box of one
-// sub-domain) is cut into tiles; one CTA per tile of every view, all views in one
-// launch.  Two exact short-cuts, both bit-identical to the plain Jacobi sweep:
-//   * stopped views: a CTA exits at once when its view already met the stopping
-//     rule (res[n-1] < tol), so the stop is exactly the first n with
-//     ||V^{n+1}-V^n|| < tol (R6) and sweeps launched past it cost nothing;
-//   * quiet tiles: T(V)|_tile depends only on V over the tile's dependency
-//     neighbourhood (the tiles within the largest foot offset).  If no node of that
-//     neighbourhood changed (bitwise) in sweep n-1, then V^{n+1} = V^n on the tile,
-//     which the other buffer already holds (it holds V^{n-1} = V^n there), so the
-//     tile is skipped.  Work per sweep follows the active front, not the grid.
+// A view is the whole grid (hj_solve) or the bounding box of one sub-domain
+// (hj_solve_partitioned); all views of a call iterate in the same launches and stop
+// independently.  Exact short-cuts, all bit-identical to the plain Jacobi sweep:
+//   * stopped views: work of a view that met the stopping rule (res[n-1] < tol) is
+//     skipped, so the stop is exactly the first n with ||V^{n+1}-V^n|| < tol (R6);
+//   * quiet tiles / nodes: T(V) on a tile depends only on V over its dependency
+//     neighbourhood; if nothing there changed (bitwise) in sweep n-1 then
+//     V^{n+1} = V^n on the tile, which the other buffer already holds — device work
+//     lists (one-sweep kernels), per-tile flags (blocked kernel) or node-level dirty
+//     masks (cooperative kernel) visit only what can change.
 //
-// Kernels:
-//   k_sweep_local2d<T,KQ,PC>  2-D, isotropic dynamics f = c(x) a (A = b = 0) with
-//       every foot within one cell (Courant <= 1): the foot's cell is fixed by the
-//       control's quadrant, so the 3x3 neighbourhood is staged once in shared memory
-//       and the bracket of every control is 3 FMA + 1 min in registers
-//       (difference form of the bilinear interpolant, prescaled per node).
-//   k_sweep_generic<T,DIM>    any dynamics / cost / h / dim: per node, per control,
-//       foot + multilinear interpolation, corners through L1/L2.
-// Every CTA folds |V^{n+1}-V^n| of its tile into res[n] (one atomicMax) and
-// publishes its "changed" flag for sweep n+1.
+// Kernels: k_sweep_local2d_coop (hj_sweep_coop.cuh; the whole iteration
+// in one cooperative launch: local, field-within-one-cell and Dubins classes),
+// k_sweep_local2d_tb (hj_sweep_tb.cuh; 8 sweeps per launch), k_sweep_local2d_x2 /
+// k_sweep_local2d (one sweep per launch, local class), k_sweep_field2d (any 2-D affine /
+// Van der Pol), k_sweep_dubins (3-D Dubins), k_sweep_generic (anything).
 #pragma once
 
 #include <algorithm>
@@ -79,35 +73,6 @@ __device__ __forceinline__ int find_view(const SweepGroup<T> *__restrict__ G, in
     int v = 0;
     while (v + 1 < G->n_views && G->t[v + 1].tile_base <= b) ++v;
     return v;
-}
-
-// Is any tile of the dependency neighbourhood changed in the previous sweep?
-// (block-wide; every thread returns the same answer).  Periodic axes wrap.
-template <typename T>
-__device__ __forceinline__ bool tile_active(const SweepGroup<T> *__restrict__ G, int v,
-                                            const int tc[3], int64_t it) {
-    if (it == 0) return true;
-    const TileView<T> &tv = G->t[v];
-    const uint8_t *prev = tv.chg + ((it - 1) & 1) * tv.tiles;
-    const int rx = G->radius[0], ry = G->radius[1], rz = G->radius[2];
-    const int wx = 2 * rx + 1, wy = 2 * ry + 1, wz = 2 * rz + 1;
-    const int count = wx * wy * wz;
-    int any = 0;
-    for (int e = threadIdx.x; e < count; e += blockDim.x) {
-        int c[3] = {tc[0] + e % wx - rx, tc[1] + (e / wx) % wy - ry, tc[2] + e / (wx * wy) - rz};
-        bool ok = true;
-#pragma unroll
-        for (int d = 0; d < 3; ++d) {
-            if (c[d] >= 0 && c[d] < tv.nt[d]) continue;
-            if (G->periodic[d]) {
-                c[d] = ((c[d] % tv.nt[d]) + tv.nt[d]) % tv.nt[d];
-            } else {
-                ok = false;
-            }
-        }
-        if (ok) any |= prev[c[0] + tv.nt[0] * ((int64_t)c[1] + (int64_t)tv.nt[1] * c[2])];
-    }
-    return __syncthreads_or(any) != 0;
 }
 
 template <typename T>
