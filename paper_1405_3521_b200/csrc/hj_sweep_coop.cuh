@@ -714,12 +714,15 @@ __global__ void __launch_bounds__(CoopNW<T>::nw * 32, CoopNW<T>::minb)
             g_tb_trace.buf[4 * n + 2] = t_c;
             g_tb_trace.buf[4 * n + 3] = 0ull;
         }
-        // the stopping rule, applied identically by every thread
-        for (int v = 0; v < S.n_views; ++v) {
-            if ((stopped >> v) & 1u) continue;
-            if (*(volatile const double *)&G->v[v].res[n] < tol) {
-                stopped |= 1u << v;
-                stop_at[v] = n + 1;
+        // the stopping rule, applied identically by every warp: lane v reads view v's
+        // residual (one round trip for all views), a ballot spreads the decisions
+        {
+            const bool met = lane < S.n_views && !((stopped >> lane) & 1u) &&
+                             *(volatile const double *)&G->v[lane].res[n] < tol;
+            const unsigned now = __ballot_sync(0xffffffffu, met);
+            if (now) {
+                for (unsigned m = now; m; m &= m - 1) stop_at[__ffs(m) - 1] = n + 1;
+                stopped |= now;
             }
         }
     }

@@ -12,17 +12,30 @@ import hj_workloads as W  # noqa: E402
 from paper_1405_3521_b200 import hj  # noqa: E402
 
 idx = int(sys.argv[1]) if len(sys.argv) > 1 else 2
+isa = len(sys.argv) > 2 and sys.argv[2] == "isa"
 cfg = W.make(idx)
 dp = hj.DeviceProblem(cfg.fine, "f32", sweep_kernel="local_coop")
 cap = 1 << 16
 buf = torch.zeros(4 * cap, dtype=torch.int64, device="cuda")
 L = hj.lib()
 L.hj_debug_set_trace.argtypes = [ctypes.c_void_p, ctypes.c_longlong, ctypes.c_longlong]
-hj.hj_solve(dp)
-L.hj_debug_set_trace(buf.data_ptr(), cap, -1)
-V, rep = hj.hj_solve(dp)
-torch.cuda.synchronize()
-L.hj_debug_set_trace(None, 0, 0)
+if isa:      # trace the partitioned fine solve of one ISA pass (the last cooperative launch)
+    from paper_1405_3521_b200 import pipeline
+    fine = hj.DeviceProblem(cfg.fine, cfg.dtype, reuse_buffers=True)
+    coarse = hj.DeviceProblem(cfg.coarse, cfg.dtype, reuse_buffers=True)
+    pipeline.run_isa(cfg, cfg.dtype, fine=fine, coarse=coarse)
+    L.hj_debug_set_trace(buf.data_ptr(), cap, -1)
+    res = pipeline.run_isa(cfg, cfg.dtype, fine=fine, coarse=coarse)
+    torch.cuda.synchronize()
+    L.hj_debug_set_trace(None, 0, 0)
+    rep = dict(iterations=max(r["iterations"] for r in res["reports"] if r),
+               device_ms=res["reports"][0]["device_ms"])
+else:
+    hj.hj_solve(dp)
+    L.hj_debug_set_trace(buf.data_ptr(), cap, -1)
+    V, rep = hj.hj_solve(dp)
+    torch.cuda.synchronize()
+    L.hj_debug_set_trace(None, 0, 0)
 t = buf.view(-1, 4).cpu().numpy()[: rep["iterations"]].astype(np.float64)
 items = t[:, 3]
 work = (t[:, 1] - t[:, 0]) / 1e3
