@@ -147,6 +147,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--dtype", default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--labeller", default="trajectory", choices=["trajectory", "ra"],
+                    help="sub-domain reconstruction: north_star trajectories or the paper's RA")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -177,7 +179,8 @@ def main():
             dist.barrier()
 
     def step():
-        return pipeline.run_isa(cfg, dtype, rank=rank, world=world, fine=fine, coarse=coarse)
+        return pipeline.run_isa(cfg, dtype, rank=rank, world=world, fine=fine, coarse=coarse,
+                                labeller=args.labeller)
 
     for _ in range(args.warmup):
         step()
@@ -294,6 +297,7 @@ def main():
                        "coarse": list(cfg.coarse.grid.n), "controls": cfg.fine.n_controls,
                        "subdomains": cfg.m, "band": cfg.band, "tol": cfg.fine.tol,
                        "parallelism": f"subdomains over {world} GPU(s)",
+                       "labeller": args.labeller,
                        "l2": "flushed (256 MiB write) between timed steps"},
             "time_to_solution_ms": total_ms / args.steps,
             "step_ms": [round(x, 3) for x in step_ms],

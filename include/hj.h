@@ -17,6 +17,8 @@
  *                         optimal feedback trajectory reaches; prolong the labels to
  *                         the fine grid with an overlap band (ISA steps 1-2,
  *                         PAPER.md line 396-418)
+ *   hj_ra_subdomains      the paper's RA reconstruction (auxiliary solves + threshold,
+ *                         PAPER.md line 310-331), prolonged the same way
  *   hj_partition_plan     bounding boxes / sizes of the fine sub-domains
  *   hj_assign_subdomains  host partitioner: sub-domains -> ranks (GPUs)
  *   hj_solve_partitioned  independent fine solves on the sub-domains and the
@@ -238,6 +240,32 @@ hj_status hj_label_subdomains(const hj_grid *coarse_grid, const hj_problem *coar
                               int32_t band, int32_t m, const int8_t *fine_piece, int32_t *label,
                               double *margin, double *geo, int32_t *steps,
                               uint32_t *fine_mask, void *stream);
+
+/* ---------------------------------------------------------------------------
+ * hj_ra_subdomains — the paper's own reconstruction algorithm RA (PAPER.md
+ * line 310-331), an alternative to hj_label_subdomains' trajectory labels:
+ *   1) for i = 0..m-1 solve V_i = T_i(V_i) on the (coarse) grid with only piece i as
+ *      the target (dG := X_i; the other pieces' nodes are ordinary nodes), as hj_solve;
+ *   2) V = min_i V_i;
+ *   3) Sigma_i = X_i + {x_j : |V_i(j) - V(j)| <= 2 (C dx^q + M dx)}, dx = the largest
+ *      spacing of the grid (C, M, q: the constants of condition (C), line 290-300);
+ * then, if fine_mask != NULL, ISA step 2: the sets are prolonged to the nested fine grid
+ * with the overlap band exactly as hj_label_subdomains does with labels (R9).
+ * Vaux: device, m * N_c values of dtype (V_i of piece i at [i * N_c]); Vmin: device
+ * N_c values; coarse_mask: device uint32[N_c], bit i = node in Sigma_i; fine_mask:
+ * device uint32[N_f] or NULL.  workspace: device, >= hj_ra_workspace_bytes().
+ * reports: host hj_report[m] (one per auxiliary solve), may be NULL.
+ * Returns HJ_ERR_NOT_CONVERGED if an auxiliary solve hit max_iter.  Synchronises.
+ * ------------------------------------------------------------------------- */
+size_t hj_ra_workspace_bytes(const hj_grid *coarse_grid, int32_t dtype, int64_t max_iter);
+
+hj_status hj_ra_subdomains(const hj_grid *coarse_grid, const hj_problem *coarse_prob,
+                           const hj_fields *coarse_fields, int32_t dtype, int32_t m, double C,
+                           double M, double q, double tol, int64_t max_iter,
+                           const hj_grid *fine_grid, const int32_t ratio[3], int32_t band,
+                           const int8_t *fine_piece, void *Vaux, void *Vmin,
+                           uint32_t *coarse_mask, uint32_t *fine_mask, void *workspace,
+                           size_t ws_bytes, void *stream, hj_report *reports);
 
 /* ---------------------------------------------------------------------------
  * hj_partition_plan — sizes of the fine sub-domains S_0..S_{m-1} from the mask.

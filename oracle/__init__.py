@@ -104,6 +104,10 @@ def _load():
                                            _dp, _dp]
             lib.or_prolong.argtypes = [_lp, _lp, _ip, ctypes.c_int, _lp, ctypes.c_long, _ip,
                                        ctypes.c_int, _bp, _up]
+            lib.or_prolong_mask.argtypes = [_lp, _lp, _ip, ctypes.c_int, _lp, ctypes.c_long, _up,
+                                            ctypes.c_int, _bp, _up]
+            lib.or_ra_masks.argtypes = [ctypes.c_long, ctypes.c_int, ctypes.POINTER(_dp), _dp, _bp,
+                                        ctypes.c_double, _up]
             lib.or_solve_subdomain.argtypes = [P, _up, ctypes.c_int, _dp, ctypes.c_double,
                                                ctypes.c_long, _dp]
             lib.or_solve_subdomain.restype = ctypes.c_long
@@ -264,6 +268,49 @@ def prolong(coarse_grid, fine_grid, ratio, band, coarse_label, m, fine_piece):
     lib.or_prolong(_ptr(nc, _lp), _ptr(nf, _lp), _ptr(per, _ip), dim, _ptr(rr, _lp), int(band),
                    _ptr(lab, _ip), int(m), _ptr(fp, _bp), _ptr(out, _up))
     return out
+
+
+def prolong_mask(coarse_grid, fine_grid, ratio, band, coarse_mask, m, fine_piece):
+    """ISA step 2 from coarse membership masks (RA output), with the band (R9)."""
+    lib = _load()
+    dim = fine_grid.dim
+    nc = np.ones(3, np.int64)
+    nf = np.ones(3, np.int64)
+    per = np.zeros(3, np.int32)
+    rr = np.ones(3, np.int64)
+    for d in range(dim):
+        nc[d], nf[d], per[d], rr[d] = coarse_grid.n[d], fine_grid.n[d], fine_grid.periodic[d], ratio[d]
+    cm = np.ascontiguousarray(coarse_mask, np.uint32)
+    fp = np.ascontiguousarray(fine_piece, np.int8)
+    out = np.empty(fine_grid.size, np.uint32)
+    lib.or_prolong_mask(_ptr(nc, _lp), _ptr(nf, _lp), _ptr(per, _ip), dim, _ptr(rr, _lp),
+                        int(band), _ptr(cm, _up), int(m), _ptr(fp, _bp), _ptr(out, _up))
+    return out
+
+
+def ra(problem, m, C, M, q, tol=None, max_iter=None):
+    """The paper's reconstruction algorithm RA on one grid:
+    1) V_i = T_i(V_i), the problem with only piece i as the target (dG := X_i);
+    2) V = min_i V_i;  3) Sigma_i = X_i + {j : |V_i(j) - V(j)| <= 2 (C dx^q + M dx)}.
+    dx = the largest grid spacing.  Returns (V_i list, V, mask, iterations)."""
+    import dataclasses
+    lib = _load()
+    piece = np.asarray(problem.piece, np.int8)
+    Vs, its = [], []
+    for i in range(m):
+        pi = np.where(piece == i, np.int8(i), np.int8(-1)).astype(np.int8)
+        V, it, _ = OracleProblem(dataclasses.replace(problem, piece=pi)).solve(tol, max_iter)
+        Vs.append(V)
+        its.append(it)
+    Vmin = np.minimum.reduce(Vs)
+    dx = max(problem.grid.spacing(d) for d in range(problem.grid.dim))
+    thr = 2.0 * (C * dx ** q + M * dx)
+    arrs = [np.ascontiguousarray(v, np.float64) for v in Vs]
+    ptrs = (_dp * m)(*[_ptr(a, _dp) for a in arrs])
+    mask = np.empty(problem.grid.size, np.uint32)
+    lib.or_ra_masks(problem.grid.size, int(m), ptrs, _ptr(np.ascontiguousarray(Vmin), _dp),
+                    _ptr(np.ascontiguousarray(piece), _bp), float(thr), _ptr(mask, _up))
+    return Vs, Vmin, mask, its
 
 
 def assemble(mask, Vks, v_out):

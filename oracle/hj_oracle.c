@@ -363,9 +363,13 @@ void or_label_nodes(const or_problem *p, const double *V, const long *nodes, lon
  * (periodic axes measured around the circle).  Coarse nodes labelled -1 count
  * for every sub-domain ("automatically included in each approximation", §4.1
  * line 587).  Target nodes of piece k on the fine grid are always in k. */
-void or_prolong(const long nc[3], const long nf[3], const int periodic[3], int dim,
-                const long ratio[3], long band, const int *coarse_label, int m,
-                const signed char *fine_piece, unsigned int *fine_mask) {
+/* Prolongation of coarse sub-domain memberships (bit k of coarse_mask = coarse node in
+ * the k-th set) to the fine grid with the overlap band (R9): fine node i is in S_k iff a
+ * coarse node I with bit k has |i_d - R_d I_d| <= R_d + band on every axis; fine target
+ * nodes of piece k are always in S_k. */
+void or_prolong_mask(const long nc[3], const long nf[3], const int periodic[3], int dim,
+                     const long ratio[3], long band, const unsigned int *coarse_mask, int m,
+                     const signed char *fine_piece, unsigned int *fine_mask) {
     unsigned int all = (m >= 32) ? 0xffffffffu : ((1u << m) - 1u);
     long Nf = 1;
     for (int d = 0; d < dim; ++d) Nf *= nf[d];
@@ -402,11 +406,37 @@ void or_prolong(const long nc[3], const long nf[3], const int periodic[3], int d
                     if (!ok) continue;
                     long cidx = 0;
                     for (int d = dim - 1; d >= 0; --d) cidx = cidx * nc[d] + J[d];
-                    int lab = coarse_label[cidx];
-                    bits |= (lab < 0) ? all : (1u << lab);
+                    bits |= coarse_mask[cidx];
                 }
         if (fine_piece[idx] >= 0) bits |= 1u << fine_piece[idx];
         fine_mask[idx] = bits & all;
+    }
+}
+
+/* ISA step 2 from trajectory labels (R8, R9): label k -> bit k, label -1 (the
+ * trajectory left the box or ran out of steps) -> every bit ("automatically included in
+ * each approximation"). */
+void or_prolong(const long nc[3], const long nf[3], const int periodic[3], int dim,
+                const long ratio[3], long band, const int *coarse_label, int m,
+                const signed char *fine_piece, unsigned int *fine_mask) {
+    unsigned int all = (m >= 32) ? 0xffffffffu : ((1u << m) - 1u);
+    long Nc = 1;
+    for (int d = 0; d < dim; ++d) Nc *= nc[d];
+    unsigned int *cm = (unsigned int *)malloc(sizeof(unsigned int) * (size_t)Nc);
+    for (long j = 0; j < Nc; ++j) cm[j] = coarse_label[j] < 0 ? all : (1u << coarse_label[j]);
+    or_prolong_mask(nc, nf, periodic, dim, ratio, band, cm, m, fine_piece, fine_mask);
+    free(cm);
+}
+
+/* RA step 3: Sigma_i = X_i plus every node j with
+ * |V_i(j) - V(j)| <= thr, thr = 2 (C dx^q + M dx); bit i of mask[j]. */
+void or_ra_masks(long N, int m, const double *const *Vi, const double *V,
+                 const signed char *piece, double thr, unsigned int *mask) {
+    for (long j = 0; j < N; ++j) {
+        unsigned int bits = 0;
+        for (int i = 0; i < m; ++i)
+            if (piece[j] == i || fabs(Vi[i][j] - V[j]) <= thr) bits |= 1u << i;
+        mask[j] = bits;
     }
 }
 

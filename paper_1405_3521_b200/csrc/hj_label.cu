@@ -226,8 +226,13 @@ __device__ __forceinline__ int64_t floordiv(int64_t a, int64_t b) {
     return (a % b != 0 && ((a < 0) != (b < 0))) ? q - 1 : q;
 }
 
-__global__ void k_prolong(const ProlongArgs A, const int32_t *__restrict__ lab,
+// MASK = false: coarse trajectory labels (k -> bit k, -1 -> every bit, R9);
+// MASK = true: coarse membership bit masks (the RA sets)
+template <bool MASK>
+__global__ void k_prolong(const ProlongArgs A, const void *__restrict__ coarse,
                           const int8_t *__restrict__ fine_piece, int64_t Nf, uint32_t *mask) {
+    const int32_t *lab = (const int32_t *)coarse;
+    const uint32_t *cmask = (const uint32_t *)coarse;
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < Nf;
          t += (int64_t)gridDim.x * blockDim.x) {
         int64_t ii[3] = {t % A.nf[0], (t / A.nf[0]) % A.nf[1], t / (A.nf[0] * A.nf[1])};
@@ -254,13 +259,43 @@ __global__ void k_prolong(const ProlongArgs A, const int32_t *__restrict__ lab,
                         J[d] = c;
                     }
                     if (!ok) continue;
-                    int32_t l = lab[J[0] + A.nc[0] * (J[1] + A.nc[1] * J[2])];
-                    bits |= (l < 0) ? A.all : (1u << l);
+                    const int64_t cidx = J[0] + A.nc[0] * (J[1] + A.nc[1] * J[2]);
+                    if (MASK) {
+                        bits |= cmask[cidx];
+                    } else {
+                        const int32_t l = lab[cidx];
+                        bits |= (l < 0) ? A.all : (1u << l);
+                    }
                 }
         int8_t p = fine_piece[t];
         if (p >= 0) bits |= 1u << p;
         mask[t] = bits & A.all;
     }
+}
+
+// ISA step 2 (R9) from labels or masks of the coarse grid cg onto the nested fine grid fg
+hj_status prolong_launch(const hj_grid &cg, const hj_grid &fg, const int32_t ratio[3],
+                         int32_t band, int32_t m, const void *coarse, bool is_mask,
+                         const int8_t *fine_piece, uint32_t *fine_mask, cudaStream_t s) {
+    ProlongArgs A;
+    memset(&A, 0, sizeof(A));
+    A.dim = fg.dim;
+    for (int d = 0; d < 3; ++d) {
+        A.nc[d] = d < cg.dim ? cg.n[d] : 1;
+        A.nf[d] = d < fg.dim ? fg.n[d] : 1;
+        A.R[d] = d < fg.dim ? ratio[d] : 1;
+        A.periodic[d] = d < fg.dim ? fg.periodic[d] : 0;
+    }
+    A.band = band;
+    A.all = m >= 32 ? 0xffffffffu : ((1u << m) - 1u);
+    const int64_t Nf = grid_nodes(fg);
+    const int blocks = (int)std::min<int64_t>((Nf + 255) / 256, 148 * 16);
+    if (is_mask)
+        k_prolong<true><<<blocks, 256, 0, s>>>(A, coarse, fine_piece, Nf, fine_mask);
+    else
+        k_prolong<false><<<blocks, 256, 0, s>>>(A, coarse, fine_piece, Nf, fine_mask);
+    HJ_CUDA(cudaGetLastError());
+    return HJ_OK;
 }
 
 template <typename Ts>
@@ -347,22 +382,7 @@ hj_status hj_label_subdomains(const hj_grid *cg, const hj_problem *cp, const hj_
                          : label_impl<float>(*cg, *cp, *cf, (const float *)Vc, n_max, label,
                                              margin, geo, steps, s);
     if (st != HJ_OK) return st;
-    ProlongArgs A;
-    memset(&A, 0, sizeof(A));
-    A.dim = fg->dim;
-    for (int d = 0; d < 3; ++d) {
-        A.nc[d] = d < cg->dim ? cg->n[d] : 1;
-        A.nf[d] = d < fg->dim ? fg->n[d] : 1;
-        A.R[d] = d < fg->dim ? ratio[d] : 1;
-        A.periodic[d] = d < fg->dim ? fg->periodic[d] : 0;
-    }
-    A.band = band;
-    A.all = m >= 32 ? 0xffffffffu : ((1u << m) - 1u);
-    int64_t Nf = grid_nodes(*fg);
-    int blocks = (int)std::min<int64_t>((Nf + 255) / 256, 148 * 16);
-    k_prolong<<<blocks, 256, 0, s>>>(A, label, fine_piece, Nf, fine_mask);
-    HJ_CUDA(cudaGetLastError());
-    return HJ_OK;
+    return prolong_launch(*cg, *fg, ratio, band, m, label, false, fine_piece, fine_mask, s);
 }
 
 }  // extern "C"

@@ -575,6 +575,81 @@ static hj_status partitioned_impl(const hj_grid &grid, const hj_problem &prob,
     return HJ_OK;
 }
 
+// ---------------------------------------------------------------------------
+// RA: the paper's reconstruction of the independent sub-domains (PAPER.md line
+// 310-331): m auxiliary solves with only piece i as the target, V = min_i V_i, and
+// Sigma_i = X_i + {j : |V_i(j) - V(j)| <= 2 (C dx^q + M dx)}.
+// ---------------------------------------------------------------------------
+__global__ void k_piece_only(const int8_t *__restrict__ piece, int i, int64_t N, int8_t *out) {
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < N;
+         j += (int64_t)gridDim.x * blockDim.x)
+        out[j] = piece[j] == i ? (int8_t)i : (int8_t)-1;
+}
+
+template <typename T>
+__global__ void k_ra_masks(const T *__restrict__ Vaux, int m, int64_t N,
+                           const int8_t *__restrict__ piece, double thr, T *Vmin,
+                           uint32_t *mask) {
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < N;
+         j += (int64_t)gridDim.x * blockDim.x) {
+        T v = Vaux[j];
+        for (int i = 1; i < m; ++i) v = fmin(v, Vaux[(int64_t)i * N + j]);
+        uint32_t bits = 0;
+        for (int i = 0; i < m; ++i) {
+            const double d = fabs((double)Vaux[(int64_t)i * N + j] - (double)v);
+            if (piece[j] == i || d <= thr) bits |= 1u << i;
+        }
+        Vmin[j] = v;
+        mask[j] = bits;
+    }
+}
+
+template <typename T>
+static size_t ra_ws(const hj_grid &g, int64_t max_iter) {
+    return Carver::align(grid_nodes(g)) + solve_ws<T>(g, max_iter);
+}
+
+template <typename T>
+static hj_status ra_impl(const hj_grid &cg, const hj_problem &cp, const hj_fields &cf, int m,
+                         double C, double M, double q, double tol, int64_t max_iter,
+                         const hj_grid &fg, const int32_t ratio[3], int32_t band,
+                         const int8_t *fine_piece, T *Vaux, T *Vmin, uint32_t *cmask,
+                         uint32_t *fmask, void *ws, size_t ws_bytes, cudaStream_t s,
+                         hj_report *reps) {
+    const int64_t N = grid_nodes(cg);
+    if (ws_bytes < ra_ws<T>(cg, max_iter)) {
+        set_error("workspace too small: need %zu bytes, got %zu", ra_ws<T>(cg, max_iter), ws_bytes);
+        return HJ_ERR_WORKSPACE;
+    }
+    int8_t *pi = (int8_t *)ws;
+    char *sws = (char *)ws + Carver::align(N);
+    const size_t sws_bytes = ws_bytes - Carver::align(N);
+    const int blocks = (int)std::min<int64_t>((N + 255) / 256, 148 * 16);
+    for (int i = 0; i < m; ++i) {          // 1) the auxiliary problems (dG := X_i)
+        k_piece_only<<<blocks, 256, 0, s>>>(cf.piece, i, N, pi);
+        HJ_CUDA(cudaGetLastError());
+        hj_fields fi = cf;
+        fi.piece = pi;
+        hj_report r;
+        memset(&r, 0, sizeof(r));
+        hj_status st = solve_impl<T>(cg, cp, fi, Vaux + (int64_t)i * N, tol, max_iter, sws,
+                                     sws_bytes, s, &r);
+        if (reps) reps[i] = r;
+        if (st != HJ_OK) return st;
+    }
+    double dx = 0;                         // 2-3) V = min_i V_i, the sets Sigma_i
+    for (int d = 0; d < cg.dim; ++d) dx = std::max(dx, grid_spacing(cg, d));
+    const double thr = 2.0 * (C * std::pow(dx, q) + M * dx);
+    k_ra_masks<T><<<blocks, 256, 0, s>>>(Vaux, m, N, cf.piece, thr, Vmin, cmask);
+    HJ_CUDA(cudaGetLastError());
+    if (fmask) {                           // ISA step 2 with the band (R9)
+        hj_status st = prolong_launch(cg, fg, ratio, band, m, cmask, true, fine_piece, fmask, s);
+        if (st != HJ_OK) return st;
+    }
+    HJ_CUDA(cudaStreamSynchronize(s));
+    return HJ_OK;
+}
+
 }  // namespace hj
 
 using namespace hj;
@@ -612,6 +687,51 @@ hj_status hj_solve(const hj_grid *grid, const hj_problem *prob, const hj_fields 
                                   ws_bytes, s, report);
     return solve_impl<float>(*grid, *prob, *fields, (float *)V, tol, max_iter, workspace,
                              ws_bytes, s, report);
+}
+
+size_t hj_ra_workspace_bytes(const hj_grid *coarse_grid, int32_t dtype, int64_t max_iter) {
+    if (!coarse_grid || validate_grid(coarse_grid) != HJ_OK || max_iter < 1) return 0;
+    return dtype == HJ_F64 ? ra_ws<double>(*coarse_grid, max_iter)
+                           : ra_ws<float>(*coarse_grid, max_iter);
+}
+
+hj_status hj_ra_subdomains(const hj_grid *cg, const hj_problem *cp, const hj_fields *cf,
+                           int32_t dtype, int32_t m, double C, double M, double q, double tol,
+                           int64_t max_iter, const hj_grid *fg, const int32_t ratio[3],
+                           int32_t band, const int8_t *fine_piece, void *Vaux, void *Vmin,
+                           uint32_t *coarse_mask, uint32_t *fine_mask, void *workspace,
+                           size_t ws_bytes, void *stream, hj_report *reports) {
+    clear_error();
+    hj_status st;
+    if ((st = validate_grid(cg)) != HJ_OK) return st;
+    if ((st = validate_problem(cg, cp)) != HJ_OK) return st;
+    if ((st = validate_fields(cf)) != HJ_OK) return st;
+    HJ_CHECK(m >= 1 && m <= HJ_MAX_SUBDOMAINS, "m must be in [1, %d]", HJ_MAX_SUBDOMAINS);
+    HJ_CHECK(Vaux && Vmin && coarse_mask && workspace, "NULL argument");
+    HJ_CHECK(C >= 0 && M >= 0 && q > 0, "need C >= 0, M >= 0, q > 0");
+    HJ_CHECK(max_iter >= 1 && tol > 0, "need max_iter >= 1 and tol > 0");
+    HJ_CHECK(dtype == HJ_F32 || dtype == HJ_F64, "dtype must be HJ_F32 or HJ_F64");
+    if (fine_mask) {
+        HJ_CHECK(fg && ratio && fine_piece, "fine_mask needs fine_grid, ratio and fine_piece");
+        if ((st = validate_grid(fg)) != HJ_OK) return st;
+        HJ_CHECK(band >= 0 && cg->dim == fg->dim, "band >= 0 and equal dims required");
+        for (int d = 0; d < cg->dim; ++d) {
+            HJ_CHECK(ratio[d] >= 1, "ratio[%d] must be >= 1", d);
+            if (fg->periodic[d])
+                HJ_CHECK(fg->n[d] == ratio[d] * cg->n[d], "periodic axis %d not nested", d);
+            else
+                HJ_CHECK(fg->n[d] - 1 == ratio[d] * (cg->n[d] - 1), "axis %d not nested", d);
+        }
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    const hj_grid &fgr = fine_mask ? *fg : *cg;
+    if (dtype == HJ_F64)
+        return ra_impl<double>(*cg, *cp, *cf, m, C, M, q, tol, max_iter, fgr, ratio, band,
+                               fine_piece, (double *)Vaux, (double *)Vmin, coarse_mask, fine_mask,
+                               workspace, ws_bytes, s, reports);
+    return ra_impl<float>(*cg, *cp, *cf, m, C, M, q, tol, max_iter, fgr, ratio, band, fine_piece,
+                          (float *)Vaux, (float *)Vmin, coarse_mask, fine_mask, workspace,
+                          ws_bytes, s, reports);
 }
 
 hj_status hj_partition_plan(const hj_grid *grid, const uint32_t *fine_mask, int32_t m,

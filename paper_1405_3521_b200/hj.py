@@ -72,7 +72,8 @@ class hj_subdomain(ctypes.Structure):
 
 EXPORTS = ["hj_last_error", "hj_version", "hj_solve_workspace_bytes", "hj_solve",
            "hj_coarse_feedback", "hj_label_subdomains", "hj_partition_plan",
-           "hj_assign_subdomains", "hj_solve_partitioned"]
+           "hj_assign_subdomains", "hj_solve_partitioned", "hj_ra_workspace_bytes",
+           "hj_ra_subdomains"]
 
 
 # hj.h HJ_SWEEP_*
@@ -104,8 +105,15 @@ def lib():
         L.hj_assign_subdomains.argtypes = [i32, S, i32, ctypes.POINTER(i32)]
         L.hj_solve_partitioned.argtypes = [G, P, F, i32, vp, i32, S, ctypes.c_uint32,
                                            ctypes.c_double, i64, vp, vp, ctypes.c_size_t, vp, R]
+        L.hj_ra_workspace_bytes.argtypes = [G, i32, i64]
+        L.hj_ra_workspace_bytes.restype = ctypes.c_size_t
+        dbl = ctypes.c_double
+        L.hj_ra_subdomains.argtypes = [G, P, F, i32, i32, dbl, dbl, dbl, dbl, i64, G,
+                                       ctypes.POINTER(i32), i32, vp, vp, vp, vp, vp, vp,
+                                       ctypes.c_size_t, vp, R]
         for name in EXPORTS[2:]:
-            getattr(L, name).restype = ctypes.c_int
+            if not name.endswith("_bytes"):
+                getattr(L, name).restype = ctypes.c_int
         _lib = L
     return _lib
 
@@ -288,3 +296,38 @@ def hj_solve_partitioned(fine: DeviceProblem, mask, m, plan, ws_bytes, solve_set
         int(max_iter), Vbar.data_ptr(), workspace.data_ptr(), workspace.numel(), _stream(stream),
         reps))
     return Vbar, [reps[k].as_dict() if (solve_set >> k) & 1 else None for k in range(m)]
+
+
+def hj_ra_subdomains(coarse: DeviceProblem, m, C=1.0, M=1.0, q=0.5, fine: DeviceProblem = None,
+                     ratio=None, band=0, tol=None, max_iter=None, stream=None):
+    """The paper's RA reconstruction on the coarse grid, prolonged
+    to the fine grid when `fine` is given.  Returns dict(Vaux (m x N_c), Vmin,
+    coarse_mask, mask (fine, or None), reports)."""
+    prob = coarse.prob
+    tol = prob.tol if tol is None else tol
+    max_iter = prob.max_iter if max_iter is None else max_iter
+    L = lib()
+    Nc = coarse.N
+    td = _torch_dtype(coarse.dtype)
+    Vaux = _buf(coarse, "ra_Vaux", m * Nc, td)
+    Vmin = _buf(coarse, "ra_Vmin", Nc, td)
+    cmask = _buf(coarse, "ra_cmask", Nc, torch.int32)
+    need = L.hj_ra_workspace_bytes(ctypes.byref(coarse.grid), _code(coarse.dtype), int(max_iter))
+    ws = _buf(coarse, "ra_ws", need, torch.uint8)
+    fmask = None
+    r = (ctypes.c_int32 * 3)(1, 1, 1)
+    if fine is not None:
+        fmask = _buf(fine, "mask", fine.N, torch.int32)
+        for d in range(len(ratio)):
+            r[d] = int(ratio[d])
+    reps = (hj_report * m)()
+    _check(L.hj_ra_subdomains(
+        ctypes.byref(coarse.grid), ctypes.byref(coarse.cprob), ctypes.byref(coarse.fields),
+        _code(coarse.dtype), int(m), float(C), float(M), float(q), float(tol), int(max_iter),
+        ctypes.byref(fine.grid) if fine is not None else None, r, int(band),
+        fine.piece.data_ptr() if fine is not None else None, Vaux.data_ptr(), Vmin.data_ptr(),
+        cmask.data_ptr(), fmask.data_ptr() if fmask is not None else None, ws.data_ptr(),
+        ws.numel(), _stream(stream), reps))
+    return dict(Vaux=Vaux.view(m, Nc), Vmin=Vmin, coarse_mask=cmask, mask=fmask,
+                reports=[reps[i].as_dict() for i in range(m)])
+

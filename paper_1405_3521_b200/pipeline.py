@@ -31,7 +31,7 @@ def gather_min(V, group=None):
 
 
 def run_isa(cfg, dtype="f32", device="cuda", rank=0, world=1, group=None, fine=None, coarse=None,
-            gather=True):
+            gather=True, labeller="trajectory", ra_params=(1.0, 1.0, 0.5)):
     """Returns dict(V=assembled fine field (on every rank after the MIN all-reduce when
     gather), labels, mask, plan, owners, reports, timings)."""
     t = {}
@@ -40,9 +40,20 @@ def run_isa(cfg, dtype="f32", device="cuda", rank=0, world=1, group=None, fine=N
     s = torch.cuda.current_stream()
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
     ev[0].record(s)
-    Vc, rep_c = hj.hj_solve(coarse)
-    ev[1].record(s)
-    lab = hj.hj_label_subdomains(coarse, Vc, cfg.n_max_steps, fine, cfg.ratio, cfg.band, cfg.m)
+    if labeller == "ra":   # the paper's RA: auxiliary solves + threshold
+        C, M, q = ra_params
+        ra = hj.hj_ra_subdomains(coarse, cfg.m, C, M, q, fine=fine, ratio=cfg.ratio,
+                                 band=cfg.band)
+        Vc, rep_c = ra["Vmin"], dict(ra["reports"][0])
+        for key in ("node_updates", "evaluated_updates", "launches"):
+            rep_c[key] = sum(r[key] for r in ra["reports"])
+        ev[1].record(s)
+        lab = dict(label=None, mask=ra["mask"], coarse_mask=ra["coarse_mask"], Vaux=ra["Vaux"])
+    else:
+        Vc, rep_c = hj.hj_solve(coarse)
+        ev[1].record(s)
+        lab = hj.hj_label_subdomains(coarse, Vc, cfg.n_max_steps, fine, cfg.ratio, cfg.band,
+                                     cfg.m)
     ev[2].record(s)
     plan, ws = hj.hj_partition_plan(fine, lab["mask"], cfg.m)
     owners = hj.hj_assign_subdomains(plan, world)

@@ -371,3 +371,54 @@ def test_full_size_solve_and_labels(idx):
     mask_o = oracle.prolong(cfg.coarse.grid, cfg.fine.grid, cfg.ratio, cfg.band,
                             res["labels"]["label"].cpu().numpy(), cfg.m, cfg.fine.piece)
     assert np.array_equal(res["mask"].cpu().numpy().view(np.uint32), mask_o)
+
+
+# ---------------------------------------------------------------------------
+# the paper's RA reconstruction on the GPU
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("idx,dtype", [(1, "f64"), (2, "f32"), (1, "f32")])
+def test_ra_matches_oracle(idx, dtype):
+    cfg = _cfg(idx)
+    tol = cfg.coarse.tol if dtype == "f64" else max(cfg.coarse.tol, 1e-7)
+    C, M, q = 1.0, 1.0, 0.5
+    coarse = hj.DeviceProblem(cfg.coarse, dtype)
+    fine = hj.DeviceProblem(cfg.fine, dtype)
+    out = hj.hj_ra_subdomains(coarse, cfg.m, C, M, q, fine=fine, ratio=cfg.ratio, band=cfg.band,
+                              tol=tol)
+    Vs, Vmin, cmask_o, its = oracle.ra(cfg.coarse, cfg.m, C, M, q, tol=tol)
+    Vaux = out["Vaux"].double().cpu().numpy()
+    for i in range(cfg.m):
+        assert np.abs(Vaux[i] - Vs[i]).max() <= TOL[dtype], i
+        if dtype == "f64":
+            assert out["reports"][i]["iterations"] == its[i]
+    assert np.abs(out["Vmin"].double().cpu().numpy() - Vmin).max() <= TOL[dtype]
+    # sets: bit-exact wherever |V_i - V| is not within the value tolerance of the threshold
+    g = cfg.coarse.grid
+    thr = 2 * (C * max(g.spacing(d) for d in range(g.dim)) ** q
+               + M * max(g.spacing(d) for d in range(g.dim)))
+    cm = out["coarse_mask"].cpu().numpy().view(np.uint32)
+    near = np.zeros(g.size, bool)
+    for i in range(cfg.m):
+        near |= np.abs(np.abs(Vs[i] - Vmin) - thr) <= 4 * TOL[dtype]
+    assert np.array_equal(cm[~near], cmask_o[~near])
+    print(f"config {idx} {dtype}: RA threshold ties {int(near.sum())} of {g.size}")
+    # prolongation of the GPU sets: bit-exact
+    fm = oracle.prolong_mask(cfg.coarse.grid, cfg.fine.grid, cfg.ratio, cfg.band, cm, cfg.m,
+                             cfg.fine.piece)
+    assert np.array_equal(out["mask"].cpu().numpy().view(np.uint32), fm)
+
+
+def test_isa_with_ra_sets_matches_oracle():
+    """ISA steps 3-4 on the RA sets: the assembled field equals the oracle's masked solves
+    + assembly on the same sets, and (Prop. 4.1) the whole-grid solution to O(dx)."""
+    cfg = _cfg(1)
+    res = pipeline.run_isa(cfg, "f64", labeller="ra")
+    mask = res["mask"].cpu().numpy().view(np.uint32)
+    of = oracle.OracleProblem(cfg.fine)
+    Vks = [of.solve_subdomain(mask, k)[0] for k in range(cfg.m)]
+    Vbar_o = oracle.assemble(mask, Vks, cfg.fine.v_out)
+    assert np.abs(res["V"].double().cpu().numpy() - Vbar_o).max() <= TOL["f64"]
+    Vo, _, _ = of.solve()
+    diff = Vbar_o - Vo
+    assert diff.min() >= -10 * cfg.fine.tol
+    assert diff.max() <= cfg.fine.grid.spacing(0)
