@@ -25,6 +25,11 @@
 
 namespace hj {
 
+// keep a value in a register as computed (stops the compiler from re-deriving it from
+// its inputs inside a loop, which it otherwise does under register pressure)
+__device__ __forceinline__ void opaque(float &x) { asm volatile("" : "+f"(x)); }
+__device__ __forceinline__ void opaque(double &x) { asm volatile("" : "+d"(x)); }
+
 struct CoopState {
     int64_t mt_base[HJ_MAX_SUBDOMAINS + 1];   // first global mini-tile id of each view
     int32_t mt0[HJ_MAX_SUBDOMAINS], mt1[HJ_MAX_SUBDOMAINS], mt2[HJ_MAX_SUBDOMAINS];
@@ -329,13 +334,16 @@ __device__ __forceinline__ void coop_eval_field(const DevProblem<T, T> &P, const
             const T X01 = beta * ((q0[-BP + 1] - Vp0) - (V0m - V00));   // +x -y
             const T X11 = beta * ((q0[-BP - 1] - Vm0) - (V0m - V00));   // -x -y
             const T C0 = fma(beta, V00, base);
+            T dx8[8] = {Dxp, Dxm, Dyp, Dym, X00, X10, X01, X11};
+#pragma unroll
+            for (int e = 0; e < 8; ++e) opaque(dx8[e]);
 #pragma unroll 4
             for (int k = 0; k < P.K; ++k) {
                 const T d0 = DYN == HJ_DYN_AFFINE ? fma(S0, P.ctrl[k][0], D0) : D0;
                 const T d1 = fma(S1, P.ctrl[k][DYN == HJ_DYN_AFFINE ? 1 : 0], D1);
                 const bool nx = d0 < T(0), ny = d1 < T(0);
-                const T A1 = nx ? Dxm : Dxp, A2 = ny ? Dym : Dyp;
-                const T A3 = ny ? (nx ? X11 : X01) : (nx ? X10 : X00);
+                const T A1 = nx ? dx8[1] : dx8[0], A2 = ny ? dx8[3] : dx8[2];
+                const T A3 = ny ? (nx ? dx8[7] : dx8[6]) : (nx ? dx8[5] : dx8[4]);
                 const T w0 = fabs(d0), w1 = fabs(d1);
                 const T ck = kruz ? C0 : C0 + hlr * P.csq[k];
                 best = fmin(best, fma(w1, fma(w0, A3, A2), fma(w0, A1, ck)));
