@@ -512,9 +512,14 @@ __global__ void __launch_bounds__(CoopNW<T>::nw * 32, CoopNW<T>::minb)
     const unsigned all = S.n_views >= 32 ? 0xffffffffu : ((1u << S.n_views) - 1u);
     int64_t n = 0;
     const bool tr = g_tb_trace.buf != nullptr && blockIdx.x == 0 && threadIdx.x == 0;
-    unsigned long long t_a = 0, t_b = 0;
+    unsigned long long t_a = 0, t_b = 0, t_s = 0;
+    int qitems = 0;
     for (; n < max_iter && stopped != all; ++n) {
-        if (tr) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_a));
+        if (tr) {
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_a));
+            t_s = 0;
+            qitems = 0;
+        }
         if (threadIdx.x < HJ_MAX_SUBDOMAINS) {
             cres[threadIdx.x] = 0ull;
             cwork[threadIdx.x] = 0ull;
@@ -558,6 +563,8 @@ __global__ void __launch_bounds__(CoopNW<T>::nw * 32, CoopNW<T>::minb)
             __syncthreads();
         }
         const int cnt = qn;
+        if (tr && t_s == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_s));
+        if (tr) qitems += cnt;
         // two mini-tiles per warp iteration: every global load of both (masks, the
         // 10 x 10 blocks of V^n, the speeds) is issued before any is used, and the mask
         // updates of both go out together
@@ -720,7 +727,7 @@ __global__ void __launch_bounds__(CoopNW<T>::nw * 32, CoopNW<T>::minb)
             g_tb_trace.buf[4 * n] = t_a;
             g_tb_trace.buf[4 * n + 1] = t_b;
             g_tb_trace.buf[4 * n + 2] = t_c;
-            g_tb_trace.buf[4 * n + 3] = 0ull;
+            g_tb_trace.buf[4 * n + 3] = ((t_s - t_a) << 16) | (unsigned long long)qitems;
         }
         // the stopping rule, applied identically by every warp: lane v reads view v's
         // residual (one round trip for all views), a ballot spreads the decisions

@@ -37,12 +37,15 @@ else:
     torch.cuda.synchronize()
     L.hj_debug_set_trace(None, 0, 0)
 t = buf.view(-1, 4).cpu().numpy()[: rep["iterations"]].astype(np.float64)
-items = t[:, 3]
+raw = buf.view(-1, 4).cpu().numpy()[: rep["iterations"], 3]
+items = (raw & 0xffff).astype(np.float64)
+scan = (raw >> 16).astype(np.float64) / 1e3
 work = (t[:, 1] - t[:, 0]) / 1e3
 sync = (t[:, 2] - t[:, 1]) / 1e3
 gap = (t[1:, 0] - t[:-1, 2]) / 1e3
 print(f"sweeps {len(t)}  total {(t[-1, 2] - t[0, 0]) / 1e6:.2f} ms  device {rep['device_ms']:.2f} ms")
-for name, x in (("items", items), ("block0 work us", work), ("sync us", sync), ("post-sync us", gap)):
+for name, x in (("block0 items", items), ("block0 scan us", scan), ("block0 work us", work),
+                ("sync us", sync), ("post-sync us", gap)):
     print(f"{name:15s} mean {x.mean():8.2f}  med {np.median(x):8.2f}  max {x.max():8.2f}")
 for k in (0, 100, 300, 500, 700):
     if k < len(t):
