@@ -470,6 +470,21 @@ __device__ __forceinline__ void coop_eval_dubins(const DevProblem<T, T> &P, cons
     evald_out = evald;
 }
 
+template <typename T>
+struct CoopBits;
+template <>
+struct CoopBits<float> {
+    using U = unsigned;
+    static __device__ __forceinline__ U bits(float x) { return __float_as_uint(x); }
+    static __device__ __forceinline__ float value(U b) { return __uint_as_float(b); }
+};
+template <>
+struct CoopBits<double> {
+    using U = unsigned long long;
+    static __device__ __forceinline__ U bits(double x) { return (U)__double_as_longlong(x); }
+    static __device__ __forceinline__ double value(U b) { return __longlong_as_double((long long)b); }
+};
+
 // warps per CTA: fp32 one 512-thread CTA per SM (fewer barrier arrivals); fp64 (its
 // staged blocks are twice the size) two 256-thread CTAs per SM
 template <typename T>
@@ -499,30 +514,40 @@ __global__ void __launch_bounds__(CoopNW<T>::nw * 32, CoopNW<T>::minb)
     __shared__ int32_t qgid[COOP_NW * 32];
     __shared__ unsigned long long qmask[COOP_NW * 32], qemask[COOP_NW * 32];
     __shared__ int wcnt[COOP_NW], qn;
-    __shared__ unsigned long long cres[HJ_MAX_SUBDOMAINS];    // per-CTA max (fp64 bits >= 0)
-    __shared__ unsigned long long cwork[HJ_MAX_SUBDOMAINS];
+    // per-CTA max of the sweep's |V^{n+1} - V^n| as the bits of a T >= 0 (monotone as
+    // unsigned: native shared atomicMax, no CAS loop), evaluated-node count
+    __shared__ typename CoopBits<T>::U cres[HJ_MAX_SUBDOMAINS];
+    __shared__ unsigned cwork[HJ_MAX_SUBDOMAINS];
+    // the views, copied once: the grid barrier invalidates L1, so reading G every sweep
+    // would put a global round trip in front of every dependent load
+    __shared__ SweepView<T> sview[HJ_MAX_SUBDOMAINS];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (threadIdx.x < (unsigned)S.n_views) sview[threadIdx.x] = G->v[threadIdx.x];
     const bool mono = P.monotone != 0;
     const bool kruz = P.cost == HJ_COST_KRUZKOV;
     const T beta = P.beta, v_out = P.v_out;
     const int64_t gn0 = P.n[0], gn1 = P.n[1];
     unsigned stopped = 0;                          // bit v: view v met the rule
-    int64_t stop_at[HJ_MAX_SUBDOMAINS];
-    for (int v = 0; v < HJ_MAX_SUBDOMAINS; ++v) stop_at[v] = max_iter;
     const unsigned all = S.n_views >= 32 ? 0xffffffffu : ((1u << S.n_views) - 1u);
     int64_t n = 0;
     const bool tr = g_tb_trace.buf != nullptr && blockIdx.x == 0 && threadIdx.x == 0;
-    unsigned long long t_a = 0, t_b = 0, t_s = 0;
+    unsigned long long t_a = 0, t_b = 0, t_s = 0, t_l = 0, t_e = 0, t_m = 0, t_q = 0;
     int qitems = 0;
-    for (; n < max_iter && stopped != all; ++n) {
+    for (; n < max_iter; ++n) {
+        // the stopping rule on res[n-1], applied identically by every warp of every CTA:
+        // lane v reads view v's residual here, so that the round trip overlaps the
+        // scan's loads; the ballot below (before any evaluation) spreads the decisions
+        const bool chk = n > 0 && lane < S.n_views && !((stopped >> lane) & 1u);
+        const double rprev = chk ? *(volatile const double *)&sview[lane].res[n - 1] : 0.0;
+        bool decided = n == 0;
         if (tr) {
             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_a));
-            t_s = 0;
+            t_s = t_l = t_e = t_m = t_q = 0;
             qitems = 0;
         }
         if (threadIdx.x < HJ_MAX_SUBDOMAINS) {
-            cres[threadIdx.x] = 0ull;
-            cwork[threadIdx.x] = 0ull;
+            cres[threadIdx.x] = 0;
+            cwork[threadIdx.x] = 0u;
         }
         __syncthreads();
         unsigned long long *dcur = S.dmask[n & 1], *dnext = S.dmask[(n + 1) & 1];
@@ -563,62 +588,95 @@ __global__ void __launch_bounds__(CoopNW<T>::nw * 32, CoopNW<T>::minb)
             __syncthreads();
         }
         const int cnt = qn;
+        if (!decided) {
+            const unsigned now = __ballot_sync(0xffffffffu, chk && rprev < tol);
+            if (now) {
+                if (blockIdx.x == 0 && threadIdx.x == 0)
+                    for (unsigned m = now; m; m &= m - 1) S.stop[__ffs(m) - 1] = n;
+                stopped |= now;
+            }
+            decided = true;
+        }
+        if (stopped == all) continue;              // (every CTA: the same decision)
         if (tr && t_s == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_s));
         if (tr) qitems += cnt;
         // two mini-tiles per warp iteration: every global load of both (masks, the
         // 10 x 10 blocks of V^n, the speeds) is issued before any is used, and the mask
         // updates of both go out together
         for (int it = warp; it < cnt; it += 2 * COOP_NW) {
-            int64_t gid[2];
+            // 32-bit mini-tile arithmetic (ids are int32; a 2-D view's nodes < 2^31)
+            int gid[2];
             gid[0] = qgid[it];
-            gid[1] = it + COOP_NW < cnt ? (int64_t)qgid[it + COOP_NW] : (int64_t)-1;
-            int vv[2], mxy[2][3];
-            int64_t x0[2], y0[2];
-            unsigned long long dd[2], im[2], em[2];
+            gid[1] = it + COOP_NW < cnt ? qgid[it + COOP_NW] : -1;
+            int vv[2], mx[2], my[2], mz[2];
+            unsigned long long dd[2], em[2];
 #pragma unroll
             for (int s2 = 0; s2 < 2; ++s2) {
-                const int64_t g = gid[s2] < 0 ? gid[0] : gid[s2];
-                vv[s2] = coop_view(S, g);
-                const int64_t mt = g - S.mt_base[vv[s2]];
-                mxy[s2][0] = (int)(mt % S.mt0[vv[s2]]);
-                mxy[s2][1] = (int)((mt / S.mt0[vv[s2]]) % S.mt1[vv[s2]]);
-                mxy[s2][2] = (int)(mt / ((int64_t)S.mt0[vv[s2]] * S.mt1[vv[s2]]));
-                x0[s2] = (int64_t)mxy[s2][0] * 8;
-                y0[s2] = (int64_t)mxy[s2][1] * 8;
+                const int g = gid[s2] < 0 ? gid[0] : gid[s2];
+                const int v = coop_view(S, g);
+                const int mt = g - (int)S.mt_base[v], m0 = S.mt0[v];
+                vv[s2] = v;
+                if (EV == 3) {
+                    const int pl = m0 * S.mt1[v];
+                    mz[s2] = mt / pl;
+                    const int r = mt - mz[s2] * pl;
+                    my[s2] = r / m0;
+                    mx[s2] = r - my[s2] * m0;
+                } else {
+                    mz[s2] = 0;
+                    my[s2] = mt / m0;
+                    mx[s2] = mt - my[s2] * m0;
+                }
                 dd[s2] = gid[s2] >= 0 ? qmask[s2 ? it + COOP_NW : it] : 0ull;
-                im[s2] = ~0ull;                    // (dd already restricted to the classes)
                 em[s2] = gid[s2] >= 0 ? qemask[s2 ? it + COOP_NW : it] : 0ull;
             }
-            // staged V^n blocks and speeds, loads first
+            // staged V^n blocks and speeds, loads first.  A block inside its view (the
+            // common case) reads rows of V^n at a fixed stride: no bounds tests.
             constexpr int NLD = (BLK + 31) / 32;
             T ld[2][NLD], lsp[2][2];
 #pragma unroll
             for (int s2 = 0; s2 < 2; ++s2) {
-                const SweepView<T> &vw = G->v[vv[s2]];
-                const int64_t vn0 = vw.vn[0], vn1 = vw.vn[1], vn2 = vw.vn[2];
+                const SweepView<T> &vw = sview[vv[s2]];
+                const int vn0 = (int)vw.vn[0], vn1 = (int)vw.vn[1], vn2 = (int)vw.vn[2];
                 const T *__restrict__ Vi = vw.V[n & 1];
+                const int x0 = mx[s2] * 8, y0 = my[s2] * 8;
+                const bool inner = EV != 3 && x0 >= 1 && y0 >= 1 && x0 + 9 <= vn0 && y0 + 9 <= vn1;
+                if (inner) {
+                    const T *__restrict__ src = Vi + ((int64_t)(y0 - 1) * vn0 + (x0 - 1));
 #pragma unroll
-                for (int k = 0; k < NLD; ++k) {
-                    const int e = lane + 32 * k;
-                    const int ee = e % (BP * BP);
-                    const int64_t li = x0[s2] - 1 + ee % BP, lj = y0[s2] - 1 + ee / BP;
-                    int64_t lk = 0;
-                    if (EV == 3) {                   // heading plane z-1+e/100, periodic
-                        lk = mxy[s2][2] - 1 + e / (BP * BP);
-                        if (lk < 0) lk += vn2;
-                        if (lk >= vn2) lk -= vn2;
+                    for (int k = 0; k < NLD; ++k) {
+                        const int e = lane + 32 * k;
+                        ld[s2][k] = e < BLK ? src[(e / BP) * vn0 + e % BP] : v_out;
                     }
-                    ld[s2][k] = (e < BLK && li >= 0 && lj >= 0 && li < vn0 && lj < vn1)
-                                    ? Vi[li + vn0 * (lj + vn1 * lk)]
-                                    : v_out;
-                }
+                } else {
 #pragma unroll
-                for (int k = 0; k < 2; ++k) {
-                    const int e = lane + 32 * k;
-                    const int64_t li = x0[s2] + (e & 7), lj = y0[s2] + (e >> 3);
-                    lsp[s2][k] = (EV != 3 && P.speed && li < vn0 && lj < vn1)
-                                     ? P.speed[(li + vw.o[0]) + gn0 * (lj + vw.o[1])]
-                                     : T(1);
+                    for (int k = 0; k < NLD; ++k) {
+                        const int e = lane + 32 * k;
+                        const int ee = e % (BP * BP);
+                        const int li = x0 - 1 + ee % BP, lj = y0 - 1 + ee / BP;
+                        int lk = 0;
+                        if (EV == 3) {               // heading plane z-1+e/100, periodic
+                            lk = mz[s2] - 1 + e / (BP * BP);
+                            if (lk < 0) lk += vn2;
+                            if (lk >= vn2) lk -= vn2;
+                        }
+                        ld[s2][k] = (e < BLK && li >= 0 && lj >= 0 && li < vn0 && lj < vn1)
+                                        ? Vi[li + (int64_t)vn0 * (lj + (int64_t)vn1 * lk)]
+                                        : v_out;
+                    }
+                }
+                if (EV != 3 && P.speed) {
+                    const int o0 = (int)vw.o[0], o1 = (int)vw.o[1];
+                    const T *__restrict__ sp = P.speed + ((int64_t)(y0 + o1) * gn0 + (x0 + o0));
+#pragma unroll
+                    for (int k = 0; k < 2; ++k) {
+                        const int e = lane + 32 * k;
+                        const int li = x0 + (e & 7), lj = y0 + (e >> 3);
+                        lsp[s2][k] = (inner || (li < vn0 && lj < vn1)) ? sp[(e >> 3) * gn0 + (e & 7)]
+                                                                       : T(1);
+                    }
+                } else {
+                    lsp[s2][0] = lsp[s2][1] = T(1);
                 }
             }
 #pragma unroll
@@ -632,32 +690,36 @@ __global__ void __launch_bounds__(CoopNW<T>::nw * 32, CoopNW<T>::minb)
                 }
             }
             __syncwarp();
+            if (tr && t_l == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_l));
             unsigned long long cmv[2] = {0ull, 0ull};
 #pragma unroll 1
             for (int s2 = 0; s2 < 2; ++s2) {
-                const int v = vv[s2];
-                if (gid[s2] < 0 || ((stopped >> v) & 1u)) continue;
-                const SweepView<T> &vw = G->v[v];
+                // (selects, not indexing: a runtime index would put the arrays in local memory)
+                const int v = s2 ? vv[1] : vv[0];
+                if ((s2 ? gid[1] : gid[0]) < 0 || ((stopped >> v) & 1u)) continue;
+                const SweepView<T> &vw = sview[v];
+                const int64_t x0 = (int64_t)(s2 ? mx[1] : mx[0]) * 8;
+                const int64_t y0 = (int64_t)(s2 ? my[1] : my[0]) * 8;
+                const unsigned long long d_s = s2 ? dd[1] : dd[0], e_s = s2 ? em[1] : em[0];
                 T rmax;
                 unsigned long long cm;
                 int evald;
                 if constexpr (EV == 3) {
-                    const T th = fma((T)(mxy[s2][2] + vw.o[2]), P.dx[2], P.lo[2]);
+                    const int z = s2 ? mz[1] : mz[0];
+                    const T th = fma((T)(z + vw.o[2]), P.dx[2], P.lo[2]);
                     T sn, cn;
                     sincos_t(th, &sn, &cn);
-                    coop_eval_dubins<T>(P, vw, blk[warp][s2], lst[warp][s2], dd[s2] | em[s2],
-                                        x0[s2], y0[s2], mxy[s2][2], P.hdx[0] * (P.dub_v * cn),
+                    coop_eval_dubins<T>(P, vw, blk[warp][s2], lst[warp][s2], d_s | e_s,
+                                        x0, y0, z, P.hdx[0] * (P.dub_v * cn),
                                         P.hdx[1] * (P.dub_v * sn), vw.V[(n + 1) & 1], rmax, cm,
                                         evald);
                 } else if constexpr (EV == 0)
                     coop_eval<T, KQ, PC>(P, C, vw, blk[warp][s2], spd[warp][s2], lst[warp][s2],
-                                         dd[s2], em[s2], x0[s2], y0[s2],
-                                         vw.V[(n + 1) & 1], rmax, cm, evald);
+                                         d_s, e_s, x0, y0, vw.V[(n + 1) & 1], rmax, cm, evald);
                 else
                     coop_eval_field<T, EV - 1>(P, vw, vw.V[n & 1], blk[warp][s2], spd[warp][s2],
-                                               lst[warp][s2], dd[s2], em[s2],
-                                               x0[s2], y0[s2], vw.V[(n + 1) & 1], rmax, cm,
-                                               evald);
+                                               lst[warp][s2], d_s, e_s, x0, y0,
+                                               vw.V[(n + 1) & 1], rmax, cm, evald);
                 cm = ((unsigned long long)__reduce_or_sync(0xffffffffu, (unsigned)(cm >> 32)) << 32) |
                      (unsigned long long)__reduce_or_sync(0xffffffffu, (unsigned)cm);
 #pragma unroll
@@ -668,11 +730,12 @@ __global__ void __launch_bounds__(CoopNW<T>::nw * 32, CoopNW<T>::minb)
                 evald = __reduce_add_sync(0xffffffffu, evald);
                 if (lane == 0) {
                     if (rmax > T(0))
-                        atomicMax(&cres[v], (unsigned long long)__double_as_longlong((double)rmax));
-                    atomicAdd(&cwork[v], (unsigned long long)evald);
+                        atomicMax(&cres[v], CoopBits<T>::bits(rmax));
+                    atomicAdd(&cwork[v], (unsigned)evald);
                 }
-                cmv[s2] = cm;
+                if (s2) cmv[1] = cm; else cmv[0] = cm;
             }
+            if (tr && t_e == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_e));
             // sweep n+1: the 3 x 3 dilation of the changed nodes into the 9 mini-tiles
             // around each item (lanes 0-8: item 0, lanes 16-24: item 1)
             // (Dubins: the same in-plane dilation into planes z-1, z, z+1: 27 mini-tiles,
@@ -680,12 +743,12 @@ __global__ void __launch_bounds__(CoopNW<T>::nw * 32, CoopNW<T>::minb)
 #pragma unroll
             for (int rep = 0; rep < (EV == 3 ? 2 : 1); ++rep) {
                 const int s2 = lane >> 4, l9 = (lane & 15) + 16 * rep;
-                const unsigned long long cm = cmv[s2];
+                const unsigned long long cm = s2 ? cmv[1] : cmv[0];
                 if (cm && l9 < (EV == 3 ? 27 : 9)) {
-                    const int v = vv[s2];
+                    const int v = s2 ? vv[1] : vv[0];
                     const int dx = l9 % 3 - 1, dy = (l9 / 3) % 3 - 1, dz = l9 / 9 - 1;
-                    const int nx = mxy[s2][0] + dx, ny = mxy[s2][1] + dy;
-                    int nz = mxy[s2][2] + (EV == 3 ? dz : 0);
+                    const int nx = (s2 ? mx[1] : mx[0]) + dx, ny = (s2 ? my[1] : my[0]) + dy;
+                    int nz = (s2 ? mz[1] : mz[0]) + (EV == 3 ? dz : 0);
                     if (nz < 0) nz += S.mt2[v];
                     if (nz >= S.mt2[v]) nz -= S.mt2[v];
                     if (nx >= 0 && ny >= 0 && nx < S.mt0[v] && ny < S.mt1[v]) {
@@ -706,43 +769,54 @@ __global__ void __launch_bounds__(CoopNW<T>::nw * 32, CoopNW<T>::minb)
                 }
             }
             __syncwarp();
+            if (tr && t_m == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_m));
         }
         __syncthreads();                           // the queue is reused by the next chunk
+        if (tr && t_q == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_q));
         }
+        if (!decided) {                            // (no candidates in this CTA)
+            const unsigned now = __ballot_sync(0xffffffffu, chk && rprev < tol);
+            if (now) {
+                if (blockIdx.x == 0 && threadIdx.x == 0)
+                    for (unsigned m = now; m; m &= m - 1) S.stop[__ffs(m) - 1] = n;
+                stopped |= now;
+            }
+        }
+        if (stopped == all) break;
         // per-CTA residual / work of this sweep, one atomic per view
         __syncthreads();
         if (threadIdx.x < (unsigned)S.n_views) {
             const int v = threadIdx.x;
-            const double m = __longlong_as_double((long long)cres[v]);
+            const double m = (double)CoopBits<T>::value(cres[v]);
             const unsigned long long w = cwork[v];
-            if (m > 0.0) atomic_max_nonneg(&G->v[v].res[n], m);
-            if (w) atomicAdd(G->v[v].work, w);
+            if (m > 0.0) atomic_max_nonneg(&sview[v].res[n], m);
+            if (w) atomicAdd(sview[v].work, w);
         }
         if (S.use_list && blockIdx.x == 0 && threadIdx.x == 0) S.count[(n + 2) % 3] = 0;
         if (tr) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_b));
+        if (g_tb_trace.buf && threadIdx.x == 0 && n < g_tb_trace.cap && gridDim.x <= 256) {
+            unsigned long long t_arr;              // every CTA's arrival (load balance)
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_arr));
+            g_tb_trace.buf[8 * g_tb_trace.cap + 256 * n + blockIdx.x] = t_arr;
+        }
         grid.sync();
-        if (tr && 4 * n + 3 < 4 * g_tb_trace.cap) {
+        if (tr && n < g_tb_trace.cap) {
             unsigned long long t_c;
             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_c));
-            g_tb_trace.buf[4 * n] = t_a;
-            g_tb_trace.buf[4 * n + 1] = t_b;
-            g_tb_trace.buf[4 * n + 2] = t_c;
-            g_tb_trace.buf[4 * n + 3] = ((t_s - t_a) << 16) | (unsigned long long)qitems;
-        }
-        // the stopping rule, applied identically by every warp: lane v reads view v's
-        // residual (one round trip for all views), a ballot spreads the decisions
-        {
-            const bool met = lane < S.n_views && !((stopped >> lane) & 1u) &&
-                             *(volatile const double *)&G->v[lane].res[n] < tol;
-            const unsigned now = __ballot_sync(0xffffffffu, met);
-            if (now) {
-                for (unsigned m = now; m; m &= m - 1) stop_at[__ffs(m) - 1] = n + 1;
-                stopped |= now;
-            }
+            unsigned long long *o = g_tb_trace.buf + 8 * n;
+            o[0] = t_a;
+            o[1] = t_b;
+            o[2] = t_c;
+            o[3] = ((t_s - t_a) << 16) | (unsigned long long)qitems;
+            o[4] = t_l;
+            o[5] = t_e;
+            o[6] = t_m;
+            o[7] = t_q;
         }
     }
     if (blockIdx.x == 0 && threadIdx.x == 0)
-        for (int v = 0; v < S.n_views; ++v) S.stop[v] = stop_at[v];
+        for (int v = 0; v < S.n_views; ++v)
+            if (!((stopped >> v) & 1u)) S.stop[v] = max_iter;
 }
 
 }  // namespace hj

@@ -15,8 +15,8 @@ idx = int(sys.argv[1]) if len(sys.argv) > 1 else 2
 isa = len(sys.argv) > 2 and sys.argv[2] == "isa"
 cfg = W.make(idx)
 dp = hj.DeviceProblem(cfg.fine, "f32", sweep_kernel="local_coop")
-cap = 1 << 16
-buf = torch.zeros(4 * cap, dtype=torch.int64, device="cuda")
+cap = 1 << 12
+buf = torch.zeros((8 + 256) * cap, dtype=torch.int64, device="cuda")
 L = hj.lib()
 L.hj_debug_set_trace.argtypes = [ctypes.c_void_p, ctypes.c_longlong, ctypes.c_longlong]
 if isa:      # trace the partitioned fine solve of one ISA pass (the last cooperative launch)
@@ -36,16 +36,32 @@ else:
     V, rep = hj.hj_solve(dp)
     torch.cuda.synchronize()
     L.hj_debug_set_trace(None, 0, 0)
-t = buf.view(-1, 4).cpu().numpy()[: rep["iterations"]].astype(np.float64)
-raw = buf.view(-1, 4).cpu().numpy()[: rep["iterations"], 3]
+hb = buf.cpu().numpy()
+t = hb[: 8 * cap].reshape(-1, 8)[: rep["iterations"]].astype(np.float64)
+raw = hb[: 8 * cap].reshape(-1, 8)[: rep["iterations"], 3]
+arr = hb[8 * cap:].reshape(-1, 256)[: rep["iterations"]].astype(np.float64)
+ncta = int((arr[0] > 0).sum())
+arr = arr[:, :ncta]
+last = arr.max(axis=1)
+spread = (last - arr.min(axis=1)) / 1e3
+b0late = (last - arr[:, 0]) / 1e3
+bar = (t[:, 2] - last) / 1e3
 items = (raw & 0xffff).astype(np.float64)
 scan = (raw >> 16).astype(np.float64) / 1e3
 work = (t[:, 1] - t[:, 0]) / 1e3
 sync = (t[:, 2] - t[:, 1]) / 1e3
 gap = (t[1:, 0] - t[:-1, 2]) / 1e3
+ts = t[:, 0] + raw.astype(np.float64) // 65536
+has = t[:, 4] > 0
+ph = {"w0 load us": (t[:, 4] - ts), "w0 eval us": (t[:, 5] - t[:, 4]),
+      "w0 mark us": (t[:, 6] - t[:, 5]), "cta wait us": (t[:, 7] - t[:, 6]),
+      "reduce us": (t[:, 1] - t[:, 7])}
+ph = {k: v[has] / 1e3 for k, v in ph.items()}
 print(f"sweeps {len(t)}  total {(t[-1, 2] - t[0, 0]) / 1e6:.2f} ms  device {rep['device_ms']:.2f} ms")
 for name, x in (("block0 items", items), ("block0 scan us", scan), ("block0 work us", work),
-                ("sync us", sync), ("post-sync us", gap)):
+                ("sync us", sync), ("post-sync us", gap),
+                ("arrival spread us", spread), ("last - block0 us", b0late),
+                ("barrier after last us", bar), *ph.items()):
     print(f"{name:15s} mean {x.mean():8.2f}  med {np.median(x):8.2f}  max {x.max():8.2f}")
 for k in (0, 100, 300, 500, 700):
     if k < len(t):
