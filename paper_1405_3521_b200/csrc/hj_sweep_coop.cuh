@@ -470,6 +470,24 @@ __device__ __forceinline__ void coop_eval_dubins(const DevProblem<T, T> &P, cons
     evald_out = evald;
 }
 
+// Grid-wide barrier of the resident (cooperative) grid on a monotone arrival counter
+// (zeroed before the launch): thread 0 of each CTA publishes the CTA's writes (fence),
+// adds its arrival without waiting for a reply, and polls until all gridDim.x arrivals
+// of barrier n+1 are in.  One round trip less than a generation-flip barrier whose
+// arrival atomic returns.  The acquire load invalidates the SM's L1, so the CTA's reads
+// after the barrier see the other CTAs' writes.
+__device__ __forceinline__ void coop_grid_barrier(unsigned *ctr, unsigned target) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(ctr) : "memory");
+        unsigned v;
+        do {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+        } while ((int)(v - target) < 0);
+    }
+    __syncthreads();
+}
+
 template <typename T>
 struct CoopBits;
 template <>
@@ -500,8 +518,6 @@ __global__ void __launch_bounds__(CoopNW<T>::nw * 32, CoopNW<T>::minb)
     k_sweep_local2d_coop(const DevProblem<T, T> P, const LocalCtrl<T> C,
                          const SweepGroup<T> *__restrict__ G, const CoopState S,
                          int64_t max_iter, double tol) {
-    namespace cg = cooperative_groups;
-    cg::grid_group grid = cg::this_grid();
     constexpr int COOP_NW = CoopNW<T>::nw;
     constexpr int BP = 10;                         // staged block pitch
     constexpr int BLK = EV == 3 ? 3 * BP * BP : BP * BP;   // Dubins: planes z-1, z, z+1
@@ -513,7 +529,7 @@ __global__ void __launch_bounds__(CoopNW<T>::nw * 32, CoopNW<T>::minb)
     __shared__ int8_t lst[COOP_NW][2][64];
     __shared__ int32_t qgid[COOP_NW * 32];
     __shared__ unsigned long long qmask[COOP_NW * 32], qemask[COOP_NW * 32];
-    __shared__ int wcnt[COOP_NW], qn;
+    __shared__ int wcnt[COOP_NW];
     // per-CTA max of the sweep's |V^{n+1} - V^n| as the bits of a T >= 0 (monotone as
     // unsigned: native shared atomicMax, no CAS loop), evaluated-node count
     __shared__ typename CoopBits<T>::U cres[HJ_MAX_SUBDOMAINS];
@@ -560,6 +576,7 @@ __global__ void __launch_bounds__(CoopNW<T>::nw * 32, CoopNW<T>::minb)
         const int32_t *litems = S.items[n & 1];
         const int64_t per_cta = ncand > blockIdx.x ? (ncand - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
         for (int64_t ch = 0; ch < per_cta; ch += COOP_NW * 32) {
+        int chunk_n;
         {
             const int64_t k = ch + threadIdx.x;
             const int64_t idx = blockIdx.x + k * (int64_t)gridDim.x;
@@ -571,8 +588,10 @@ __global__ void __launch_bounds__(CoopNW<T>::nw * 32, CoopNW<T>::minb)
             const unsigned bal = __ballot_sync(0xffffffffu, m != 0ull);
             if (lane == 0) wcnt[warp] = __popc(bal);
             __syncthreads();
-            int base_i = 0;
-            for (int w = 0; w < warp; ++w) base_i += wcnt[w];
+            // this warp's offset and the chunk's total: one shared load + two warp
+            // reductions (lane w holds warp w's count)
+            const int wc = lane < COOP_NW ? wcnt[lane] : 0;
+            const int base_i = __reduce_add_sync(0xffffffffu, lane < warp ? wc : 0);
             if (m) {
                 const int pos = base_i + __popc(bal & ((1u << lane) - 1u));
                 qgid[pos] = (int32_t)g;
@@ -580,14 +599,10 @@ __global__ void __launch_bounds__(CoopNW<T>::nw * 32, CoopNW<T>::minb)
                 qemask[pos] = m & cem;
                 dcur[g] = 0ull;                    // consumed
             }
-            if (threadIdx.x == 0) {
-                int t = 0;
-                for (int w = 0; w < COOP_NW; ++w) t += wcnt[w];
-                qn = t;
-            }
-            __syncthreads();
+            chunk_n = __reduce_add_sync(0xffffffffu, wc);
+            __syncthreads();                       // the queue is complete
         }
-        const int cnt = qn;
+        const int cnt = chunk_n;
         if (!decided) {
             const unsigned now = __ballot_sync(0xffffffffu, chk && rprev < tol);
             if (now) {
@@ -799,7 +814,8 @@ __global__ void __launch_bounds__(CoopNW<T>::nw * 32, CoopNW<T>::minb)
             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_arr));
             g_tb_trace.buf[8 * g_tb_trace.cap + 256 * n + blockIdx.x] = t_arr;
         }
-        grid.sync();
+        coop_grid_barrier(reinterpret_cast<unsigned *>(S.count + 3),
+                          (unsigned)(n + 1) * gridDim.x);
         if (tr && n < g_tb_trace.cap) {
             unsigned long long t_c;
             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_c));
