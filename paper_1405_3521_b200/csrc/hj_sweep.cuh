@@ -1221,12 +1221,74 @@ hj_status sweep_launch_rerun(const DevProblem<T, T> &P, const SweepLaunch<T> &L,
 
 // The whole iteration of the local class in one cooperative launch (hj_sweep_coop.cuh).
 // stop[v] (host, out) = iterations performed by view v.
+// Cluster mode (views solved by one thread-block cluster each): the cluster size and
+// how many such clusters are resident at once, or {0, 0} if no cluster of 8+ fits.
+template <typename T, int KQ, bool PC, int EV>
+static void coop_cluster_shape(size_t dyn, int &cs, int &maxc) {
+    static int c_cs = -1, c_maxc = 0;
+    if (c_cs < 0) {
+        auto kern = k_sweep_local2d_coop<T, KQ, PC, EV, true>;
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+        cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        c_cs = 0;
+        for (int want : {16, 8}) {
+            cudaLaunchConfig_t cfg = {};
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeClusterDimension;
+            at[0].val.clusterDim.x = want;
+            at[0].val.clusterDim.y = 1;
+            at[0].val.clusterDim.z = 1;
+            cfg.gridDim = dim3(want);
+            cfg.blockDim = dim3(CoopNW<T>::nw * 32);
+            cfg.dynamicSmemBytes = dyn;
+            cfg.attrs = at;
+            cfg.numAttrs = 1;
+            int m = 0;
+            if (cudaOccupancyMaxActiveClusters(&m, (void *)kern, &cfg) == cudaSuccess && m >= 1) {
+                c_cs = want;
+                c_maxc = m;
+                break;
+            }
+            cudaGetLastError();
+        }
+    }
+    cs = c_cs;
+    maxc = c_maxc;
+}
+
 template <typename T, int KQ, bool PC, int EV = 0>
 static hj_status launch_coop_kq(const DevProblem<T, T> &P, const SweepLaunch<T> &L,
                                 const CoopState &S, int64_t max_iter, double tol,
                                 cudaStream_t s) {
     constexpr int BLK = EV == 3 ? 300 : 100;
     const size_t dyn = (size_t)CoopNW<T>::nw * 2 * BLK * sizeof(T);
+    if (S.cluster) {        // one cluster per view (at most maxc resident at a time)
+        int cs = 0, maxc = 0;
+        coop_cluster_shape<T, KQ, PC, EV>(dyn, cs, maxc);
+        if (cs > 0) {
+            auto kern = k_sweep_local2d_coop<T, KQ, PC, EV, true>;
+            const int ncl = std::max(1, std::min(S.n_views, maxc));
+            cudaLaunchConfig_t cfg = {};
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeClusterDimension;
+            at[0].val.clusterDim.x = cs;
+            at[0].val.clusterDim.y = 1;
+            at[0].val.clusterDim.z = 1;
+            cfg.gridDim = dim3(ncl * cs);
+            cfg.blockDim = dim3(CoopNW<T>::nw * 32);
+            cfg.dynamicSmemBytes = dyn;
+            cfg.stream = s;
+            cfg.attrs = at;
+            cfg.numAttrs = 1;
+            const SweepGroup<T> *g = L.d_group;
+            cudaError_t e = cudaLaunchKernelEx(&cfg, kern, P, L.ctrl, g, S, max_iter, tol);
+            if (e != cudaSuccess) {
+                set_error("cluster sweep launch failed: %s", cudaGetErrorString(e));
+                return HJ_ERR_CUDA;
+            }
+            return HJ_OK;
+        }
+    }
     static int grid = 0;
     if (!grid) {
         cudaFuncSetAttribute(k_sweep_local2d_coop<T, KQ, PC, EV>,
@@ -1273,6 +1335,20 @@ hj_status sweep_coop(const DevProblem<T, T> &P, const SweepLaunch<T> &L, int64_t
     // beyond, keep a list of the mini-tiles with a nonzero mask
     S.use_list = tot > (int64_t)148 * 512 * 2 ? 1 : 0;
     if (const char *e = getenv("HJ_COOP_LIST")) S.use_list = atoi(e) != 0;   // tests / tuning
+    // cluster mode: several independent views (a partitioned solve), or a grid small
+    // enough that a cluster's SMs cover it — there the per-sweep grid barrier and the
+    // spread of 148 CTAs' arrival times cost more than the work
+    S.cluster = (nv >= 2 || tot <= 4096) ? 1 : 0;
+    if (const char *e = getenv("HJ_COOP_CLUSTER")) S.cluster = atoi(e) != 0;
+    if (S.cluster) S.use_list = 0;    // (the list ring is shared by all views)
+    {
+        std::vector<int> ord(nv);
+        for (int v = 0; v < nv; ++v) ord[v] = v;
+        std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) {
+            return S.mt_base[a + 1] - S.mt_base[a] > S.mt_base[b + 1] - S.mt_base[b];
+        });
+        for (int v = 0; v < nv; ++v) S.vorder[v] = ord[v];
+    }
     Carver c(L.wl_mem, (size_t)1 << 62);
     S.imask = (unsigned long long *)c.take(8 * tot);
     S.emask = (unsigned long long *)c.take(8 * tot);

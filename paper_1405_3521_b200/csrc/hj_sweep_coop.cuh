@@ -43,6 +43,8 @@ struct CoopState {
     int dubins;                     // 3-D Dubins views: 8 x 8 mini-tiles per heading plane
     int n_views;
     int64_t total;
+    int32_t vorder[HJ_MAX_SUBDOMAINS];   // cluster mode: views by decreasing size
+    int cluster;                    // 1: cluster mode (k_sweep_local2d_coop<..., CL>)
 };
 
 __device__ __forceinline__ int coop_view(const CoopState &S, int64_t gid) {
@@ -108,6 +110,7 @@ template <typename T, int KQ, bool PC>
 __device__ __forceinline__ void coop_eval(const DevProblem<T, T> &P, const LocalCtrl<T> &C,
                                           const SweepView<T> &vw, const T *__restrict__ b,
                                           const T *__restrict__ spd, int8_t *lstw,
+                                          const T *__restrict__ sctl,
                                           unsigned long long di, unsigned long long de,
                                           int64_t x0, int64_t y0, T *__restrict__ Vo,
                                           T &rmax_out, unsigned long long &cm_out,
@@ -126,6 +129,8 @@ __device__ __forceinline__ void coop_eval(const DevProblem<T, T> &P, const Local
     if ((dlo >> lane) & 1u) lstw[__popc(dlo & lt)] = (int8_t)lane;
     if ((dhi >> lane) & 1u) lstw[plo + __popc(dhi & lt)] = (int8_t)(32 + lane);
     __syncwarp();
+    const bool dbg = g_tb_trace.buf && blockIdx.x == 0 && threadIdx.x == 0;
+    const long long dc0 = dbg ? clock64() : 0;
             T rmax = T(0);
     unsigned long long cm = 0;             // changed nodes (bit = local index)
     int evald = 0;
@@ -191,18 +196,20 @@ __device__ __forceinline__ void coop_eval(const DevProblem<T, T> &P, const Local
         }
     }
     }
-    // box-edge nodes (R3): 4 at a time, 8 lanes per node (2 per quadrant)
+    const long long dc1 = dbg ? clock64() : 0;
+    // box-edge nodes (R3): 8 at a time, 4 lanes per node (one per quadrant, all its
+    // controls)
     const int nE = __popcll(de);
     if (nE > 0) {
-    const int sg = lane >> 3, sl = lane & 7;
-    unsigned long long rest = de;
-    for (int e0 = 0; e0 < nE; e0 += 4) {
-        // the sg-th remaining set bit
-        unsigned long long mm = rest;
-        for (int s = 0; s < sg && mm; ++s) mm &= mm - 1;
-        const bool ok = mm != 0ull;
-        const int loc = ok ? __ffsll((long long)mm) - 1 : 0;
-        for (int s = 0; s < 4 && rest; ++s) rest &= rest - 1;
+    const int sg = lane >> 2, qd = lane & 3;
+    const unsigned elo = (unsigned)de, ehi = (unsigned)(de >> 32);
+    const int pel = __popc(elo);
+    for (int e0 = 0; e0 < nE; e0 += 8) {
+        // this group's node: the (e0 + sg)-th set bit of de
+        const int gi = e0 + sg;
+        const bool ok = gi < nE;
+        const int loc = !ok ? 0 : gi < pel ? (int)__fns(elo, 0, gi + 1)
+                                           : 32 + (int)__fns(ehi, 0, gi - pel + 1);
         const int r = loc >> 3, c = loc & 7;
         const T *sp = b + (r + 1) * BP + (c + 1);
         const int64_t g0 = x0 + c + vw.o[0], g1 = y0 + r + vw.o[1];
@@ -218,22 +225,22 @@ __device__ __forceinline__ void coop_eval(const DevProblem<T, T> &P, const Local
         const bool lx = g0 == 0, hx = g0 == gn0 - 1, ly = g1 == 0, hy = g1 == gn1 - 1;
         T e_best = (T)INFINITY;
         {
-            const int qd = sl >> 1;
             const T Vx = (qd & 1) ? sp[-1] : sp[1];
             const T Vy = (qd & 2) ? sp[-BP] : sp[BP];
-            const T Vxy = (qd == 0)   ? sp[BP + 1]
-                          : (qd == 1) ? sp[BP - 1]
-                          : (qd == 2) ? sp[-BP + 1]
-                                      : sp[-BP - 1];
+            const T Vxy = sp[((qd & 2) ? -BP : BP) + ((qd & 1) ? -1 : 1)];
             const bool ex = (qd & 1) ? lx : hx, ey = (qd & 2) ? ly : hy;
             const T Dx = beta * (Vx - eV00), Dy = beta * (Vy - eV00);
             const T Dxy = beta * ((Vxy - Vx) - (Vy - eV00));
             const T c_out = fma(beta, v_out, base);
             const T eps = (T)BOX_EPS;
-#pragma unroll 4
-            for (int k = sl & 1; k < KQ; k += 2) {
-                T wx = e_sc * C.ax[qd][k], wy = e_sc * C.ay[qd][k];
-                const T ck = PC ? C.ck[qd][k] : T(0);
+            // (the control tables from shared memory: qd differs across the lanes, a
+            // lane-divergent constant-bank read would serialise)
+            const T *__restrict__ tax = sctl + qd * KQ, *__restrict__ tay = sctl + (4 + qd) * KQ;
+            const T *__restrict__ tck = sctl + (8 + qd) * KQ;
+#pragma unroll 8
+            for (int k = 0; k < KQ; ++k) {
+                T wx = e_sc * tax[k], wy = e_sc * tay[k];
+                const T ck = PC ? tck[k] : T(0);
                 const bool out = (ex && wx > eps) || (ey && wy > eps);
                 if (ex) wx = T(0);
                 if (ey) wy = T(0);
@@ -241,10 +248,9 @@ __device__ __forceinline__ void coop_eval(const DevProblem<T, T> &P, const Local
                 e_best = fmin(e_best, out ? c_out + ck : in);
             }
         }
-#pragma unroll
-        for (int o = 4; o > 0; o >>= 1)
-            e_best = fmin(e_best, __shfl_xor_sync(0xffffffffu, e_best, o));
-        if (ok && sl == 0) {
+        e_best = fmin(e_best, __shfl_xor_sync(0xffffffffu, e_best, 1));
+        e_best = fmin(e_best, __shfl_xor_sync(0xffffffffu, e_best, 2));
+        if (ok && qd == 0) {
             const T vnew = mono ? fmin(e_best, eV00) : e_best;
             Vo[(x0 + c) + vn0 * (y0 + r)] = vnew;
             ++evald;
@@ -255,6 +261,15 @@ __device__ __forceinline__ void coop_eval(const DevProblem<T, T> &P, const Local
             }
         }
     }
+    }
+    if (dbg) {
+        const long long dc2 = clock64();
+        unsigned long long *acc = g_tb_trace.buf + (8 + 256) * g_tb_trace.cap;
+        acc[0] += dc1 - dc0;
+        acc[1] += dc2 - dc1;
+        acc[2] += 1;
+        acc[3] += nI;
+        acc[4] += __popcll(de);
     }
     rmax_out = rmax;
     cm_out = cm;
@@ -513,7 +528,11 @@ struct CoopNW {
 
 // EV: 0 = local class (LocalCtrl, FFMA2 quadrants), HJ_DYN_AFFINE + 1 / HJ_DYN_VANDERPOL + 1
 // = field class with feet within one cell, 3 = Dubins (3-D, heading planes)
-template <typename T, int KQ, bool PC, int EV = 0>
+// CL: cluster mode — each thread-block cluster solves whole views on its own (views
+// are independent problems until the gather): view vorder[c], vorder[c + #clusters], ...
+// for cluster c, with the hardware cluster barrier between sweeps instead of the
+// grid-wide one.
+template <typename T, int KQ, bool PC, int EV = 0, bool CL = false>
 __global__ void __launch_bounds__(CoopNW<T>::nw * 32, CoopNW<T>::minb)
     k_sweep_local2d_coop(const DevProblem<T, T> P, const LocalCtrl<T> C,
                          const SweepGroup<T> *__restrict__ G, const CoopState S,
@@ -537,18 +556,36 @@ __global__ void __launch_bounds__(CoopNW<T>::nw * 32, CoopNW<T>::minb)
     // the views, copied once: the grid barrier invalidates L1, so reading G every sweep
     // would put a global round trip in front of every dependent load
     __shared__ SweepView<T> sview[HJ_MAX_SUBDOMAINS];
+    // local class: the quadrant control tables ax | ay | ck, [3][4][KQ]
+    __shared__ T sctl[EV == 0 ? 12 * KQ : 1];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if (threadIdx.x < (unsigned)S.n_views) sview[threadIdx.x] = G->v[threadIdx.x];
+    if (EV == 0 && threadIdx.x < 12u * KQ) {
+        const int w = threadIdx.x / (4 * KQ), q = (threadIdx.x / KQ) % 4, k = threadIdx.x % KQ;
+        sctl[threadIdx.x] = w == 0 ? C.ax[q][k] : w == 1 ? C.ay[q][k] : C.ck[q][k];
+    }
     const bool mono = P.monotone != 0;
     const bool kruz = P.cost == HJ_COST_KRUZKOV;
     const T beta = P.beta, v_out = P.v_out;
     const int64_t gn0 = P.n[0], gn1 = P.n[1];
-    unsigned stopped = 0;                          // bit v: view v met the rule
     const unsigned all = S.n_views >= 32 ? 0xffffffffu : ((1u << S.n_views) - 1u);
-    int64_t n = 0;
+    // the CTA group that sweeps together: the whole grid, or (CL) this CTA's cluster
+    unsigned grank = blockIdx.x, gsize = gridDim.x, grp = 0, ngrp = 1;
+    if constexpr (CL) {
+        asm("mov.u32 %0, %%cluster_ctarank;" : "=r"(grank));
+        asm("mov.u32 %0, %%cluster_nctarank;" : "=r"(gsize));
+        asm("mov.u32 %0, %%clusterid.x;" : "=r"(grp));
+        asm("mov.u32 %0, %%nclusterid.x;" : "=r"(ngrp));
+    }
     const bool tr = g_tb_trace.buf != nullptr && blockIdx.x == 0 && threadIdx.x == 0;
     unsigned long long t_a = 0, t_b = 0, t_s = 0, t_l = 0, t_e = 0, t_m = 0, t_q = 0;
     int qitems = 0;
+    for (int vs = (int)grp; vs < (CL ? S.n_views : 1); vs += (int)ngrp) {
+    const int vsel = CL ? S.vorder[vs] : -1;
+    unsigned stopped = CL ? (all & ~(1u << vsel)) : 0u;   // bit v: view v met the rule
+    const int64_t cbase = CL ? S.mt_base[vsel] : 0;
+    const int64_t ctot = CL ? S.mt_base[vsel + 1] - cbase : S.total;
+    int64_t n = 0;
     for (; n < max_iter; ++n) {
         // the stopping rule on res[n-1], applied identically by every warp of every CTA:
         // lane v reads view v's residual here, so that the round trip overlaps the
@@ -572,15 +609,15 @@ __global__ void __launch_bounds__(CoopNW<T>::nw * 32, CoopNW<T>::minb)
         // ones in shared memory, then the warps take two per iteration.
         // (list mode: the candidates are the listed mini-tiles of this sweep instead)
         const int64_t ncand =
-            S.use_list ? (int64_t)*(volatile const int32_t *)&S.count[n % 3] : S.total;
+            S.use_list ? (int64_t)*(volatile const int32_t *)&S.count[n % 3] : ctot;
         const int32_t *litems = S.items[n & 1];
-        const int64_t per_cta = ncand > blockIdx.x ? (ncand - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+        const int64_t per_cta = ncand > grank ? (ncand - grank + gsize - 1) / gsize : 0;
         for (int64_t ch = 0; ch < per_cta; ch += COOP_NW * 32) {
         int chunk_n;
         {
             const int64_t k = ch + threadIdx.x;
-            const int64_t idx = blockIdx.x + k * (int64_t)gridDim.x;
-            const int64_t g = k < per_cta ? (S.use_list ? (int64_t)litems[idx] : idx) : 0;
+            const int64_t idx = grank + k * (int64_t)gsize;
+            const int64_t g = k < per_cta ? (S.use_list ? (int64_t)litems[idx] : cbase + idx) : 0;
             const unsigned long long m = k < per_cta ? dcur[g] : 0ull;
             // the class masks ride along with the dirty mask (one round trip for all three)
             const unsigned long long cim = k < per_cta ? S.imask[g] : 0ull;
@@ -606,7 +643,7 @@ __global__ void __launch_bounds__(CoopNW<T>::nw * 32, CoopNW<T>::minb)
         if (!decided) {
             const unsigned now = __ballot_sync(0xffffffffu, chk && rprev < tol);
             if (now) {
-                if (blockIdx.x == 0 && threadIdx.x == 0)
+                if (grank == 0 && threadIdx.x == 0)
                     for (unsigned m = now; m; m &= m - 1) S.stop[__ffs(m) - 1] = n;
                 stopped |= now;
             }
@@ -730,7 +767,8 @@ __global__ void __launch_bounds__(CoopNW<T>::nw * 32, CoopNW<T>::minb)
                                         evald);
                 } else if constexpr (EV == 0)
                     coop_eval<T, KQ, PC>(P, C, vw, blk[warp][s2], spd[warp][s2], lst[warp][s2],
-                                         d_s, e_s, x0, y0, vw.V[(n + 1) & 1], rmax, cm, evald);
+                                         sctl, d_s, e_s, x0, y0, vw.V[(n + 1) & 1], rmax, cm,
+                                         evald);
                 else
                     coop_eval_field<T, EV - 1>(P, vw, vw.V[n & 1], blk[warp][s2], spd[warp][s2],
                                                lst[warp][s2], d_s, e_s, x0, y0,
@@ -792,7 +830,7 @@ __global__ void __launch_bounds__(CoopNW<T>::nw * 32, CoopNW<T>::minb)
         if (!decided) {                            // (no candidates in this CTA)
             const unsigned now = __ballot_sync(0xffffffffu, chk && rprev < tol);
             if (now) {
-                if (blockIdx.x == 0 && threadIdx.x == 0)
+                if (grank == 0 && threadIdx.x == 0)
                     for (unsigned m = now; m; m &= m - 1) S.stop[__ffs(m) - 1] = n;
                 stopped |= now;
             }
@@ -814,8 +852,14 @@ __global__ void __launch_bounds__(CoopNW<T>::nw * 32, CoopNW<T>::minb)
             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_arr));
             g_tb_trace.buf[8 * g_tb_trace.cap + 256 * n + blockIdx.x] = t_arr;
         }
-        coop_grid_barrier(reinterpret_cast<unsigned *>(S.count + 3),
-                          (unsigned)(n + 1) * gridDim.x);
+        if constexpr (CL) {
+            // (acquire: the SM's L1 is invalidated, the cluster's writes are visible)
+            asm volatile("barrier.cluster.arrive.release.aligned;\n\t"
+                         "barrier.cluster.wait.acquire.aligned;" ::: "memory");
+        } else {
+            coop_grid_barrier(reinterpret_cast<unsigned *>(S.count + 3),
+                              (unsigned)(n + 1) * gridDim.x);
+        }
         if (tr && n < g_tb_trace.cap) {
             unsigned long long t_c;
             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_c));
@@ -830,9 +874,10 @@ __global__ void __launch_bounds__(CoopNW<T>::nw * 32, CoopNW<T>::minb)
             o[7] = t_q;
         }
     }
-    if (blockIdx.x == 0 && threadIdx.x == 0)
+    if (grank == 0 && threadIdx.x == 0)
         for (int v = 0; v < S.n_views; ++v)
             if (!((stopped >> v) & 1u)) S.stop[v] = max_iter;
+    }
 }
 
 }  // namespace hj

@@ -13,10 +13,11 @@ from paper_1405_3521_b200 import hj  # noqa: E402
 
 idx = int(sys.argv[1]) if len(sys.argv) > 1 else 2
 isa = len(sys.argv) > 2 and sys.argv[2] == "isa"
+coarse = len(sys.argv) > 2 and sys.argv[2] == "coarse"
 cfg = W.make(idx)
-dp = hj.DeviceProblem(cfg.fine, "f32", sweep_kernel="local_coop")
+dp = hj.DeviceProblem(cfg.coarse if coarse else cfg.fine, "f32", sweep_kernel="local_coop")
 cap = 1 << 12
-buf = torch.zeros((8 + 256) * cap, dtype=torch.int64, device="cuda")
+buf = torch.zeros((8 + 256) * cap + 16, dtype=torch.int64, device="cuda")
 L = hj.lib()
 L.hj_debug_set_trace.argtypes = [ctypes.c_void_p, ctypes.c_longlong, ctypes.c_longlong]
 if isa:      # trace the partitioned fine solve of one ISA pass (the last cooperative launch)
@@ -39,7 +40,10 @@ else:
 hb = buf.cpu().numpy()
 t = hb[: 8 * cap].reshape(-1, 8)[: rep["iterations"]].astype(np.float64)
 raw = hb[: 8 * cap].reshape(-1, 8)[: rep["iterations"], 3]
-arr = hb[8 * cap:].reshape(-1, 256)[: rep["iterations"]].astype(np.float64)
+acc = hb[(8 + 256) * cap:]
+if acc[2]:
+    print(f"coop_eval (block 0 warp 0): calls {acc[2]}  interior {acc[0] / acc[2]:.0f} cyc  edge {acc[1] / acc[2]:.0f} cyc  nI {acc[3] / acc[2]:.1f}  nE {acc[4] / acc[2]:.2f}")
+arr = hb[8 * cap:(8 + 256) * cap].reshape(-1, 256)[: rep["iterations"]].astype(np.float64)
 ncta = int((arr[0] > 0).sum())
 arr = arr[:, :ncta]
 last = arr.max(axis=1)
@@ -66,3 +70,11 @@ for name, x in (("block0 items", items), ("block0 scan us", scan), ("block0 work
 for k in (0, 100, 300, 500, 700):
     if k < len(t):
         print(f"  sweep {k}: items {int(items[k])} work {work[k]:.1f} us sync {sync[k]:.1f} us")
+# which CTAs arrive last: per-CTA mean lateness (arrival - mean arrival of the sweep)
+late = (arr - arr.mean(axis=1, keepdims=True)) / 1e3
+ml = late.mean(axis=0)
+order = np.argsort(ml)
+print("CTA lateness us: earliest", [(int(i), round(float(ml[i]), 2)) for i in order[:4]],
+      "latest", [(int(i), round(float(ml[i]), 2)) for i in order[-4:]],
+      "std of per-CTA means", round(float(ml.std()), 2), "mean per-sweep std",
+      round(float(late.std(axis=1).mean()), 2))
