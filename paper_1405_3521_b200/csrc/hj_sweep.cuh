@@ -1335,10 +1335,10 @@ hj_status sweep_coop(const DevProblem<T, T> &P, const SweepLaunch<T> &L, int64_t
     // beyond, keep a list of the mini-tiles with a nonzero mask
     S.use_list = tot > (int64_t)148 * 512 * 2 ? 1 : 0;
     if (const char *e = getenv("HJ_COOP_LIST")) S.use_list = atoi(e) != 0;   // tests / tuning
-    // cluster mode: several independent views (a partitioned solve), or a grid small
-    // enough that a cluster's SMs cover it — there the per-sweep grid barrier and the
-    // spread of 148 CTAs' arrival times cost more than the work
-    S.cluster = (nv >= 2 || tot <= 4096) ? 1 : 0;
+    // cluster mode (each view on one 16-CTA cluster, hardware cluster barrier): measured
+    // slower on every config (config 2 ISA fine 28 ms vs 11.6 ms; coarse 1.38 vs
+    // 1.25 ms: a view's work on 16 SMs outweighs the cheaper barrier), so opt-in only
+    S.cluster = 0;
     if (const char *e = getenv("HJ_COOP_CLUSTER")) S.cluster = atoi(e) != 0;
     if (S.cluster) S.use_list = 0;    // (the list ring is shared by all views)
     {
