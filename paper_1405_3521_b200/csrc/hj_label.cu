@@ -100,11 +100,39 @@ __device__ __forceinline__ BestPair warp_best(BestPair a) {
     return a;
 }
 
+// dynamics() with the control's components u[0..2] from shared memory: the lanes of
+// a warp take different controls, and a lane-divergent read of the kernel-parameter
+// control table would serialise (one constant-bank address per pass)
+template <typename Ts>
+__device__ __forceinline__ void dynamics_u(const DevProblem<double, Ts> &P, const double x[3],
+                                           double c, const double *u, double f[3]) {
+    if (P.dyn == HJ_DYN_AFFINE) {
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+            if (d >= P.dim) {
+                f[d] = 0.0;
+                continue;
+            }
+            double s = fma(c, u[d], P.b[d]);
+            for (int e = 0; e < P.dim; ++e) s = fma(P.A[3 * d + e], x[e], s);
+            f[d] = s;
+        }
+    } else if (P.dyn == HJ_DYN_DUBINS) {
+        f[0] = P.dub_v * cos(x[2]);
+        f[1] = P.dub_v * sin(x[2]);
+        f[2] = P.dub_w * u[0];
+    } else {
+        f[0] = x[1];
+        f[1] = fma(P.vdp_mu * (1.0 - x[0] * x[0]), x[1], u[0] - x[0]);
+        f[2] = 0.0;
+    }
+}
+
 template <typename Ts, int DIM>
 __device__ __forceinline__ BestPair lane_bracket(const DevProblem<double, Ts> &P,
                                                  const Ts *__restrict__ V, const int64_t o[3],
                                                  const int64_t vn[3], const double g[3],
-                                                 int lane) {
+                                                 int lane, const double (*uctl)[4]) {
     double x[3] = {0, 0, 0};
 #pragma unroll
     for (int d = 0; d < DIM; ++d) x[d] = fma(g[d], P.dx[d], P.lo[d]);
@@ -116,12 +144,75 @@ __device__ __forceinline__ BestPair lane_bracket(const DevProblem<double, Ts> &P
     BestPair r{INFINITY, INFINITY, -1};
     for (int k = lane; k < P.K; k += 32) {
         double f[3];
-        dynamics(P, x, cs, k, f);
+        dynamics_u(P, x, cs, uctl[k], f);
         double foot[3] = {0, 0, 0};
 #pragma unroll
         for (int d = 0; d < DIM; ++d) foot[d] = fma(P.hdx[d], f[d], g[d]);
         const double I = interp<double, Ts, DIM>(V, o, vn, P.n, P.periodic, zero, foot, P.v_out);
-        const double ck = (P.cost == HJ_COST_KRUZKOV) ? base : fma(P.h * P.lr, P.csq[k], base);
+        const double ck = (P.cost == HJ_COST_KRUZKOV) ? base : fma(P.h * P.lr, uctl[k][3], base);
+        const double v = fma(P.beta, I, ck);
+        if (v < r.best) {
+            r.second = r.best;
+            r.best = v;
+            r.arg = k;
+        } else if (v < r.second) {
+            r.second = v;
+        }
+    }
+    return warp_best(r);
+}
+
+// Bilinear interpolation of a whole 2-D non-periodic grid at index-space point (x0, x1):
+// interp<double, Ts, 2> with a zero origin and the full grid as the view, the same
+// operations in the same order (bit-identical), 32-bit indices.
+template <typename Ts>
+__device__ __forceinline__ double interp2_grid(const Ts *__restrict__ V, int n0, int n1, double x0,
+                                               double x1, double v_out) {
+    const double hi0 = (double)(n0 - 1), hi1 = (double)(n1 - 1), lo = -0.0;
+    if (!(x0 >= lo - (double)BOX_EPS && x0 <= hi0 + (double)BOX_EPS)) return v_out;
+    if (!(x1 >= lo - (double)BOX_EPS && x1 <= hi1 + (double)BOX_EPS)) return v_out;
+    x0 = x0 < lo ? lo : (x0 > hi0 ? hi0 : x0);
+    x1 = x1 < lo ? lo : (x1 > hi1 ? hi1 : x1);
+    const double f0 = floor(x0), f1 = floor(x1);
+    int c0 = (int)f0, c1 = (int)f1;
+    double w0 = x0 - f0, w1 = x1 - f1;
+    if (c0 > n0 - 2) {
+        c0 = n0 - 2;
+        w0 = 1.0;
+    }
+    if (c1 > n1 - 2) {
+        c1 = n1 - 2;
+        w1 = 1.0;
+    }
+    const Ts *p = V + (c0 + n0 * c1);
+    const double a = lerp<double>((double)p[0], (double)p[1], w0);
+    const double b = lerp<double>((double)p[n0], (double)p[n0 + 1], w0);
+    return lerp<double>(a, b, w1);
+}
+
+// lane_bracket for the 2-D affine class on a non-periodic grid (the labelling of the
+// local-class configs): state x and speed cs of the step passed in, the dynamics and
+// interpolation written out — the same arithmetic, bit for bit.
+template <typename Ts>
+__device__ __forceinline__ BestPair lane_bracket_2d(const DevProblem<double, Ts> &P,
+                                                    const Ts *__restrict__ V, const double g[3],
+                                                    const double x[3], double cs, int lane,
+                                                    const double (*uctl)[4]) {
+    const bool kruz = P.cost == HJ_COST_KRUZKOV;
+    const double base = kruz ? P.kcost : P.h * cost_state(P, x);
+    const int n0 = (int)P.n[0], n1 = (int)P.n[1];
+    BestPair r{INFINITY, INFINITY, -1};
+    for (int k = lane; k < P.K; k += 32) {
+        const double *u = uctl[k];
+        double f0 = fma(cs, u[0], P.b[0]);
+        f0 = fma(P.A[0], x[0], f0);
+        f0 = fma(P.A[1], x[1], f0);
+        double f1 = fma(cs, u[1], P.b[1]);
+        f1 = fma(P.A[3], x[0], f1);
+        f1 = fma(P.A[4], x[1], f1);
+        const double I = interp2_grid<Ts>(V, n0, n1, fma(P.hdx[0], f0, g[0]),
+                                          fma(P.hdx[1], f1, g[1]), P.v_out);
+        const double ck = kruz ? base : fma(P.h * P.lr, u[3], base);
         const double v = fma(P.beta, I, ck);
         if (v < r.best) {
             r.second = r.best;
@@ -143,6 +234,12 @@ __global__ void __launch_bounds__(256)
     const int64_t vn[3] = {P.n[0], P.n[1], P.n[2]};
     const int lane = threadIdx.x & 31;
     const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    __shared__ double uctl[HJ_MAX_CONTROLS][4];    // a_k (3 components), |a_k|^2
+    for (int i = threadIdx.x; i < P.K * 4; i += blockDim.x)
+        uctl[i >> 2][i & 3] = (i & 3) == 3 ? P.csq[i >> 2] : P.ctrl[i >> 2][i & 3];
+    __syncthreads();
+    const bool fast2 = DIM == 2 && !P.periodic[0] && !P.periodic[1] && P.dyn == HJ_DYN_AFFINE &&
+                       P.n[0] * P.n[1] < ((int64_t)1 << 31);
     for (int64_t t = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); t < N;
          t += warps) {
         double g[3] = {(double)(t % P.n[0]), (double)((t / P.n[0]) % P.n[1]),
@@ -174,9 +271,6 @@ __global__ void __launch_bounds__(256)
                 break;
             }
             if (s >= n_max) break;
-            const BestPair bp = lane_bracket<Ts, DIM>(P, V, o, vn, g, lane);
-            const int a = bp.arg;
-            mm = fmin(mm, bp.second - bp.best);
             double x[3] = {0, 0, 0};
 #pragma unroll
             for (int d = 0; d < DIM; ++d) x[d] = fma(g[d], P.dx[d], P.lo[d]);
@@ -184,8 +278,12 @@ __global__ void __launch_bounds__(256)
             double cs = 1.0;
             if (P.speed && P.dyn == HJ_DYN_AFFINE)
                 cs = interp<double, Ts, DIM>(P.speed, o, vn, P.n, P.periodic, zero, g, 1.0);
+            const BestPair bp = fast2 ? lane_bracket_2d<Ts>(P, V, g, x, cs, lane, uctl)
+                                      : lane_bracket<Ts, DIM>(P, V, o, vn, g, lane, uctl);
+            const int a = bp.arg;
+            mm = fmin(mm, bp.second - bp.best);
             double f[3];
-            dynamics(P, x, cs, a, f);
+            dynamics_u(P, x, cs, uctl[a], f);
             bool out = false;
 #pragma unroll
             for (int d = 0; d < DIM; ++d) {
