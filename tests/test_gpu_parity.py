@@ -152,6 +152,21 @@ def test_coop_list_mode_matches_scan_mode(idx, kernel, oracle_cache, monkeypatch
     assert torch.equal(out[0][0], out[1][0]) and out[0][1] == out[1][1]
 
 
+@pytest.mark.parametrize("idx", [1, 2, 3, 4])
+def test_coop_cluster_mode_matches_grid_mode(idx, monkeypatch):
+    """Opt-in cluster mode (each view solved by one thread-block cluster with the hardware
+    cluster barrier) must reproduce the grid-barrier iterates of a partitioned solve bit
+    for bit, and the per-view sweep counts."""
+    cfg = _cfg(idx)
+    out = []
+    for mode in ("0", "1"):
+        monkeypatch.setenv("HJ_COOP_CLUSTER", mode)
+        res = pipeline.run_isa(cfg, "f32")
+        out.append((res["V"].cpu(), [r["iterations"] for r in res["reports"] if r]))
+    assert torch.equal(out[0][0], out[1][0])
+    assert out[0][1] == out[1][1]
+
+
 def test_local_kernel_refuses_nonlocal_problem():
     cfg = _cfg(3)                        # Zermelo drift: feet leave the 3x3 cell block
     with pytest.raises(hj.HJError, match="does not qualify"):
