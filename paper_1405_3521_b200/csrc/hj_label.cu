@@ -103,9 +103,12 @@ __device__ __forceinline__ BestPair warp_best(BestPair a) {
 // dynamics() with the control's components u[0..2] from shared memory: the lanes of
 // a warp take different controls, and a lane-divergent read of the kernel-parameter
 // control table would serialise (one constant-bank address per pass)
+// (ct, st: cos and sin of the heading x[2], computed once per trajectory step for the
+// Dubins car — the same values dynamics() computes per control)
 template <typename Ts>
 __device__ __forceinline__ void dynamics_u(const DevProblem<double, Ts> &P, const double x[3],
-                                           double c, const double *u, double f[3]) {
+                                           double c, const double *u, double f[3], double ct,
+                                           double st) {
     if (P.dyn == HJ_DYN_AFFINE) {
 #pragma unroll
         for (int d = 0; d < 3; ++d) {
@@ -118,8 +121,8 @@ __device__ __forceinline__ void dynamics_u(const DevProblem<double, Ts> &P, cons
             f[d] = s;
         }
     } else if (P.dyn == HJ_DYN_DUBINS) {
-        f[0] = P.dub_v * cos(x[2]);
-        f[1] = P.dub_v * sin(x[2]);
+        f[0] = P.dub_v * ct;
+        f[1] = P.dub_v * st;
         f[2] = P.dub_w * u[0];
     } else {
         f[0] = x[1];
@@ -132,7 +135,8 @@ template <typename Ts, int DIM>
 __device__ __forceinline__ BestPair lane_bracket(const DevProblem<double, Ts> &P,
                                                  const Ts *__restrict__ V, const int64_t o[3],
                                                  const int64_t vn[3], const double g[3],
-                                                 int lane, const double (*uctl)[4]) {
+                                                 int lane, const double (*uctl)[4], double ct,
+                                                 double st) {
     double x[3] = {0, 0, 0};
 #pragma unroll
     for (int d = 0; d < DIM; ++d) x[d] = fma(g[d], P.dx[d], P.lo[d]);
@@ -144,7 +148,7 @@ __device__ __forceinline__ BestPair lane_bracket(const DevProblem<double, Ts> &P
     BestPair r{INFINITY, INFINITY, -1};
     for (int k = lane; k < P.K; k += 32) {
         double f[3];
-        dynamics_u(P, x, cs, uctl[k], f);
+        dynamics_u(P, x, cs, uctl[k], f, ct, st);
         double foot[3] = {0, 0, 0};
 #pragma unroll
         for (int d = 0; d < DIM; ++d) foot[d] = fma(P.hdx[d], f[d], g[d]);
@@ -225,23 +229,59 @@ __device__ __forceinline__ BestPair lane_bracket_2d(const DevProblem<double, Ts>
     return warp_best(r);
 }
 
+// The bracket of one trajectory point by one thread, controls in index order (the
+// serial scan warp_best reproduces: smallest value, lowest index among equal ones, the
+// second smallest of the multiset) — for small control sets (the Dubins car's 3), where a
+// warp per trajectory would leave most lanes idle.
 template <typename Ts, int DIM>
+__device__ __forceinline__ BestPair thread_bracket(const DevProblem<double, Ts> &P,
+                                                   const Ts *__restrict__ V, const int64_t o[3],
+                                                   const int64_t vn[3], const double g[3],
+                                                   const double x[3], double cs,
+                                                   const double (*uctl)[4], double ct, double st) {
+    const int64_t zero[3] = {0, 0, 0};
+    const double base = (P.cost == HJ_COST_KRUZKOV) ? P.kcost : P.h * cost_state(P, x);
+    BestPair r{INFINITY, INFINITY, -1};
+    for (int k = 0; k < P.K; ++k) {
+        double f[3];
+        dynamics_u(P, x, cs, uctl[k], f, ct, st);
+        double foot[3] = {0, 0, 0};
+#pragma unroll
+        for (int d = 0; d < DIM; ++d) foot[d] = fma(P.hdx[d], f[d], g[d]);
+        const double I = interp<double, Ts, DIM>(V, o, vn, P.n, P.periodic, zero, foot, P.v_out);
+        const double ck = (P.cost == HJ_COST_KRUZKOV) ? base : fma(P.h * P.lr, uctl[k][3], base);
+        const double v = fma(P.beta, I, ck);
+        if (v < r.best) {
+            r.second = r.best;
+            r.best = v;
+            r.arg = k;
+        } else if (v < r.second) {
+            r.second = v;
+        }
+    }
+    return r;
+}
+
+// THREAD: one thread per coarse node (small control sets), else one warp per node.
+template <typename Ts, int DIM, bool THREAD = false>
 __global__ void __launch_bounds__(256)
     k_label_warp(const DevProblem<double, Ts> P, const Ts *__restrict__ V,
                  const int8_t *__restrict__ piece, int64_t N, int64_t n_max, int32_t *label,
                  double *margin_out, double *geo_out, int32_t *steps_out) {
     const int64_t o[3] = {0, 0, 0};
     const int64_t vn[3] = {P.n[0], P.n[1], P.n[2]};
-    const int lane = threadIdx.x & 31;
-    const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    const int lane = THREAD ? 0 : (int)(threadIdx.x & 31);
+    const int64_t warps = THREAD ? (int64_t)gridDim.x * blockDim.x
+                                 : (int64_t)gridDim.x * (blockDim.x >> 5);
     __shared__ double uctl[HJ_MAX_CONTROLS][4];    // a_k (3 components), |a_k|^2
     for (int i = threadIdx.x; i < P.K * 4; i += blockDim.x)
         uctl[i >> 2][i & 3] = (i & 3) == 3 ? P.csq[i >> 2] : P.ctrl[i >> 2][i & 3];
     __syncthreads();
     const bool fast2 = DIM == 2 && !P.periodic[0] && !P.periodic[1] && P.dyn == HJ_DYN_AFFINE &&
                        P.n[0] * P.n[1] < ((int64_t)1 << 31);
-    for (int64_t t = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); t < N;
-         t += warps) {
+    for (int64_t t = THREAD ? blockIdx.x * (int64_t)blockDim.x + threadIdx.x
+                            : blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
+         t < N; t += warps) {
         double g[3] = {(double)(t % P.n[0]), (double)((t / P.n[0]) % P.n[1]),
                        (double)(t / (P.n[0] * P.n[1]))};
         double mm = INFINITY, mg = INFINITY;
@@ -278,12 +318,21 @@ __global__ void __launch_bounds__(256)
             double cs = 1.0;
             if (P.speed && P.dyn == HJ_DYN_AFFINE)
                 cs = interp<double, Ts, DIM>(P.speed, o, vn, P.n, P.periodic, zero, g, 1.0);
-            const BestPair bp = fast2 ? lane_bracket_2d<Ts>(P, V, g, x, cs, lane, uctl)
-                                      : lane_bracket<Ts, DIM>(P, V, o, vn, g, lane, uctl);
+            double ct = 0.0, st = 0.0;
+            if (P.dyn == HJ_DYN_DUBINS) {
+                ct = cos(x[2]);
+                st = sin(x[2]);
+            }
+            BestPair bp;
+            if constexpr (THREAD)
+                bp = thread_bracket<Ts, DIM>(P, V, o, vn, g, x, cs, uctl, ct, st);
+            else
+                bp = fast2 ? lane_bracket_2d<Ts>(P, V, g, x, cs, lane, uctl)
+                           : lane_bracket<Ts, DIM>(P, V, o, vn, g, lane, uctl, ct, st);
             const int a = bp.arg;
             mm = fmin(mm, bp.second - bp.best);
             double f[3];
-            dynamics_u(P, x, cs, uctl[a], f);
+            dynamics_u(P, x, cs, uctl[a], f, ct, st);
             bool out = false;
 #pragma unroll
             for (int d = 0; d < DIM; ++d) {
@@ -371,6 +420,76 @@ __global__ void k_prolong(const ProlongArgs A, const void *__restrict__ coarse,
     }
 }
 
+// The same prolongation, one fine x-row (i1, i2) per CTA iteration: the y/z coarse
+// intervals are uniform over the row, so the CTA first ORs, for every coarse x index J0,
+// the coarse bits over the row's y-z box (ryz[J0], shared memory), then each fine node
+// ORs ryz over its x interval — ~(cnt_y cnt_z + cnt_x) loads per node instead of
+// cnt_x cnt_y cnt_z (125 for the Dubins grid).  OR is order-free: bit-identical.
+__device__ __forceinline__ bool prolong_wrap(const ProlongArgs &A, int d, int64_t &c) {
+    if (A.periodic[d]) {
+        c %= A.nc[d];
+        if (c < 0) c += A.nc[d];
+        return true;
+    }
+    return c >= 0 && c <= A.nc[d] - 1;
+}
+
+template <bool MASK>
+__global__ void __launch_bounds__(256)
+    k_prolong_rows(const ProlongArgs A, const void *__restrict__ coarse,
+                   const int8_t *__restrict__ fine_piece, uint32_t *mask) {
+    extern __shared__ uint32_t ryz[];                 // [nc0]
+    const int32_t *lab = (const int32_t *)coarse;
+    const uint32_t *cmask = (const uint32_t *)coarse;
+    const int64_t rows = A.nf[1] * A.nf[2];
+    for (int64_t row = blockIdx.x; row < rows; row += gridDim.x) {
+        const int64_t i12[2] = {row % A.nf[1], row / A.nf[1]};
+        int64_t lo[2] = {0, 0}, hi[2] = {0, 0};
+        for (int e = 0; e < 2; ++e) {
+            const int d = e + 1;
+            if (d >= A.dim) continue;
+            const int64_t reach = A.R[d] + A.band;
+            lo[e] = -floordiv(-(i12[e] - reach), A.R[d]);   // ceil
+            hi[e] = floordiv(i12[e] + reach, A.R[d]);
+        }
+        __syncthreads();                                   // the previous row's reads
+        for (int64_t J0 = threadIdx.x; J0 < A.nc[0]; J0 += blockDim.x) {
+            uint32_t b = 0;
+            for (int64_t I2 = lo[1]; I2 <= hi[1]; ++I2) {
+                int64_t J2 = I2;
+                if (A.dim > 2 && !prolong_wrap(A, 2, J2)) continue;
+                for (int64_t I1 = lo[0]; I1 <= hi[0]; ++I1) {
+                    int64_t J1 = I1;
+                    if (A.dim > 1 && !prolong_wrap(A, 1, J1)) continue;
+                    const int64_t cidx = J0 + A.nc[0] * (J1 + A.nc[1] * J2);
+                    if (MASK) {
+                        b |= cmask[cidx];
+                    } else {
+                        const int32_t l = lab[cidx];
+                        b |= (l < 0) ? A.all : (1u << l);
+                    }
+                }
+            }
+            ryz[J0] = b;
+        }
+        __syncthreads();
+        const int64_t reach0 = A.R[0] + A.band;
+        for (int64_t i0 = threadIdx.x; i0 < A.nf[0]; i0 += blockDim.x) {
+            const int64_t lo0 = -floordiv(-(i0 - reach0), A.R[0]), hi0 = floordiv(i0 + reach0, A.R[0]);
+            uint32_t bits = 0;
+            for (int64_t I0 = lo0; I0 <= hi0; ++I0) {
+                int64_t J0 = I0;
+                if (!prolong_wrap(A, 0, J0)) continue;
+                bits |= ryz[J0];
+            }
+            const int64_t t = i0 + A.nf[0] * (i12[0] + A.nf[1] * i12[1]);
+            const int8_t p = fine_piece[t];
+            if (p >= 0) bits |= 1u << p;
+            mask[t] = bits & A.all;
+        }
+    }
+}
+
 // ISA step 2 (R9) from labels or masks of the coarse grid cg onto the nested fine grid fg
 hj_status prolong_launch(const hj_grid &cg, const hj_grid &fg, const int32_t ratio[3],
                          int32_t band, int32_t m, const void *coarse, bool is_mask,
@@ -387,6 +506,17 @@ hj_status prolong_launch(const hj_grid &cg, const hj_grid &fg, const int32_t rat
     A.band = band;
     A.all = m >= 32 ? 0xffffffffu : ((1u << m) - 1u);
     const int64_t Nf = grid_nodes(fg);
+    if (A.nc[0] <= 8192) {                  // row scheme (ryz fits in shared memory)
+        const int64_t rows = A.nf[1] * A.nf[2];
+        const int rb = (int)std::min<int64_t>(rows, 148 * 8);
+        const size_t sm = (size_t)A.nc[0] * sizeof(uint32_t);
+        if (is_mask)
+            k_prolong_rows<true><<<rb, 256, sm, s>>>(A, coarse, fine_piece, fine_mask);
+        else
+            k_prolong_rows<false><<<rb, 256, sm, s>>>(A, coarse, fine_piece, fine_mask);
+        HJ_CUDA(cudaGetLastError());
+        return HJ_OK;
+    }
     const int blocks = (int)std::min<int64_t>((Nf + 255) / 256, 148 * 16);
     if (is_mask)
         k_prolong<true><<<blocks, 256, 0, s>>>(A, coarse, fine_piece, Nf, fine_mask);
@@ -416,14 +546,25 @@ static hj_status label_impl(const hj_grid &g, const hj_problem &p, const hj_fiel
                             double *geo, int32_t *steps, cudaStream_t s) {
     auto P = make_dev_problem<double, Ts>(g, p, f);
     int64_t N = grid_nodes(g);
-    // one warp per coarse node
-    int blocks = (int)std::min<int64_t>((N + 7) / 8, 148 * 64);
-    if (g.dim == 2)
-        k_label_warp<Ts, 2><<<blocks, 256, 0, s>>>(P, V, f.piece, N, n_max, label, margin, geo,
-                                                   steps);
-    else
-        k_label_warp<Ts, 3><<<blocks, 256, 0, s>>>(P, V, f.piece, N, n_max, label, margin, geo,
-                                                   steps);
+    // one warp per coarse node; one thread per node for small control sets
+    const bool thread = p.n_controls <= 8;
+    int blocks = thread ? (int)std::min<int64_t>((N + 255) / 256, 148 * 8)
+                        : (int)std::min<int64_t>((N + 7) / 8, 148 * 64);
+    if (g.dim == 2) {
+        if (thread)
+            k_label_warp<Ts, 2, true><<<blocks, 256, 0, s>>>(P, V, f.piece, N, n_max, label,
+                                                             margin, geo, steps);
+        else
+            k_label_warp<Ts, 2><<<blocks, 256, 0, s>>>(P, V, f.piece, N, n_max, label, margin,
+                                                       geo, steps);
+    } else {
+        if (thread)
+            k_label_warp<Ts, 3, true><<<blocks, 256, 0, s>>>(P, V, f.piece, N, n_max, label,
+                                                             margin, geo, steps);
+        else
+            k_label_warp<Ts, 3><<<blocks, 256, 0, s>>>(P, V, f.piece, N, n_max, label, margin,
+                                                       geo, steps);
+    }
     HJ_CUDA(cudaGetLastError());
     return HJ_OK;
 }
