@@ -91,11 +91,15 @@ __global__ void k_assemble(const AsmView<T> *__restrict__ av, int nv,
     }
 }
 
-__global__ void k_plan(const uint32_t *__restrict__ mask, int64_t N, int64_t n0, int64_t n1,
-                       int m, int *bb /* [m][6]: lo0..2, hi0..2 */,
-                       unsigned long long *cnt) {
+// Bounding box and node count of every sub-domain in the fine mask.  Warp-aggregated:
+// for each sub-domain bit present in the warp's 32 nodes, one warp reduction per
+// coordinate bound and one shared update per warp (a node of reading R9 carries every
+// bit, so per-node shared atomics contended on the same m addresses).
+__global__ void __launch_bounds__(256)
+    k_plan(const uint32_t *__restrict__ mask, int64_t N, int64_t n0, int64_t n1, int m,
+           int *bb /* [m][6]: lo0..2, hi0..2 */, unsigned long long *cnt) {
     __shared__ int s_lo[HJ_MAX_SUBDOMAINS][3], s_hi[HJ_MAX_SUBDOMAINS][3];
-    __shared__ unsigned long long s_cnt[HJ_MAX_SUBDOMAINS];
+    __shared__ unsigned s_cnt[HJ_MAX_SUBDOMAINS];
     for (int t = threadIdx.x; t < HJ_MAX_SUBDOMAINS; t += blockDim.x) {
         for (int d = 0; d < 3; ++d) {
             s_lo[t][d] = 0x7fffffff;
@@ -104,24 +108,39 @@ __global__ void k_plan(const uint32_t *__restrict__ mask, int64_t N, int64_t n0,
         s_cnt[t] = 0;
     }
     __syncthreads();
-    for (int64_t gi = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; gi < N;
-         gi += (int64_t)gridDim.x * blockDim.x) {
-        uint32_t bits = mask[gi];
-        if (!bits) continue;
+    const int lane = threadIdx.x & 31;
+    const uint32_t mm = m >= 32 ? 0xffffffffu : ((1u << m) - 1u);
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t w0 = blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31); w0 < N;
+         w0 += stride) {
+        const int64_t gi = w0 + lane;
+        const uint32_t bits = gi < N ? (mask[gi] & mm) : 0u;
+        uint32_t any = __reduce_or_sync(0xffffffffu, bits);
+        if (!any) continue;
         int c[3];
         c[0] = (int)(gi % n0);
-        int64_t r = gi / n0;
+        const int64_t r = gi / n0;
         c[1] = (int)(r % n1);
         c[2] = (int)(r / n1);
-        while (bits) {
-            int k = __ffs(bits) - 1;
-            bits &= bits - 1;
-            if (k >= m) break;
+        while (any) {
+            const int k = __ffs(any) - 1;
+            any &= any - 1;
+            const bool has = (bits >> k) & 1u;
+            const unsigned cntk = __popc(__ballot_sync(0xffffffffu, has));
+            int lo[3], hi[3];
+#pragma unroll
             for (int d = 0; d < 3; ++d) {
-                atomicMin(&s_lo[k][d], c[d]);
-                atomicMax(&s_hi[k][d], c[d]);
+                lo[d] = __reduce_min_sync(0xffffffffu, has ? c[d] : 0x7fffffff);
+                hi[d] = __reduce_max_sync(0xffffffffu, has ? c[d] : -1);
             }
-            atomicAdd(&s_cnt[k], 1ull);
+            if (lane == 0) {
+#pragma unroll
+                for (int d = 0; d < 3; ++d) {
+                    atomicMin(&s_lo[k][d], lo[d]);
+                    atomicMax(&s_hi[k][d], hi[d]);
+                }
+                atomicAdd(&s_cnt[k], cntk);
+            }
         }
     }
     __syncthreads();
@@ -131,7 +150,7 @@ __global__ void k_plan(const uint32_t *__restrict__ mask, int64_t N, int64_t n0,
             atomicMin(&bb[6 * k + d], s_lo[k][d]);
             atomicMax(&bb[6 * k + 3 + d], s_hi[k][d]);
         }
-        atomicAdd(&cnt[k], s_cnt[k]);
+        atomicAdd(&cnt[k], (unsigned long long)s_cnt[k]);
     }
 }
 

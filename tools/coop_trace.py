@@ -15,7 +15,8 @@ idx = int(sys.argv[1]) if len(sys.argv) > 1 else 2
 isa = len(sys.argv) > 2 and sys.argv[2] == "isa"
 coarse = len(sys.argv) > 2 and sys.argv[2] == "coarse"
 cfg = W.make(idx)
-dp = hj.DeviceProblem(cfg.coarse if coarse else cfg.fine, "f32", sweep_kernel="local_coop")
+dp = hj.DeviceProblem(cfg.coarse if coarse else cfg.fine, "f32",
+                      sweep_kernel=os.environ.get("HJ_TRACE_KERNEL", "auto"))
 cap = 1 << 12
 buf = torch.zeros((8 + 256) * cap + 16, dtype=torch.int64, device="cuda")
 L = hj.lib()
