@@ -363,15 +363,52 @@ __device__ __forceinline__ void coop_eval_field(const DevProblem<T, T> &P, const
                 const T ck = kruz ? C0 : C0 + hlr * P.csq[k];
                 best = fmin(best, fma(w1, fma(w0, A3, A2), fma(w0, A1, ck)));
             }
-        } else {   // box edge (R3): the general interpolation on the global V^n
+        } else {
+            // box edge (R3): interp()'s arithmetic step for step (box test, clamp onto the
+            // box, floor, weights, the last-cell rule, three lerps), the corners read from
+            // the staged block — it holds V^n of the view and v_out outside it, exactly
+            // what interp()'s view_fetch returns.  A corner one past the block only occurs
+            // with weight 0 (foot offset exactly +1), where any finite value gives the same
+            // lerp, so its index is clamped.  Offsets beyond one cell (not expected for the
+            // class) take interp() on the global V^n.
             const int64_t o[3] = {vw.o[0], vw.o[1], 0};
             const int64_t vn[3] = {vw.vn[0], vw.vn[1], 1};
+            const T eps = (T)BOX_EPS;
+            const T lo0 = -(T)gi[0], hi0 = (T)(P.n[0] - 1 - gi[0]);
+            const T lo1 = -(T)gi[1], hi1 = (T)(P.n[1] - 1 - gi[1]);
             T eb = (T)INFINITY;
 #pragma unroll 1
             for (int k = 0; k < P.K; ++k) {
-                const T delta[3] = {DYN == HJ_DYN_AFFINE ? fma(S0, P.ctrl[k][0], D0) : D0,
-                                    fma(S1, P.ctrl[k][DYN == HJ_DYN_AFFINE ? 1 : 0], D1), T(0)};
-                const T I = interp<T, T, 2>(Vi, o, vn, P.n, P.periodic, gi, delta, P.v_out);
+                const T e0 = DYN == HJ_DYN_AFFINE ? fma(S0, P.ctrl[k][0], D0) : D0;
+                const T e1 = fma(S1, P.ctrl[k][DYN == HJ_DYN_AFFINE ? 1 : 0], D1);
+                T I;
+                if (!(e0 >= lo0 - eps && e0 <= hi0 + eps) || !(e1 >= lo1 - eps && e1 <= hi1 + eps)) {
+                    I = P.v_out;
+                } else {
+                    const T xa = e0 < lo0 ? lo0 : (e0 > hi0 ? hi0 : e0);
+                    const T xb = e1 < lo1 ? lo1 : (e1 > hi1 ? hi1 : e1);
+                    const T fa = floor(xa), fb = floor(xb);
+                    if (fa < T(-1) || fa > T(1) || fb < T(-1) || fb > T(1)) {
+                        const T delta[3] = {e0, e1, T(0)};
+                        I = interp<T, T, 2>(Vi, o, vn, P.n, P.periodic, gi, delta, P.v_out);
+                    } else {
+                        int ca = (int)fa, cb = (int)fb;
+                        T wa = xa - fa, wb = xb - fb;
+                        if (gi[0] + ca > P.n[0] - 2) {
+                            ca = (int)(P.n[0] - 2 - gi[0]);
+                            wa = T(1);
+                        }
+                        if (gi[1] + cb > P.n[1] - 2) {
+                            cb = (int)(P.n[1] - 2 - gi[1]);
+                            wb = T(1);
+                        }
+                        const int ba = c + 1 + ca, bb = r + 1 + cb;      // block col / row
+                        const int ba1 = min(ba + 1, BP - 1), bb1 = min(bb + 1, BP - 1);
+                        const T a = lerp<T>(b[bb * BP + ba], b[bb * BP + ba1], wa);
+                        const T a2 = lerp<T>(b[bb1 * BP + ba], b[bb1 * BP + ba1], wa);
+                        I = lerp<T>(a, a2, wb);
+                    }
+                }
                 const T ck = kruz ? base : fma(hlr, P.csq[k], base);
                 eb = fmin(eb, fma(beta, I, ck));
             }
