@@ -729,13 +729,26 @@ __global__ void __launch_bounds__(CoopNW<T>::nw * 32, CoopNW<T>::minb)
                 const int vn0 = (int)vw.vn[0], vn1 = (int)vw.vn[1], vn2 = (int)vw.vn[2];
                 const T *__restrict__ Vi = vw.V[n & 1];
                 const int x0 = mx[s2] * 8, y0 = my[s2] * 8;
-                const bool inner = EV != 3 && x0 >= 1 && y0 >= 1 && x0 + 9 <= vn0 && y0 + 9 <= vn1;
+                const bool inner = x0 >= 1 && y0 >= 1 && x0 + 9 <= vn0 && y0 + 9 <= vn1;
                 if (inner) {
                     const T *__restrict__ src = Vi + ((int64_t)(y0 - 1) * vn0 + (x0 - 1));
+                    // Dubins: planes z-1, z, z+1 (periodic in the view, as below)
+                    int64_t poff[3] = {0, 0, 0};
+                    if (EV == 3) {
+#pragma unroll
+                        for (int q = 0; q < 3; ++q) {
+                            int lk = mz[s2] - 1 + q;
+                            if (lk < 0) lk += vn2;
+                            if (lk >= vn2) lk -= vn2;
+                            poff[q] = (int64_t)lk * vn0 * vn1;
+                        }
+                    }
 #pragma unroll
                     for (int k = 0; k < NLD; ++k) {
                         const int e = lane + 32 * k;
-                        ld[s2][k] = e < BLK ? src[(e / BP) * vn0 + e % BP] : v_out;
+                        const int q = e / (BP * BP), ee = e - (BP * BP) * q;
+                        const int64_t po = q == 0 ? poff[0] : (q == 1 ? poff[1] : poff[2]);
+                        ld[s2][k] = e < BLK ? src[po + (ee / BP) * vn0 + ee % BP] : v_out;
                     }
                 } else {
 #pragma unroll
@@ -873,8 +886,8 @@ __global__ void __launch_bounds__(CoopNW<T>::nw * 32, CoopNW<T>::minb)
             }
         }
         if (stopped == all) break;
-        // per-CTA residual / work of this sweep, one atomic per view
-        __syncthreads();
+        // per-CTA residual / work of this sweep, one atomic per view (the chunk loop ended
+        // on a CTA barrier, or never ran: cres/cwork are final)
         if (threadIdx.x < (unsigned)S.n_views) {
             const int v = threadIdx.x;
             const double m = (double)CoopBits<T>::value(cres[v]);
