@@ -129,8 +129,6 @@ __device__ __forceinline__ void coop_eval(const DevProblem<T, T> &P, const Local
     if ((dlo >> lane) & 1u) lstw[__popc(dlo & lt)] = (int8_t)lane;
     if ((dhi >> lane) & 1u) lstw[plo + __popc(dhi & lt)] = (int8_t)(32 + lane);
     __syncwarp();
-    const bool dbg = g_tb_trace.buf && blockIdx.x == 0 && threadIdx.x == 0;
-    const long long dc0 = dbg ? clock64() : 0;
             T rmax = T(0);
     unsigned long long cm = 0;             // changed nodes (bit = local index)
     int evald = 0;
@@ -196,7 +194,6 @@ __device__ __forceinline__ void coop_eval(const DevProblem<T, T> &P, const Local
         }
     }
     }
-    const long long dc1 = dbg ? clock64() : 0;
     // box-edge nodes (R3): 8 at a time, 4 lanes per node (one per quadrant, all its
     // controls)
     const int nE = __popcll(de);
@@ -261,15 +258,6 @@ __device__ __forceinline__ void coop_eval(const DevProblem<T, T> &P, const Local
             }
         }
     }
-    }
-    if (dbg) {
-        const long long dc2 = clock64();
-        unsigned long long *acc = g_tb_trace.buf + (8 + 256) * g_tb_trace.cap;
-        acc[0] += dc1 - dc0;
-        acc[1] += dc2 - dc1;
-        acc[2] += 1;
-        acc[3] += nI;
-        acc[4] += __popcll(de);
     }
     rmax_out = rmax;
     cm_out = cm;
@@ -614,7 +602,12 @@ __global__ void __launch_bounds__(CoopNW<T>::nw * 32, CoopNW<T>::minb)
         asm("mov.u32 %0, %%clusterid.x;" : "=r"(grp));
         asm("mov.u32 %0, %%nclusterid.x;" : "=r"(ngrp));
     }
-    const bool tr = g_tb_trace.buf != nullptr && blockIdx.x == 0 && threadIdx.x == 0;
+    // (debug trace, tools/coop_trace.py: read once — after each barrier a global read
+    // would cost an L2 round trip in front of the CTA's arrival)
+    unsigned long long *const tr_buf = g_tb_trace.buf;
+    const long long tr_cap = g_tb_trace.cap;
+    const bool tr = tr_buf != nullptr && blockIdx.x == 0 && threadIdx.x == 0;
+    const bool tr_all = tr_buf != nullptr && threadIdx.x == 0 && gridDim.x <= 256;
     unsigned long long t_a = 0, t_b = 0, t_s = 0, t_l = 0, t_e = 0, t_m = 0, t_q = 0;
     int qitems = 0;
     for (int vs = (int)grp; vs < (CL ? S.n_views : 1); vs += (int)ngrp) {
@@ -897,10 +890,10 @@ __global__ void __launch_bounds__(CoopNW<T>::nw * 32, CoopNW<T>::minb)
         }
         if (S.use_list && blockIdx.x == 0 && threadIdx.x == 0) S.count[(n + 2) % 3] = 0;
         if (tr) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_b));
-        if (g_tb_trace.buf && threadIdx.x == 0 && n < g_tb_trace.cap && gridDim.x <= 256) {
+        if (tr_all && n < tr_cap) {
             unsigned long long t_arr;              // every CTA's arrival (load balance)
             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_arr));
-            g_tb_trace.buf[8 * g_tb_trace.cap + 256 * n + blockIdx.x] = t_arr;
+            tr_buf[8 * tr_cap + 256 * n + blockIdx.x] = t_arr;
         }
         if constexpr (CL) {
             // (acquire: the SM's L1 is invalidated, the cluster's writes are visible)
@@ -910,10 +903,10 @@ __global__ void __launch_bounds__(CoopNW<T>::nw * 32, CoopNW<T>::minb)
             coop_grid_barrier(reinterpret_cast<unsigned *>(S.count + 3),
                               (unsigned)(n + 1) * gridDim.x);
         }
-        if (tr && n < g_tb_trace.cap) {
+        if (tr && n < tr_cap) {
             unsigned long long t_c;
             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_c));
-            unsigned long long *o = g_tb_trace.buf + 8 * n;
+            unsigned long long *o = tr_buf + 8 * n;
             o[0] = t_a;
             o[1] = t_b;
             o[2] = t_c;

@@ -41,9 +41,6 @@ else:
 hb = buf.cpu().numpy()
 t = hb[: 8 * cap].reshape(-1, 8)[: rep["iterations"]].astype(np.float64)
 raw = hb[: 8 * cap].reshape(-1, 8)[: rep["iterations"], 3]
-acc = hb[(8 + 256) * cap:]
-if acc[2]:
-    print(f"coop_eval (block 0 warp 0): calls {acc[2]}  interior {acc[0] / acc[2]:.0f} cyc  edge {acc[1] / acc[2]:.0f} cyc  nI {acc[3] / acc[2]:.1f}  nE {acc[4] / acc[2]:.2f}  prunable quadrants/call final {acc[5] / acc[2]:.2f} running {acc[6] / acc[2]:.2f}")
 arr = hb[8 * cap:(8 + 256) * cap].reshape(-1, 256)[: rep["iterations"]].astype(np.float64)
 ncta = int((arr[0] > 0).sum())
 arr = arr[:, :ncta]
