@@ -155,16 +155,20 @@ def test_coop_list_mode_matches_scan_mode(idx, kernel, oracle_cache, monkeypatch
 @pytest.mark.parametrize("idx", [1, 2, 3, 4])
 def test_coop_cluster_mode_matches_grid_mode(idx, monkeypatch):
     """Opt-in cluster mode (each view solved by one thread-block cluster with the hardware
-    cluster barrier) must reproduce the grid-barrier iterates of a partitioned solve bit
-    for bit, and the per-view sweep counts."""
+    cluster barrier) and the device-list enumeration of all views' mini-tiles must
+    reproduce the grid-barrier / mask-scan iterates of a partitioned solve bit for bit,
+    and the per-view sweep counts."""
     cfg = _cfg(idx)
     out = []
-    for mode in ("0", "1"):
-        monkeypatch.setenv("HJ_COOP_CLUSTER", mode)
+    # grid barrier + mask scan, cluster mode, grid barrier + device list of all views
+    for cluster, lst in (("0", "0"), ("1", "0"), ("0", "1")):
+        monkeypatch.setenv("HJ_COOP_CLUSTER", cluster)
+        monkeypatch.setenv("HJ_COOP_LIST", lst)
         res = pipeline.run_isa(cfg, "f32")
         out.append((res["V"].cpu(), [r["iterations"] for r in res["reports"] if r]))
-    assert torch.equal(out[0][0], out[1][0])
-    assert out[0][1] == out[1][1]
+    for o in out[1:]:
+        assert torch.equal(out[0][0], o[0])
+        assert out[0][1] == o[1]
 
 
 def test_local_kernel_refuses_nonlocal_problem():
