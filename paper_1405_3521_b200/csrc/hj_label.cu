@@ -317,7 +317,8 @@ __global__ void __launch_bounds__(256)
             const int64_t zero[3] = {0, 0, 0};
             double cs = 1.0;
             if (P.speed && P.dyn == HJ_DYN_AFFINE)
-                cs = interp<double, Ts, DIM>(P.speed, o, vn, P.n, P.periodic, zero, g, 1.0);
+                cs = fast2 ? interp2_grid<Ts>(P.speed, (int)P.n[0], (int)P.n[1], g[0], g[1], 1.0)
+                           : interp<double, Ts, DIM>(P.speed, o, vn, P.n, P.periodic, zero, g, 1.0);
             double ct = 0.0, st = 0.0;
             if (P.dyn == HJ_DYN_DUBINS) {
                 ct = cos(x[2]);
