@@ -11,10 +11,13 @@
 // arithmetic as k_sweep_local2d: bit-identical iterates), writes V^{n+1}, and ORs the
 // 3 x 3 dilation of its changed nodes into the masks of the 9 surrounding mini-tiles
 // for sweep n+1 — a mini-tile whose mask was empty is appended to the next list.  Then
-// one grid-wide barrier; every CTA reads the per-view residuals of sweep n and applies
-// the stopping rule itself (identical decisions everywhere), so the host never waits
-// per sweep.  No halo is recomputed, no tile is visited whose nodes cannot change, and
-// the node-level work is spread over all SMs every sweep.
+// one grid-wide barrier (coop_grid_barrier: a monotone arrival counter); at the start of
+// sweep n+1 every CTA reads the per-view residuals of sweep n together with its mask
+// scan and applies the stopping rule itself before any evaluation (identical decisions
+// everywhere), so the host never waits per sweep.  No halo is recomputed, no tile is
+// visited whose nodes cannot change, and the node-level work is spread over all SMs
+// every sweep.  (Opt-in cluster mode, HJ_COOP_CLUSTER=1: one thread-block cluster per
+// view with the hardware cluster barrier — measured slower.)
 //
 // Nodes not recomputed hold the same value in both buffers (they did not change in the
 // previous sweep either), so nothing is copied; the final iterate of view v is in
