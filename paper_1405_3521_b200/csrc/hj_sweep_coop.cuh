@@ -428,6 +428,7 @@ __device__ __forceinline__ void coop_eval_dubins(const DevProblem<T, T> &P, cons
                                                  const T *__restrict__ b, int8_t *lstw,
                                                  unsigned long long di, int64_t x0, int64_t y0,
                                                  int64_t z, T d0, T d1, T *__restrict__ Vo,
+                                                 const T *__restrict__ wext,
                                                  T &rmax_out, unsigned long long &cm_out,
                                                  int &evald_out) {
     constexpr int BP = 10;
@@ -491,12 +492,30 @@ __device__ __forceinline__ void coop_eval_dubins(const DevProblem<T, T> &P, cons
                 I3[s] = lerp<T>(a, bb, wy);
             }
             const T dM = I3[0] - I3[1], dP = I3[2] - I3[1];
+            if (kruz) {
+                // Kruzkov (every control costs the same): within each sign group of
+                // d_k = h w a_k / dth the computed bracket fl(beta fl(|d_k| D + I0) + c) is
+                // monotone in |d_k| (D = I_{+-1} - I0 fixed, rounding is monotone), so
+                // its minimum over the group is at the group's smallest or largest
+                // |d_k| — the same min as the loop over all controls, bit for bit.
+                // wext: {min, max} |d_k| over d_k >= 0, then over d_k < 0 (+inf / -inf
+                // when a group is empty: those candidates never win).
+                if (wext[0] <= wext[1]) {
+                    best = fmin(best, fma(beta, fma(wext[0], dP, I3[1]), base));
+                    best = fmin(best, fma(beta, fma(wext[1], dP, I3[1]), base));
+                }
+                if (wext[2] <= wext[3]) {
+                    best = fmin(best, fma(beta, fma(wext[2], dM, I3[1]), base));
+                    best = fmin(best, fma(beta, fma(wext[3], dM, I3[1]), base));
+                }
+            } else {
 #pragma unroll 4
-            for (int k = 0; k < P.K; ++k) {
-                const T dk = hw * P.ctrl[k][0];
-                const T I = fma(fabs(dk), dk < T(0) ? dM : dP, I3[1]);
-                const T ck = kruz ? base : fma(hlr, P.csq[k], base);
-                best = fmin(best, fma(beta, I, ck));
+                for (int k = 0; k < P.K; ++k) {
+                    const T dk = hw * P.ctrl[k][0];
+                    const T I = fma(fabs(dk), dk < T(0) ? dM : dP, I3[1]);
+                    const T ck = fma(hlr, P.csq[k], base);
+                    best = fmin(best, fma(beta, I, ck));
+                }
             }
         }
         if (mono) best = fmin(best, V00);
@@ -586,6 +605,20 @@ __global__ void __launch_bounds__(CoopNW<T>::nw * 32, CoopNW<T>::minb)
     __shared__ SweepView<T> sview[HJ_MAX_SUBDOMAINS];
     // local class: the quadrant control tables ax | ay | ck, [3][4][KQ]
     __shared__ T sctl[EV == 0 ? 12 * KQ : 1];
+    // Dubins: extreme |h w a_k / dth| of each sign group (coop_eval_dubins)
+    __shared__ T dub_wext[4];
+    if (EV == 3 && threadIdx.x == 0) {
+        const T hw = P.hdx[2] * P.dub_w;
+        T e[4] = {(T)INFINITY, -(T)INFINITY, (T)INFINITY, -(T)INFINITY};
+        for (int k = 0; k < P.K; ++k) {
+            const T dk = hw * P.ctrl[k][0];
+            const T w = fabs(dk);
+            const int o = dk < T(0) ? 2 : 0;
+            e[o] = fmin(e[o], w);
+            e[o + 1] = fmax(e[o + 1], w);
+        }
+        for (int i = 0; i < 4; ++i) dub_wext[i] = e[i];
+    }
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if (threadIdx.x < (unsigned)S.n_views) sview[threadIdx.x] = G->v[threadIdx.x];
     if (EV == 0 && threadIdx.x < 12u * KQ) {
@@ -809,8 +842,8 @@ __global__ void __launch_bounds__(CoopNW<T>::nw * 32, CoopNW<T>::minb)
                     sincos_t(th, &sn, &cn);
                     coop_eval_dubins<T>(P, vw, blk[warp][s2], lst[warp][s2], d_s | e_s,
                                         x0, y0, z, P.hdx[0] * (P.dub_v * cn),
-                                        P.hdx[1] * (P.dub_v * sn), vw.V[(n + 1) & 1], rmax, cm,
-                                        evald);
+                                        P.hdx[1] * (P.dub_v * sn), vw.V[(n + 1) & 1], dub_wext,
+                                        rmax, cm, evald);
                 } else if constexpr (EV == 0)
                     coop_eval<T, KQ, PC>(P, C, vw, blk[warp][s2], spd[warp][s2], lst[warp][s2],
                                          sctl, d_s, e_s, x0, y0, vw.V[(n + 1) & 1], rmax, cm,

@@ -105,6 +105,11 @@ def test_sweep_kernels_match_oracle(idx, dtype, oracle_cache):
         if k in out:
             assert torch.equal(out["local_scalar"][0], out[k][0]), k
             assert out["local_scalar"][1] == out[k][1], k
+    # the cooperative Dubins sweep evaluates only the extreme controls of each sign group
+    # (Kruzkov: exact, the bracket is monotone in |d_k|) — same iterates as the full loop
+    if "dubins" in out and "dubins_coop" in out:
+        assert torch.equal(out["dubins"][0], out["dubins_coop"][0])
+        assert out["dubins"][1] == out["dubins_coop"][1]
 
 
 @pytest.mark.parametrize("max_iter", [1, 5, 8, 13, 16])
