@@ -9,6 +9,12 @@
 
 namespace hj {
 
+// control sets up to this size are labelled one thread per trajectory (a warp per
+// trajectory would leave most lanes without a control)
+#ifndef HJ_LABEL_THREAD_MAX_K
+#define HJ_LABEL_THREAD_MAX_K 16
+#endif
+
 // min over controls of the Tdef bracket at index-space point g (fp64), lowest
 // index argmin, second-best gap.
 template <typename Ts, int DIM>
@@ -548,7 +554,7 @@ static hj_status label_impl(const hj_grid &g, const hj_problem &p, const hj_fiel
     auto P = make_dev_problem<double, Ts>(g, p, f);
     int64_t N = grid_nodes(g);
     // one warp per coarse node; one thread per node for small control sets
-    const bool thread = p.n_controls <= 8;
+    const bool thread = p.n_controls <= HJ_LABEL_THREAD_MAX_K;
     int blocks = thread ? (int)std::min<int64_t>((N + 255) / 256, 148 * 8)
                         : (int)std::min<int64_t>((N + 7) / 8, 148 * 64);
     if (g.dim == 2) {
