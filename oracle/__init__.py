@@ -35,8 +35,10 @@ INTERIOR, TARGET, GHOST = 0, 1, 2
 def build(force: bool = False) -> str:
     """Compile the C oracle (gcc, no FMA contraction, no fast-math)."""
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
-        cmd = ["gcc", "-O2", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared",
-               "-o", _LIB, _SRC, "-lm"]
+        # -fopenmp: the per-node loops run on the host's cores (Jacobi: every node reads
+        # only the previous iterate, so the result does not depend on the thread count)
+        cmd = ["gcc", "-O2", "-ffp-contract=off", "-fno-fast-math", "-fopenmp", "-fPIC",
+               "-shared", "-o", _LIB, _SRC, "-lm"]
         subprocess.run(cmd, check=True)
     return _LIB
 
@@ -311,6 +313,27 @@ def ra(problem, m, C, M, q, tol=None, max_iter=None):
     lib.or_ra_masks(problem.grid.size, int(m), ptrs, _ptr(np.ascontiguousarray(Vmin), _dp),
                     _ptr(np.ascontiguousarray(piece), _bp), float(thr), _ptr(mask, _up))
     return Vs, Vmin, mask, its
+
+
+def ra_masks(Vs, V, piece, thr):
+    """RA step 3 alone on given arrays: bit i of mask[j] set iff
+    piece[j] == i or |V_i(j) - V(j)| <= thr."""
+    lib = _load()
+    m = len(Vs)
+    arrs = [np.ascontiguousarray(v, np.float64) for v in Vs]
+    ptrs = (_dp * m)(*[_ptr(a, _dp) for a in arrs])
+    V = np.ascontiguousarray(V, np.float64)
+    piece = np.ascontiguousarray(piece, np.int8)
+    mask = np.empty(len(V), np.uint32)
+    lib.or_ra_masks(len(V), int(m), ptrs, _ptr(V, _dp), _ptr(piece, _bp), float(thr),
+                    _ptr(mask, _up))
+    return mask
+
+
+def threads():
+    """OpenMP threads the oracle's node loops use (OMP_NUM_THREADS, else all cores)."""
+    n = os.environ.get("OMP_NUM_THREADS")
+    return int(n) if n and n.isdigit() else (os.cpu_count() or 1)
 
 
 def assemble(mask, Vks, v_out):

@@ -207,6 +207,7 @@ static double or_node_g(const or_problem *p, long idx) { return p->g ? p->g[idx]
  * is a ghost holding v_out (R10); a target node holds g (Tdef line 242). */
 void or_classes(const or_problem *p, const unsigned int *mask, int k, signed char *cls) {
     long N = or_size(p);
+#pragma omp parallel for schedule(static)
     for (long i = 0; i < N; ++i) {
         int in = mask ? ((mask[i] >> k) & 1u) : 1;
         if (!in) cls[i] = OR_GHOST;
@@ -218,6 +219,9 @@ void or_classes(const or_problem *p, const unsigned int *mask, int k, signed cha
 double or_apply_T(const or_problem *p, const signed char *cls, const double *V, double *Vn) {
     long N = or_size(p);
     double res = 0.0;
+    /* every node is computed independently from V (Jacobi) and max is exact, so the
+     * result does not depend on the thread count */
+#pragma omp parallel for schedule(static) reduction(max : res)
     for (long idx = 0; idx < N; ++idx) {
         double v;
         if (cls[idx] == OR_GHOST) {
@@ -268,6 +272,7 @@ long or_value_iteration(const or_problem *p, const signed char *cls, double *V, 
 /* Discrete optimal feedback at every node (north_star "coarse feedback"). */
 void or_feedback(const or_problem *p, const double *V, int *astar, double *margin) {
     long N = or_size(p);
+#pragma omp parallel for schedule(static)
     for (long idx = 0; idx < N; ++idx) {
         long ii[3];
         double gi[3];
@@ -353,6 +358,7 @@ int or_label_trajectory(const or_problem *p, const double *V, long start, long n
 
 void or_label_nodes(const or_problem *p, const double *V, const long *nodes, long count,
                     long n_max, int *labels, long *steps, double *margins, double *geo) {
+#pragma omp parallel for schedule(dynamic, 64)
     for (long t = 0; t < count; ++t)
         labels[t] = or_label_trajectory(p, V, nodes[t], n_max, &steps[t], &margins[t], &geo[t]);
 }
@@ -373,6 +379,7 @@ void or_prolong_mask(const long nc[3], const long nf[3], const int periodic[3], 
     unsigned int all = (m >= 32) ? 0xffffffffu : ((1u << m) - 1u);
     long Nf = 1;
     for (int d = 0; d < dim; ++d) Nf *= nf[d];
+#pragma omp parallel for schedule(static)
     for (long idx = 0; idx < Nf; ++idx) {
         long ii[3] = {0, 0, 0}, t = idx;
         for (int d = 0; d < dim; ++d) {
@@ -432,6 +439,7 @@ void or_prolong(const long nc[3], const long nf[3], const int periodic[3], int d
  * |V_i(j) - V(j)| <= thr, thr = 2 (C dx^q + M dx); bit i of mask[j]. */
 void or_ra_masks(long N, int m, const double *const *Vi, const double *V,
                  const signed char *piece, double thr, unsigned int *mask) {
+#pragma omp parallel for schedule(static)
     for (long j = 0; j < N; ++j) {
         unsigned int bits = 0;
         for (int i = 0; i < m; ++i)
@@ -455,6 +463,7 @@ long or_solve_subdomain(const or_problem *p, const unsigned int *mask, int k, do
 /* ISA step 4 (§4): Vbar(j) = min { V_k(j) : x_j in S_k }. */
 void or_assemble(long N, int m, const unsigned int *mask, const double *const *Vk, double v_out,
                  double *Vbar) {
+#pragma omp parallel for schedule(static)
     for (long j = 0; j < N; ++j) {
         double v = v_out;
         int any = 0;

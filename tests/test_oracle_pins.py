@@ -276,8 +276,9 @@ def test_p11_dynamics_through_bracket(kind):
             f = [math.cos(pt[2]), math.sin(pt[2]), a[0]]
         else:
             f = [pt[1], (1 - pt[0] ** 2) * pt[1] - pt[0] + a[0]]
-        for d in range(grid.dim - (1 if kind == "dubins" else 0)):
-            # lambda = 0, l = 0 -> bracket = I[x_d](x + h f) = x_d + h f_d
+        for d in range(grid.dim):
+            # lambda = 0, l = 0 -> bracket = I[x_d](x + h f) = x_d + h f_d (the heading
+            # field is linear in its index away from the periodic wrap)
             val = o.bracket(xs[d].reshape(-1), gi, k)
             assert abs(val - (pt[d] + h * f[d])) < 1e-12, (kind, k, d)
     if kind == "vdp":
@@ -484,3 +485,277 @@ def test_p14_prolong_mask_matches_label_prolongation():
         a = oracle.prolong(cg, fg, (4, 4), band, lab, m, fpiece)
         b = oracle.prolong_mask(cg, fg, (4, 4), band, cmask, m, fpiece)
         assert np.array_equal(a, b)
+
+
+# ---------------------------------------------------------------------------
+# P15  the speed field c(x) of f = c(x) u_a (config 2's dynamics, §2 line 36).
+#  (a) c == 2 on the lattice with h = dx/2: every foot lands on a neighbour node, so the
+#      Kruzkov values are the BFS ones, V = 1 - beta^d (a speed ignored or squared puts
+#      the feet half a cell or two cells away).
+#  (b) c depending on x only, target = the left edge: the minimum time is the 1-D
+#      travel time T(x) = int_0^x ds / c(s) = 2 ln(1 + x/2) for c = 1 + x/2, and the
+#      discrete times converge to it at O(dx) (Theorem 3.1).
+# ---------------------------------------------------------------------------
+def test_p15a_constant_speed_lattice():
+    grid = W.Grid((13, 9), (-1.0, -0.5), (1.4, 1.1), (False, False))
+    rng = np.random.default_rng(15)
+    piece = np.full(grid.size, -1, np.int8)
+    piece[rng.choice(grid.size, 3, replace=False)] = np.arange(3)
+    speed = np.full(grid.size, 2.0)
+    p = mk_problem(grid, W.axis_controls(), piece, h=grid.spacing(0) / 2, speed=speed)
+    V, it, res = oracle.OracleProblem(p).solve()
+    d = bfs_distance((9, 13), (piece >= 0).reshape(9, 13)).reshape(-1)
+    beta = 1.0 / (1.0 + p.h)
+    np.testing.assert_allclose(V, 1.0 - beta ** d, rtol=0, atol=1e-13)
+    assert it == d.max() + 1
+
+
+def test_p15b_variable_speed_travel_time():
+    errs = []
+    for n in (21, 41, 81):
+        grid = W.Grid((n, (n - 1) // 4 + 1), (0.0, 0.0), (1.0, 0.25), (False, False))
+        x, y = [a.reshape(-1) for a in grid.mesh()]
+        piece = np.where(np.isclose(x, 0.0), 0, -1).astype(np.int8)
+        speed = 1.0 + 0.5 * x
+        p = mk_problem(grid, W.unit_circle_controls(64), piece, h=grid.spacing(0) / 1.5,
+                       speed=speed, tol=1e-12)
+        V, it, res = oracle.OracleProblem(p).solve()
+        Td = -np.log1p(-V) * p.h / math.log1p(p.h)
+        T = 2.0 * np.log1p(0.5 * x)
+        err = np.abs(Td - T).max()
+        assert err <= 2.0 * grid.spacing(0), (n, err)
+        errs.append(err)
+    assert errs[-1] < errs[0] / 2.5
+    # the speed really enters: constant speed 1 would give T = x (0.19 off at x = 1)
+    assert abs(T.max() - 1.0) > 0.15
+
+
+# ---------------------------------------------------------------------------
+# P16  the control minimisation of the bracket (R7): best = min_k bracket_k, argmin =
+#      the LOWEST index attaining it, margin = second smallest bracket - smallest (>= 0),
+#      by brute force over the pinned bracket (P1-P13) at every node; and an exact tie
+#      (two lattice moves to the same BFS level) that has margin 0 and the lower index.
+# ---------------------------------------------------------------------------
+def test_p16_min_bracket_brute_force():
+    cfg = W.make(2, scale=24 / 1024, ratio=1)      # 25^2, 64 controls, speed field
+    p = cfg.fine
+    o = oracle.OracleProblem(p)
+    rng = np.random.default_rng(16)
+    V = rng.uniform(0, 1, p.grid.size)
+    a, margin = o.feedback(V)
+    n0 = p.grid.n[0]
+    for idx in range(p.grid.size):
+        if p.piece[idx] >= 0:
+            assert a[idx] == -1 and margin[idx] == np.inf
+            continue
+        gi = [idx % n0, idx // n0]
+        b = np.array([o.bracket(V, gi, k) for k in range(p.n_controls)])
+        srt = np.sort(b)
+        assert a[idx] == int(np.nonzero(b == srt[0])[0][0])
+        assert margin[idx] == srt[1] - srt[0] and margin[idx] >= 0
+        best, arg, mm = o.min_bracket(V, gi)
+        assert best == srt[0] and arg == a[idx] and mm == margin[idx]
+
+
+def test_p16_exact_tie_lowest_index():
+    grid = W.Grid((7, 7), (0.0, 0.0), (1.0, 1.0), (False, False))
+    piece = np.full(grid.size, -1, np.int8)
+    piece[0] = 0                                      # target at node (0, 0)
+    ctrl = W.axis_controls()                          # +x, +y, -x, -y
+    p = mk_problem(grid, ctrl, piece)
+    o = oracle.OracleProblem(p)
+    V, _, _ = o.solve()
+    a, margin = o.feedback(V)
+    # node (i, j), i, j >= 1: -x and -y both reach BFS level i + j - 1 (an exact tie)
+    for j in range(1, 7):
+        for i in range(1, 7):
+            assert a[j * 7 + i] == 2 and margin[j * 7 + i] == 0.0
+    # on the axis y = 0 the move -x is unique: the best bracket is 1 - beta^i (level
+    # i - 1), the next best 1 - beta^(i+2) (+x or +y to level i + 1; -y leaves the box)
+    beta = 1.0 / (1.0 + p.h)
+    for i in range(1, 6):
+        assert a[i] == 2
+        assert abs(margin[i] - (beta ** i - beta ** (i + 2))) < 1e-14
+
+
+# ---------------------------------------------------------------------------
+# P17  the trajectory bookkeeping of the labelling (R8): a plain re-simulation with the
+#      feedback taken AT y_s (o.min_bracket at the off-grid point), the speed
+#      interpolated at y_s, y_{s+1} = y_s + h f / dx, the label of the nearest node,
+#      gives the oracle's labels and step counts exactly, its minimum control margin
+#      along the path exactly, and its "geo" output = the smallest distance of a
+#      nearest-node rounding (positions y_0..y_S) or of a box test (y_1..y_S) to its
+#      threshold.  A feedback taken at the nearest node instead moves differently (the
+#      test asserts that it would on this problem).
+# ---------------------------------------------------------------------------
+def _simulate(o, p, V, start, n_max):
+    g = p.grid
+    n = g.n
+    gi = [float(start % n[0]), float(start // n[0])]
+    dx = [g.spacing(0), g.spacing(1)]
+    mm, geo, differs = np.inf, np.inf, False
+    s = 0
+    while True:
+        # distance of the rounding floor(g + 1/2) to its threshold (a half-integer)
+        for d in range(2):
+            geo = min(geo, abs(gi[d] - (math.floor(gi[d]) + 0.5)))
+        r = [min(int(math.floor(gi[d] + 0.5)), n[d] - 1) for d in range(2)]
+        pc = p.piece[r[0] + n[0] * r[1]]
+        if pc >= 0:
+            return int(pc), s, mm, geo, differs
+        if s >= n_max:
+            return -1, s, mm, geo, differs
+        _, a, margin = o.min_bracket(V, gi)
+        _, a_node, _ = o.min_bracket(V, r)
+        differs |= (a_node != a)
+        mm = min(mm, margin)
+        c = o.interp(p.speed, gi) if p.speed is not None else 1.0
+        x = [g.lo[d] + gi[d] * dx[d] for d in range(2)]
+        u = p.controls[a]
+        out = False
+        for d in range(2):
+            f = c * u[d] + p.b[d]
+            for e in range(2):
+                f += p.A[d, e] * x[e]
+            gi[d] = gi[d] + p.h * f / dx[d]
+            geo = min(geo, abs(gi[d]), abs((n[d] - 1) - gi[d]))
+            out |= gi[d] < 0.0 or gi[d] > n[d] - 1
+        s += 1
+        if out:
+            return -1, s, mm, geo, differs
+
+
+@pytest.mark.parametrize("idx", [2, 3])
+def test_p17_trajectory_bruteforce(idx):
+    cfg = W.make(idx, scale=32 / (1024 if idx == 2 else 4096), ratio=1)
+    p = cfg.fine
+    o = oracle.OracleProblem(p)
+    V, _, _ = o.solve()
+    rng = np.random.default_rng(17)
+    nodes = rng.choice(np.nonzero(p.piece < 0)[0], 60, replace=False)
+    lab, st, mar, geo = o.label(V, nodes, cfg.n_max_steps)
+    any_differs = False
+    for t, start in enumerate(nodes):
+        el, es, em, eg, differs = _simulate(o, p, V, int(start), cfg.n_max_steps)
+        any_differs |= differs
+        assert (lab[t], st[t]) == (el, es), (start, lab[t], st[t], el, es)
+        assert mar[t] == em
+        assert abs(geo[t] - eg) <= 1e-12, (geo[t], eg)
+    assert any_differs       # the nearest node's feedback would have steered elsewhere
+    assert np.all(mar >= 0) and np.all(geo >= 0) and np.isfinite(geo).all()
+
+
+# ---------------------------------------------------------------------------
+# P18  the trajectory step budget n_max (R8): on the lattice, a node at BFS distance d
+#      from the target is labelled after exactly d steps; a budget of d - 1 steps ends
+#      unlabelled (-1) after d - 1 steps.
+# ---------------------------------------------------------------------------
+def test_p18_step_budget():
+    grid = W.Grid((11, 5), (0.0, 0.0), (1.0, 0.4), (False, False))
+    piece = np.full(grid.size, -1, np.int8)
+    piece[0] = 0
+    p = mk_problem(grid, W.axis_controls(), piece)
+    o = oracle.OracleProblem(p)
+    V, _, _ = o.solve()
+    d = bfs_distance((5, 11), (piece >= 0).reshape(5, 11)).reshape(-1)
+    nodes = np.nonzero(d >= 2)[0]
+    for t, node in enumerate(nodes):
+        lab, st, _, _ = o.label(V, [node], d[node])
+        assert lab[0] == 0 and st[0] == d[node]
+        lab, st, _, _ = o.label(V, [node], d[node] - 1)
+        assert lab[0] == -1 and st[0] == d[node] - 1
+
+
+# ---------------------------------------------------------------------------
+# P19  the sub-domain solve (ISA step 3, R10): nodes outside S_k are ghosts holding
+#      v_out — a target node of another piece outside S_k included — and every target
+#      node inside S_k keeps g.  On the lattice the restricted solution is the BFS
+#      distance through S_k's nodes only: V = 1 - beta^d_S, V = 1 where no path exists.
+# ---------------------------------------------------------------------------
+def bfs_restricted(shape, targets, allowed):
+    d = bfs_distance(shape, targets & allowed)
+    ny, nx = shape
+    # re-run on the allowed nodes only (a plain BFS that never enters a ghost node)
+    d = np.full(shape, -1, np.int64)
+    q = collections.deque()
+    for j, i in zip(*np.nonzero(targets & allowed)):
+        d[j, i] = 0
+        q.append((j, i))
+    while q:
+        j, i = q.popleft()
+        for dj, di in ((1, 0), (-1, 0), (0, 1), (0, -1)):
+            a, b = j + dj, i + di
+            if 0 <= a < ny and 0 <= b < nx and allowed[a, b] and d[a, b] < 0:
+                d[a, b] = d[j, i] + 1
+                q.append((a, b))
+    return d
+
+
+def test_p19_subdomain_ghosts_and_targets():
+    nx, ny = 12, 8
+    grid = W.Grid((nx, ny), (0.0, 0.0), (1.1, 0.7), (False, False))
+    piece = np.full((ny, nx), -1, np.int8)
+    piece[1, 1] = 0                 # piece 0 inside S_0
+    piece[6, 2] = 1                 # piece 1 inside S_0: keeps g = 0
+    piece[2, 9] = 1                 # piece 1 outside S_0: a ghost of S_0
+    allowed = np.ones((ny, nx), bool)
+    allowed[:, 7] = False           # a wall column ...
+    allowed[5, 7] = True            # ... with one gap
+    allowed[2, 8:] = False          # and the far piece-1 node's row cut off
+    allowed[2, 9] = False
+    mask = allowed.reshape(-1).astype(np.uint32)     # bit 0 = S_0
+    mask[piece.reshape(-1) == 1] |= 2
+    p = mk_problem(grid, W.axis_controls(), piece.reshape(-1), tol=1e-14)
+    o = oracle.OracleProblem(p)
+    V, it, _ = o.solve_subdomain(mask, 0)
+    d = bfs_restricted((ny, nx), piece >= 0, allowed).reshape(-1)
+    beta = 1.0 / (1.0 + p.h)
+    exp = np.where(d >= 0, 1.0 - beta ** np.maximum(d, 0), 1.0)
+    np.testing.assert_allclose(V, exp, rtol=0, atol=1e-13)
+    assert V[2 * nx + 9] == p.v_out and V[6 * nx + 2] == 0.0
+
+
+# ---------------------------------------------------------------------------
+# P20  RA step 3 ("if |V_i(j) - V(j)| <= 2(C dx^q + M dx)"): the
+#      comparison includes equality, and the piece's own nodes are always in its set.
+# ---------------------------------------------------------------------------
+def test_p20_ra_threshold_inclusive():
+    V = np.array([0.0, 0.0, 0.5, 0.25, 0.75])
+    V0 = np.array([0.25, 0.25 + 2 ** -40, 0.25, 0.25, 0.25])   # |.| = thr, > thr, thr, 0, thr
+    V1 = np.array([1.0, 1.0, 1.0, 1.0, 0.75])
+    piece = np.array([-1, -1, -1, 1, -1], np.int8)
+    mask = oracle.ra_masks([V0, V1], V, piece, 0.25)
+    assert list(mask & 1) == [1, 0, 1, 1, 0]
+    assert list((mask >> 1) & 1) == [0, 0, 0, 1, 1]
+
+
+# ---------------------------------------------------------------------------
+# P21  the box tolerance of R3 only decides feet that lie ON the box in exact
+#      arithmetic: on every edge node of a unit-circle control problem, the brackets
+#      with the tabulated controls (cos(pi/2) = 6e-17 ...) equal the brackets with the
+#      controls' exact-zero components snapped to 0, and every foot that is outside
+#      the box in exact arithmetic reads v_out.
+# ---------------------------------------------------------------------------
+def test_p21_box_tolerance_only_moves_exact_box_feet():
+    n = 17
+    grid = W.Grid((n, n), (-1.0, -1.0), (1.0, 1.0), (False, False))
+    piece = np.full(grid.size, -1, np.int8)
+    piece[n * (n // 2) + n // 2] = 0
+    ctrl = W.unit_circle_controls(16)
+    snapped = np.where(np.abs(ctrl) < 1e-12, 0.0, ctrl)
+    assert np.any((ctrl != snapped))
+    p = mk_problem(grid, ctrl, piece)
+    ps = mk_problem(grid, snapped, piece)
+    o, os_ = oracle.OracleProblem(p), oracle.OracleProblem(ps)
+    V = np.random.default_rng(21).uniform(0, 0.5, grid.size)
+    beta = o.beta()
+    for idx in range(grid.size):
+        i, j = idx % n, idx // n
+        if 0 < i < n - 1 and 0 < j < n - 1:
+            continue
+        for k in range(16):
+            b, bs = o.bracket(V, [i, j], k), os_.bracket(V, [i, j], k)
+            assert abs(b - bs) <= 1e-15, (i, j, k)     # (a 6e-17 weight moves 1 ulp)
+            foot = np.array([i, j]) + snapped[k, :2]     # h = dx: one cell per unit
+            if np.any(foot < 0) or np.any(foot > n - 1):
+                assert b == beta * p.v_out + (1 - beta)
