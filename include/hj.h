@@ -227,7 +227,13 @@ hj_status hj_coarse_feedback(const hj_grid *grid, const hj_problem *prob,
  * fine_grid      nested fine grid: (n_f - 1) = R (n_c - 1), or n_f = R n_c periodic
  * ratio[3]       R per axis (1 for unused axes); band >= 0 in fine cells
  * m              number of target pieces / sub-domains, 1..32
- * fine_piece     device int8[N_f] target pieces on the fine grid
+ * fine_piece     device int8[N_f] target pieces on the fine grid; piece values must
+ *                lie in [-1, m): a piece >= m (not checked on the device) belongs to
+ *                no sub-domain bit
+ * The trajectory's own arithmetic (x(y_s), the speed at y_s, f, y_s + h f / dx) is
+ * evaluated with every operation rounded separately in the recursion's left-to-right
+ * order, so the positions depend only on the controls taken (R8/R11); an
+ * all-NaN bracket set (a NaN in Vc) ends the trajectory unlabelled (-1).
  * Outputs (device): label int32[N_c]; margin double[N_c] = min control margin
  *     along the trajectory; geo double[N_c] = min distance (index units) of a
  *     rounding / box decision to its threshold; steps int32[N_c];

@@ -98,6 +98,8 @@ def _load():
             lib.or_classes.argtypes = [P, _up, ctypes.c_int, _bp]
             lib.or_apply_T.argtypes = [P, _bp, _dp, _dp]
             lib.or_apply_T.restype = ctypes.c_double
+            lib.or_apply_T_range.argtypes = [P, _bp, _dp, _dp, ctypes.c_long, ctypes.c_long]
+            lib.or_apply_T_range.restype = ctypes.c_double
             lib.or_initial.argtypes = [P, _bp, _dp]
             lib.or_value_iteration.argtypes = [P, _bp, _dp, ctypes.c_double, ctypes.c_long, _dp]
             lib.or_value_iteration.restype = ctypes.c_long
@@ -205,6 +207,13 @@ class OracleProblem:
         out = np.empty_like(V)
         res = self.lib.or_apply_T(self.ref, _ptr(cls, _bp), _ptr(V, _dp), _ptr(out, _dp))
         return out, res
+
+    def apply_T_rows(self, V, cls, out, row0, row1):
+        """T(V) on the node rows [row0, row1) of axis 1 only (written into `out`); for
+        timing the oracle on a bounded sample.  Returns the sup-norm change there."""
+        n0 = self.prob.grid.n[0]
+        return self.lib.or_apply_T_range(self.ref, _ptr(cls, _bp), _ptr(V, _dp), _ptr(out, _dp),
+                                         int(row0 * n0), int(row1 * n0))
 
     def initial(self, cls=None):
         cls = self.classes() if cls is None else np.ascontiguousarray(cls, np.int8)

@@ -215,14 +215,16 @@ void or_classes(const or_problem *p, const unsigned int *mask, int k, signed cha
     }
 }
 
-/* One Jacobi application V_new = T(V) (PAPER.md eq. (SL) line 235 / (Tdef)). */
-double or_apply_T(const or_problem *p, const signed char *cls, const double *V, double *Vn) {
-    long N = or_size(p);
+/* One Jacobi application V_new = T(V) (PAPER.md eq. (SL) line 235 / (Tdef)) on the nodes
+ * [lo, hi) of the flat index (the whole grid in or_apply_T; a bounded sample of rows for
+ * bench.py's timing of the oracle).  Returns the sup-norm change on those nodes. */
+double or_apply_T_range(const or_problem *p, const signed char *cls, const double *V,
+                        double *Vn, long lo, long hi) {
     double res = 0.0;
     /* every node is computed independently from V (Jacobi) and max is exact, so the
      * result does not depend on the thread count */
 #pragma omp parallel for schedule(static) reduction(max : res)
-    for (long idx = 0; idx < N; ++idx) {
+    for (long idx = lo; idx < hi; ++idx) {
         double v;
         if (cls[idx] == OR_GHOST) {
             v = p->v_out;
@@ -240,6 +242,10 @@ double or_apply_T(const or_problem *p, const signed char *cls, const double *V, 
         if (dv > res) res = dv;
     }
     return res;
+}
+
+double or_apply_T(const or_problem *p, const signed char *cls, const double *V, double *Vn) {
+    return or_apply_T_range(p, cls, V, Vn, 0, or_size(p));
 }
 
 /* V^0: g on target nodes, v_out elsewhere (R6). */

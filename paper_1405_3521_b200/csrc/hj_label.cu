@@ -268,6 +268,84 @@ __device__ __forceinline__ BestPair thread_bracket(const DevProblem<double, Ts> 
     return r;
 }
 
+// The trajectory's own arithmetic — the state x(y_s), the speed c(y_s), f(y_s, a) and the
+// step y_{s+1} = y_s + h f / dx (R8) — in the plain left-to-right order of the recursion,
+// every product and sum rounded on its own (no contraction).  The positions, and so every
+// nearest-node and box decision, are then a function of the argmins alone: any IEEE fp64
+// evaluation of the same recursion that takes the same controls lands on the same bits
+// (only the Dubins car's cos/sin may differ by an ulp between libraries).  The brackets,
+// which only pick the control, keep their fused form.
+__device__ __forceinline__ double rn_add(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double rn_mul(double a, double b) { return __dmul_rn(a, b); }
+
+// multilinear interpolation of a whole-grid node field at index point g: corner weights
+// prod_d (w_d or 1 - w_d) accumulated corner by corner (corner bit d = upper node on d)
+template <typename Ts, int DIM>
+__device__ double traj_interp(const DevProblem<double, Ts> &P, const Ts *__restrict__ F,
+                              const double g[3], double outside) {
+    int64_t i0[3] = {0, 0, 0}, i1[3] = {0, 0, 0};
+    double w[3] = {0, 0, 0};
+#pragma unroll
+    for (int d = 0; d < DIM; ++d) {
+        double x = g[d];
+        const int64_t n = P.n[d];
+        if (P.periodic[d]) {
+            const double f = floor(x);
+            w[d] = __dsub_rn(x, f);
+            int64_t c = (int64_t)f % n;
+            if (c < 0) c += n;
+            i0[d] = c;
+            i1[d] = (c + 1) % n;
+        } else {
+            const double hi = (double)(n - 1);
+            if (x < -(double)BOX_EPS || x > hi + (double)BOX_EPS) return outside;
+            x = x < 0.0 ? 0.0 : (x > hi ? hi : x);
+            int64_t c = (int64_t)floor(x);
+            if (c > n - 2) c = n - 2;
+            w[d] = __dsub_rn(x, (double)c);
+            i0[d] = c;
+            i1[d] = c + 1;
+        }
+    }
+    double acc = 0.0;
+#pragma unroll
+    for (int corner = 0; corner < (1 << DIM); ++corner) {
+        int64_t idx = 0;
+        double wt = 1.0;
+#pragma unroll
+        for (int d = DIM - 1; d >= 0; --d) idx = idx * P.n[d] + ((corner >> d) & 1 ? i1[d] : i0[d]);
+#pragma unroll
+        for (int d = 0; d < DIM; ++d)
+            wt = rn_mul(wt, (corner >> d) & 1 ? w[d] : __dsub_rn(1.0, w[d]));
+        acc = rn_add(acc, rn_mul(wt, (double)F[idx]));
+    }
+    return acc;
+}
+
+// f(x, a) with the control's components u (§2 line 36; DESIGN.md configs)
+template <typename Ts>
+__device__ __forceinline__ void traj_dynamics(const DevProblem<double, Ts> &P, const double x[3],
+                                              double c, const double *u, double f[3], double ct,
+                                              double st) {
+    f[0] = f[1] = f[2] = 0.0;
+    if (P.dyn == HJ_DYN_AFFINE) {
+        for (int d = 0; d < P.dim; ++d) {
+            double s = rn_add(rn_mul(c, u[d]), P.b[d]);
+            for (int e = 0; e < P.dim; ++e) s = rn_add(s, rn_mul(P.A[3 * d + e], x[e]));
+            f[d] = s;
+        }
+    } else if (P.dyn == HJ_DYN_DUBINS) {
+        f[0] = rn_mul(P.dub_v, ct);
+        f[1] = rn_mul(P.dub_v, st);
+        f[2] = rn_mul(P.dub_w, u[0]);
+    } else {
+        f[0] = x[1];
+        f[1] = rn_add(__dsub_rn(rn_mul(rn_mul(P.vdp_mu, __dsub_rn(1.0, rn_mul(x[0], x[0]))), x[1]),
+                                x[0]),
+                      u[0]);
+    }
+}
+
 // THREAD: one thread per coarse node (small control sets), else one warp per node.
 template <typename Ts, int DIM, bool THREAD = false>
 __global__ void __launch_bounds__(256)
@@ -319,12 +397,9 @@ __global__ void __launch_bounds__(256)
             if (s >= n_max) break;
             double x[3] = {0, 0, 0};
 #pragma unroll
-            for (int d = 0; d < DIM; ++d) x[d] = fma(g[d], P.dx[d], P.lo[d]);
-            const int64_t zero[3] = {0, 0, 0};
+            for (int d = 0; d < DIM; ++d) x[d] = rn_add(P.lo[d], rn_mul(g[d], P.dx[d]));
             double cs = 1.0;
-            if (P.speed && P.dyn == HJ_DYN_AFFINE)
-                cs = fast2 ? interp2_grid<Ts>(P.speed, (int)P.n[0], (int)P.n[1], g[0], g[1], 1.0)
-                           : interp<double, Ts, DIM>(P.speed, o, vn, P.n, P.periodic, zero, g, 1.0);
+            if (P.speed && P.dyn == HJ_DYN_AFFINE) cs = traj_interp<Ts, DIM>(P, P.speed, g, 1.0);
             double ct = 0.0, st = 0.0;
             if (P.dyn == HJ_DYN_DUBINS) {
                 ct = cos(x[2]);
@@ -337,16 +412,17 @@ __global__ void __launch_bounds__(256)
                 bp = fast2 ? lane_bracket_2d<Ts>(P, V, g, x, cs, lane, uctl)
                            : lane_bracket<Ts, DIM>(P, V, o, vn, g, lane, uctl, ct, st);
             const int a = bp.arg;
+            if (a < 0) break;        // every bracket NaN (a NaN in V): no control, unlabelled
             mm = fmin(mm, bp.second - bp.best);
             double f[3];
-            dynamics_u(P, x, cs, uctl[a], f, ct, st);
+            traj_dynamics(P, x, cs, uctl[a], f, ct, st);
             bool out = false;
 #pragma unroll
             for (int d = 0; d < DIM; ++d) {
-                g[d] = fma(P.hdx[d], f[d], g[d]);
+                g[d] = rn_add(g[d], __ddiv_rn(rn_mul(P.h, f[d]), P.dx[d]));
                 if (P.periodic[d]) {
-                    double n = (double)P.n[d];
-                    g[d] = g[d] - n * floor(g[d] / n);
+                    const double n = (double)P.n[d];
+                    g[d] = __dsub_rn(g[d], rn_mul(n, floor(__ddiv_rn(g[d], n))));
                 } else {
                     double hi = (double)(P.n[d] - 1);
                     mg = fmin(mg, fmin(fabs(g[d]), fabs(hi - g[d])));
@@ -418,11 +494,11 @@ __global__ void k_prolong(const ProlongArgs A, const void *__restrict__ coarse,
                         bits |= cmask[cidx];
                     } else {
                         const int32_t l = lab[cidx];
-                        bits |= (l < 0) ? A.all : (1u << l);
+                        bits |= (l < 0) ? A.all : (l < 32 ? (1u << l) : 0u);
                     }
                 }
         int8_t p = fine_piece[t];
-        if (p >= 0) bits |= 1u << p;
+        if (p >= 0 && p < 32) bits |= 1u << p;
         mask[t] = bits & A.all;
     }
 }
@@ -473,7 +549,7 @@ __global__ void __launch_bounds__(256)
                         b |= cmask[cidx];
                     } else {
                         const int32_t l = lab[cidx];
-                        b |= (l < 0) ? A.all : (1u << l);
+                        b |= (l < 0) ? A.all : (l < 32 ? (1u << l) : 0u);
                     }
                 }
             }
@@ -491,7 +567,7 @@ __global__ void __launch_bounds__(256)
             }
             const int64_t t = i0 + A.nf[0] * (i12[0] + A.nf[1] * i12[1]);
             const int8_t p = fine_piece[t];
-            if (p >= 0) bits |= 1u << p;
+            if (p >= 0 && p < 32) bits |= 1u << p;
             mask[t] = bits & A.all;
         }
     }

@@ -419,7 +419,7 @@ static hj_status solve_impl(const hj_grid &grid, const hj_problem &prob, const h
     HJ_CUDA(cudaStreamSynchronize(s));
     const unsigned long long interior = counts[0];
     if (rep) {
-        rep->evaluated_updates = (int64_t)counts[1] * prob.n_controls;
+        rep->evaluated_updates = (int64_t)counts[1] * L.evals;
         rep->iterations = it;
         rep->residual = r.resid[0];
         rep->converged = r.converged[0];
@@ -582,7 +582,7 @@ static hj_status partitioned_impl(const hj_grid &grid, const hj_problem &prob,
             rp.residual = r.resid[q];
             rp.converged = r.converged[q];
             rp.node_updates = (int64_t)interior[q] * prob.n_controls * r.iters[q];
-            rp.evaluated_updates = (int64_t)interior[m + q] * prob.n_controls;
+            rp.evaluated_updates = (int64_t)interior[m + q] * SL.evals;
             rp.device_ms = r.ms;
             rp.launches = q == 0 ? r.launches + nv + 3 + (f.speed ? 1 : 0) : 0;  // counted once
         }

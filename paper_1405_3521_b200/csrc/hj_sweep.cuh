@@ -805,6 +805,8 @@ struct SweepLaunch {
     int64_t total_tiles = 0;
     SweepGroup<T> *d_group = nullptr;   // device copy (inside the caller's workspace)
     LocalCtrl<T> ctrl;
+    int evals = 0;                      // brackets evaluated per interior node and sweep
+                                        // (the control count unless a kernel prunes)
 };
 
 // bytes of change flags a view needs under the smallest tiling (32 x 8 x 1)
@@ -886,12 +888,25 @@ __global__ void k_wl_live(const SweepGroup<T> *__restrict__ G) {
 
 // Persistent grid of a work-list kernel: resident CTAs (occupancy x SMs), capped by
 // the number of tiles.
+// the current device and its SM count (per-device caches: a process may drive several)
+static inline int current_device() {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) dev = 0;
+    return dev;
+}
+static inline int device_sms() {
+    static int sms[64] = {0};
+    const int dev = current_device();
+    if (!sms[dev] &&
+        cudaDeviceGetAttribute(&sms[dev], cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+        sms[dev] = 148;
+    return sms[dev];
+}
+
 template <typename K>
 static unsigned grid_for(K kernel, int threads, size_t smem, int64_t total, bool dense = false) {
     (void)dense;   // dense mode walks the live list too (persistent grid)
-    static int sms = 0;
-    if (!sms && cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0) != cudaSuccess)
-        sms = 148;
+    const int sms = device_sms();
     int per_sm = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem) !=
             cudaSuccess ||
@@ -1040,6 +1055,20 @@ hj_status sweep_prepare(const hj_grid &g, const hj_problem &p, const hj_fields &
     if (L.kind == SWEEP_DUBINS && H[0] <= 1.0 && H[1] <= 1.0 &&
         (want == HJ_SWEEP_AUTO || want == HJ_SWEEP_DUBINS_COOP))
         L.coop = true;         // (x, y) feet within one cell: the cooperative kernel
+    L.evals = p.n_controls;
+    if (L.kind == SWEEP_DUBINS && L.coop && p.cost == HJ_COST_KRUZKOV) {
+        // coop_eval_dubins evaluates only each heading-sign group's extreme |d_k|
+        double e[4] = {INFINITY, -INFINITY, INFINITY, -INFINITY};
+        for (int k = 0; k < p.n_controls; ++k) {
+            const double dk = p.controls[k][0], w = std::fabs(dk);
+            const int o = dk < 0 ? 2 : 0;
+            e[o] = std::min(e[o], w);
+            e[o + 1] = std::max(e[o + 1], w);
+        }
+        L.evals = 0;
+        for (int o = 0; o < 4; o += 2)
+            if (e[o] <= e[o + 1]) L.evals += e[o] == e[o + 1] ? 1 : 2;
+    }
     if (want == HJ_SWEEP_DUBINS_COOP && !(L.kind == SWEEP_DUBINS && L.coop)) {
         set_error("sweep_kernel %d requested, but the problem does not qualify for it "
                   "(Dubins, feet within one cell)", want);
@@ -1175,12 +1204,13 @@ static void launch_local(const DevProblem<T, T> &P, const SweepLaunch<T> &L, int
 template <typename T, int KQ, bool PC>
 static void launch_tb_kq(const DevProblem<T, T> &P, const SweepLaunch<T> &L, int64_t n0, int S_run,
                          int rerun, double tol, cudaStream_t s) {
-    static bool attr = false;   // opt in to > 48 KB dynamic shared memory (fp64) once
+    static bool attr[64] = {false};   // opt in to > 48 KB dynamic shared memory, per device
     const size_t smem = sizeof(TBSmem<T>);
-    if (!attr) {
+    const int dev = current_device();
+    if (!attr[dev]) {
         cudaFuncSetAttribute(k_sweep_local2d_tb<T, KQ, PC>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        attr = true;
+        attr[dev] = true;
     }
     k_sweep_local2d_tb<T, KQ, PC><<<grid_for(k_sweep_local2d_tb<T, KQ, PC>, 256, smem,
                                              L.total_tiles),
@@ -1289,12 +1319,14 @@ static hj_status launch_coop_kq(const DevProblem<T, T> &P, const SweepLaunch<T> 
             return HJ_OK;
         }
     }
-    static int grid = 0;
+    static int grids[64] = {0};        // resident grid, per device
+    const int dev = current_device();
+    int &grid = grids[dev];
     if (!grid) {
         cudaFuncSetAttribute(k_sweep_local2d_coop<T, KQ, PC, EV>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
-        int sms = 148, per_sm = 0;
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+        const int sms = device_sms();
+        int per_sm = 0;
         if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sweep_local2d_coop<T, KQ, PC, EV>,
                                                           CoopNW<T>::nw * 32, dyn) != cudaSuccess ||
             per_sm < 1)

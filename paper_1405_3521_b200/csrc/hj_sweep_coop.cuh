@@ -621,10 +621,12 @@ __global__ void __launch_bounds__(CoopNW<T>::nw * 32, CoopNW<T>::minb)
     }
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if (threadIdx.x < (unsigned)S.n_views) sview[threadIdx.x] = G->v[threadIdx.x];
-    if (EV == 0 && threadIdx.x < 12u * KQ) {
-        const int w = threadIdx.x / (4 * KQ), q = (threadIdx.x / KQ) % 4, k = threadIdx.x % KQ;
-        sctl[threadIdx.x] = w == 0 ? C.ax[q][k] : w == 1 ? C.ay[q][k] : C.ck[q][k];
-    }
+    // (strided: 12 KQ entries can exceed the block — fp64 runs 256 threads, KQ up to 32)
+    if (EV == 0)
+        for (int i = threadIdx.x; i < 12 * KQ; i += blockDim.x) {
+            const int w = i / (4 * KQ), q = (i / KQ) % 4, k = i % KQ;
+            sctl[i] = w == 0 ? C.ax[q][k] : w == 1 ? C.ay[q][k] : C.ck[q][k];
+        }
     const bool mono = P.monotone != 0;
     const bool kruz = P.cost == HJ_COST_KRUZKOV;
     const T beta = P.beta, v_out = P.v_out;

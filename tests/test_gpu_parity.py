@@ -19,7 +19,32 @@ if not torch.cuda.is_available():  # pragma: no cover - CPU container
 from paper_1405_3521_b200 import hj, pipeline  # noqa: E402
 
 TOL = {"f32": 1e-5, "f64": 1e-10}
-TIE = 1e-9
+TIE = 1e-9          # north_star: labels bit-exact where the oracle's control margin > 1e-9
+GEO_TIE = 1e-12     # R11: Dubins positions go through cos/sin (libm vs CUDA may differ by
+                    # an ulp): a rounding/box decision that close to its threshold is a tie
+# upper bounds on the fraction of margin-tie coarse nodes (measured with the oracle at the
+# test sizes, R11): exact ties of the discrete problem, e.g. trajectories
+# crossing regions where every foot leaves the box (all brackets = beta v_out + c)
+MAX_TIE_FRAC = {1: 0.12, 2: 0.06, 3: 0.12, 4: 0.45, 5: 0.02}
+
+
+def compare_labels(tie_report, what, idx, lab, lab_o, mar_o, geo_o, steps=None, steps_o=None):
+    """Bit-exact labels (and step counts) wherever the oracle's decision is not a tie;
+    the ties are counted, reported (terminal summary) and bounded."""
+    margin_tie = mar_o <= TIE
+    geo_tie = (~margin_tie) & (geo_o <= GEO_TIE) if idx == 4 else np.zeros_like(margin_tie)
+    clear = ~(margin_tie | geo_tie)
+    bad = np.nonzero(lab[clear] != lab_o[clear])[0]
+    assert len(bad) == 0, (what, len(bad), np.nonzero(clear)[0][bad[:10]])
+    if steps is not None:
+        assert np.array_equal(steps[clear], steps_o[clear]), what
+    n = len(lab)
+    tie_report.append(f"config {idx} {what}: {int(clear.sum())}/{n} labels bit-exact; "
+                      f"{int(margin_tie.sum())} margin ties (GPU label differs at "
+                      f"{int((lab[margin_tie] != lab_o[margin_tie]).sum())}); "
+                      f"{int(geo_tie.sum())} Dubins rounding ties")
+    assert margin_tie.mean() <= MAX_TIE_FRAC[idx], (what, margin_tie.mean())
+    return clear
 
 # reduced sizes the oracle finishes in seconds; several tiles and ragged tails.
 # (scale, fine/coarse ratio): small fine grids need a finer coarse grid.
@@ -202,7 +227,7 @@ def test_feedback_bitexact(idx, oracle_cache):
 
 
 @pytest.mark.parametrize("idx", [1, 2, 3, 4, 5])
-def test_labels_and_prolongation_bitexact(idx, oracle_cache):
+def test_labels_and_prolongation_bitexact(idx, oracle_cache, tie_report):
     cfg = _cfg(idx)
     Vc, _, _ = _oracle_solve(oracle_cache, idx, "coarse")
     coarse = hj.DeviceProblem(cfg.coarse, "f64")
@@ -212,20 +237,16 @@ def test_labels_and_prolongation_bitexact(idx, oracle_cache):
     oc = oracle.OracleProblem(cfg.coarse)
     lab_o, st_o, mar_o, geo_o = oc.label(Vc, np.arange(oc.N), cfg.n_max_steps)
     lab = out["label"].cpu().numpy()
-    clear = (mar_o > TIE) & (geo_o > TIE)
-    assert np.array_equal(lab[clear], lab_o[clear])
-    assert np.array_equal(out["steps"].cpu().numpy()[clear], st_o[clear])
-    ties = int((~clear).sum())
-    print(f"config {idx}: {ties} tie nodes of {oc.N}, label mismatches there: "
-          f"{int((lab[~clear] != lab_o[~clear]).sum())}")
+    compare_labels(tie_report, "reduced, f64, oracle Vc", idx, lab, lab_o, mar_o, geo_o,
+                   out["steps"].cpu().numpy(), st_o)
     # prolongation (ISA step 2) of the GPU labels: bit-exact
     mask_o = oracle.prolong(cfg.coarse.grid, cfg.fine.grid, cfg.ratio, cfg.band, lab, cfg.m,
                             cfg.fine.piece)
     assert np.array_equal(out["mask"].cpu().numpy().view(np.uint32), mask_o)
 
 
-@pytest.mark.parametrize("idx,dtype", [(1, "f64"), (1, "f32"), (2, "f32"), (4, "f32"),
-                                       (5, "f32")])
+@pytest.mark.parametrize("idx,dtype", [(1, "f64"), (1, "f32"), (2, "f32"), (3, "f32"),
+                                       (3, "f64"), (4, "f32"), (5, "f32")])
 def test_partitioned_matches_oracle(idx, dtype):
     """ISA steps 3-4 on the GPU mask vs the oracle's masked solves + assembly."""
     cfg = _cfg(idx)
@@ -367,34 +388,110 @@ def _sampled_residual(prob, V, n_samples, seed):
 
 
 @pytest.mark.parametrize("idx", [2])
-def test_full_size_solve_and_labels(idx):
+def test_full_size_sampled_fixed_point(idx):
+    """Full BASELINE size, the launch configuration bench.py times: the assembled field
+    is a fixed point of T at sampled nodes (stopping rule + fp32 rounding), lies in the
+    Kruzkov range, and agrees with the whole-grid solve up to O(dx) (Prop. 4.1)."""
     cfg = W.make(idx)
     fine = hj.DeviceProblem(cfg.fine, cfg.dtype)
     res = pipeline.run_isa(cfg, cfg.dtype, fine=fine)
     Vbar = res["V"].double().cpu().numpy()
     assert Vbar.min() >= 0.0 and Vbar.max() <= 1.0
-    # fixed point of T at sampled nodes (stopping rule + fp32 rounding)
     worst = _sampled_residual(cfg.fine, Vbar, 300, 7)
     assert worst <= cfg.fine.tol + 2e-6, worst
-    # whole-grid solve agrees with the assembled one up to O(dx) (Prop. 4.1), never above
     V, rep = hj.hj_solve(fine)
     diff = Vbar - V.double().cpu().numpy()
     assert diff.min() >= -1e-5
     assert diff.max() <= 2 * cfg.fine.grid.spacing(0)
     assert (np.abs(diff) > 1e-5).mean() < 0.02
-    # sampled coarse labels against the oracle's trajectories on the same coarse V
-    Vc = res["Vc"].double().cpu().numpy()
-    oc = oracle.OracleProblem(cfg.coarse)
-    rng = np.random.default_rng(3)
-    nodes = rng.choice(oc.N, 500, replace=False)
-    lab_o, _, mar_o, geo_o = oc.label(Vc, nodes, cfg.n_max_steps)
-    lab = res["labels"]["label"].cpu().numpy()[nodes]
-    clear = (mar_o > TIE) & (geo_o > TIE)
-    assert np.array_equal(lab[clear], lab_o[clear])
-    # prolongation of all coarse labels: bit-exact on the full fine grid
     mask_o = oracle.prolong(cfg.coarse.grid, cfg.fine.grid, cfg.ratio, cfg.band,
                             res["labels"]["label"].cpu().numpy(), cfg.m, cfg.fine.piece)
     assert np.array_equal(res["mask"].cpu().numpy().view(np.uint32), mask_o)
+
+
+def _speed_as(prob, dtype):
+    """The problem with its speed field rounded to the GPU storage dtype (the oracle then
+    sees exactly the node values the GPU path reads)."""
+    import dataclasses
+    if prob.speed is None or dtype == "f64":
+        return prob
+    return dataclasses.replace(prob, speed=np.asarray(prob.speed, np.float32).astype(np.float64))
+
+
+@pytest.mark.parametrize("idx", [2, 3, 4, 5])
+def test_full_size_coarse_solve_and_labels(idx, tie_report):
+    """The whole coarse stage at the BASELINE coarse size, independently on both sides:
+    (a) fp64: the GPU's coarse value iteration vs the oracle's from scratch (<= 1e-10,
+        same iteration count), and the GPU's labels on its own Vc vs the oracle's labels on
+        its own Vc (bit-exact at every non-tie node);
+    (b) the product path (fp32 Vc, the bench's launch configuration): the GPU labels vs the
+        oracle's trajectories on the same fp32 values (bit-exact at every non-tie node),
+        and the prolongation of all labels to the full fine grid (bit-exact)."""
+    cfg = W.make(idx)
+    oc = oracle.OracleProblem(cfg.coarse)
+    Vo, it_o, _ = oc.solve()
+    lab_o, st_o, mar_o, geo_o = oc.label(Vo, np.arange(oc.N), cfg.n_max_steps)
+    coarse = hj.DeviceProblem(cfg.coarse, "f64")
+    fine = hj.DeviceProblem(cfg.fine, "f64")
+    Vg, rep = hj.hj_solve(coarse)
+    assert np.abs(Vg.cpu().numpy() - Vo).max() <= TOL["f64"]
+    assert rep["iterations"] == it_o
+    out = hj.hj_label_subdomains(coarse, Vg, cfg.n_max_steps, fine, cfg.ratio, cfg.band, cfg.m)
+    compare_labels(tie_report, "full coarse, f64, independent", idx,
+                   out["label"].cpu().numpy(), lab_o, mar_o, geo_o,
+                   out["steps"].cpu().numpy(), st_o)
+    # (b) product dtype
+    dt = cfg.dtype
+    coarse32 = hj.DeviceProblem(cfg.coarse, dt)
+    fine32 = hj.DeviceProblem(cfg.fine, dt)
+    Vc32, _ = hj.hj_solve(coarse32)
+    assert np.abs(Vc32.double().cpu().numpy() - Vo).max() <= TOL[dt]
+    out32 = hj.hj_label_subdomains(coarse32, Vc32, cfg.n_max_steps, fine32, cfg.ratio, cfg.band,
+                                   cfg.m)
+    oc32 = oracle.OracleProblem(_speed_as(cfg.coarse, dt))
+    Vc32h = Vc32.double().cpu().numpy()
+    l32, s32, m32, g32 = oc32.label(Vc32h, np.arange(oc.N), cfg.n_max_steps)
+    lab32 = out32["label"].cpu().numpy()
+    compare_labels(tie_report, f"full coarse, {dt} product path, same Vc", idx, lab32, l32, m32,
+                   g32, out32["steps"].cpu().numpy(), s32)
+    mask_o = oracle.prolong(cfg.coarse.grid, cfg.fine.grid, cfg.ratio, cfg.band, lab32, cfg.m,
+                            cfg.fine.piece)
+    assert np.array_equal(out32["mask"].cpu().numpy().view(np.uint32), mask_o)
+
+
+@pytest.mark.parametrize("idx", [1, 2, 3, 4, 5])
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_isa_end_to_end_independent(idx, dtype, tie_report):
+    """The whole hot path on both sides from the same seeded inputs and nothing else: the
+    oracle's ISA pass (coarse solve -> labels -> prolongation -> masked solves -> min
+    assembly) against the GPU's run_isa.  Where the two sub-domain sets coincide the
+    assembled fields agree to the value tolerance; where a tie node took another label the
+    GPU's result must still be a valid ISA result (Prop. 4.1): never
+    below the whole-grid solution by more than the tolerance, and above it by at most the
+    scheme's O(dx)."""
+    cfg = _cfg(idx)
+    if dtype == "f32":
+        cfg.fine.tol = max(cfg.fine.tol, 1e-7)
+        cfg.coarse.tol = max(cfg.coarse.tol, 1e-7)
+        cfg.fine = _speed_as(cfg.fine, "f32")
+        cfg.coarse = _speed_as(cfg.coarse, "f32")
+    ref = oracle.isa(cfg.fine, cfg.coarse, cfg.ratio, cfg.band, cfg.m, cfg.n_max_steps)
+    res = pipeline.run_isa(cfg, dtype)
+    Vbar = res["V"].double().cpu().numpy()
+    mask = res["mask"].cpu().numpy().view(np.uint32)
+    same = np.array_equal(mask, ref["mask"])
+    err = np.abs(Vbar - ref["Vbar"]).max()
+    lab = res["labels"]["label"].cpu().numpy()
+    tie_report.append(f"config {idx} end-to-end {dtype}: coarse labels differing "
+                      f"{int((lab != ref['labels']).sum())}/{len(lab)}, masks "
+                      f"{'identical' if same else 'differ'}, max|Vbar - oracle Vbar| = {err:.2e}")
+    if same:
+        assert err <= TOL[dtype], (idx, dtype, err)
+    else:
+        Vw, _, _ = oracle.OracleProblem(cfg.fine).solve()
+        diff = Vbar - Vw
+        assert diff.min() >= -TOL[dtype] - 10 * cfg.fine.tol, diff.min()
+        assert diff.max() <= 2 * max(cfg.coarse.grid.spacing(d) for d in range(cfg.fine.grid.dim))
 
 
 # ---------------------------------------------------------------------------
