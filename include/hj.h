@@ -90,7 +90,10 @@ enum { HJ_COST_KRUZKOV = 0, HJ_COST_DISCOUNTED = 1 };
  * blocked in shared memory) — FFMA2-packed for fp32, bit-identical iterates to the
  * one-sweep LOCAL_PACKED (fp32 only) / LOCAL_SCALAR kernels; FIELD_COOP for any other 2-D
  * affine / Van der Pol problem whose feet stay within one cell (the same cooperative
- * scheme, the foot's cell picked by the signs of its offsets); FIELD2D for the other 2-D
+ * scheme, the foot's cell picked by the signs of its offsets); FIELD_COL for the other 2-D
+ * affine problems without a speed field whose controls share their axis-0 component
+ * (config 5: one x-interpolated column per node, walked once over the controls sorted by
+ * their axis-1 component — bit-identical iterates to FIELD2D); FIELD2D for the other 2-D
  * affine / Van der Pol problems without periodic axes; DUBINS_COOP (the cooperative
  * scheme on 8x8 mini-tiles of each heading plane) for Dubins problems whose (x, y) and
  * heading steps stay within one cell; DUBINS for Dubins dynamics whose heading step is <= 1 cell; GENERIC
@@ -99,7 +102,7 @@ enum { HJ_COST_KRUZKOV = 0, HJ_COST_DISCOUNTED = 1 };
 enum { HJ_SWEEP_AUTO = 0, HJ_SWEEP_GENERIC = 1, HJ_SWEEP_LOCAL_SCALAR = 2,
        HJ_SWEEP_LOCAL_PACKED = 3, HJ_SWEEP_FIELD2D = 4, HJ_SWEEP_DUBINS = 5,
        HJ_SWEEP_LOCAL_TB = 6, HJ_SWEEP_LOCAL_COOP = 7, HJ_SWEEP_FIELD_COOP = 8,
-       HJ_SWEEP_DUBINS_COOP = 9 };
+       HJ_SWEEP_DUBINS_COOP = 9, HJ_SWEEP_FIELD_COL = 10 };
 
 typedef struct {
     int32_t dim;            /* 2 or 3                                          */

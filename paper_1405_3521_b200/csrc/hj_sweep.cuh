@@ -672,6 +672,120 @@ __global__ void __launch_bounds__(256, 4)
 }
 
 // ---------------------------------------------------------------------------
+// k_sweep_field2d for the affine problems whose controls all move the foot by the same
+// amount along axis 0 (u_k = (u0, u1_k): config 5's f = (x2, a - x1/2)).  Then
+// d0 = D0 + S0 u0, its cell i0 and weight w0 are the node's, not the control's, and the
+// bilinear interpolant of control k is  lerp(X(i1_k), X(i1_k + 1), w1_k)  with
+// X(j) = lerp(V(i0, j), V(i0 + 1, j), w0) the x-interpolated column at the node's foot
+// abscissa — exactly the two inner lerps k_sweep_field2d computes.  With the controls
+// sorted by u1 (host; the min over controls is order-free), d1_k is non-decreasing, so
+// the node walks its column once: each X(j) is formed once (one pair of loads + one
+// lerp per row instead of four gathers + two lerps per control) and the cell index
+// i1_k = floor(d1_k) advances by comparison instead of a floor per control.  Every value
+// is the one k_sweep_field2d forms: bit-identical iterates (asserted in the parity
+// suite).  Tiles whose footprint leaves the view take k_sweep_field2d's general path.
+// ---------------------------------------------------------------------------
+template <typename T>
+struct ColCtrl {
+    T u0;                              // the shared axis-0 control component
+    T u1[HJ_MAX_CONTROLS];             // axis-1 components, ascending
+    T csq[HJ_MAX_CONTROLS];            // |a_k|^2 in the same order
+};
+
+template <typename T, bool KRUZ, int RY>
+__global__ void __launch_bounds__(256, 4)
+    k_sweep_field2d_col(const DevProblem<T, T> P, const ColCtrl<T> C,
+                        const SweepGroup<T> *__restrict__ G, int64_t it, double tol) {
+    HJ_LIST_BEGIN(G, it, tol)
+    const int vn0 = (int)vw.vn[0], vn1 = (int)vw.vn[1];
+    const T *__restrict__ Vi = vw.V[it & 1];
+    T *__restrict__ Vo = vw.V[(it + 1) & 1];
+    constexpr int TY = 8 * RY;
+    const int li = tc[0] * 32 + (threadIdx.x & 31);
+    const int hx = G->halo[0], hy = G->halo[1];
+    const bool fast = tc[0] * 32 - hx >= 0 && tc[0] * 32 + 31 + hx + 1 <= vn0 - 1 &&
+                      tc[1] * TY - hy >= 0 && tc[1] * TY + TY - 1 + hy + 1 <= vn1 - 1;
+    T rmax = T(0);
+    int changed = 0, evaluated = 0;
+#pragma unroll 1
+    for (int rr = 0; rr < RY; ++rr) {
+    const int lj = tc[1] * TY + (threadIdx.x >> 5) + 8 * rr;
+    if (li < vn0 && lj < vn1) {
+        const int64_t t = li + (int64_t)vn0 * lj;
+        const int64_t gi[3] = {li + vw.o[0], lj + vw.o[1], 0};
+        const int64_t gidx = gi[0] + P.n[0] * gi[1];
+        const int8_t c = vw.cls[t];
+        const T vin = Vi[t];
+        T vnew;
+        if (c == -2) {
+            vnew = P.v_out;
+        } else if (c >= 0) {
+            vnew = P.g ? P.g[gidx] : T(0);
+        } else {
+            const T x0 = fma((T)gi[0], P.dx[0], P.lo[0]), x1 = fma((T)gi[1], P.dx[1], P.lo[1]);
+            const T cs = P.speed ? P.speed[gidx] : T(1);
+            const T D0 = P.hdx[0] * fma(P.A[0], x0, fma(P.A[1], x1, P.b[0]));
+            const T D1 = P.hdx[1] * fma(P.A[3], x0, fma(P.A[4], x1, P.b[1]));
+            const T S0 = P.hdx[0] * cs, S1 = P.hdx[1] * cs;
+            T base;
+            if (KRUZ) {
+                base = P.kcost;
+            } else {
+                const T x[3] = {x0, x1, T(0)};
+                base = P.h * cost_state(P, x);
+            }
+            const T hlr = P.h * P.lr;
+            T best = (T)INFINITY;
+            if (fast) {
+                T w0, w1;
+                const int i0 = floor_split(fma(S0, C.u0, D0), w0);
+                T d1 = fma(S1, C.u1[0], D1);
+                const int j = floor_split(d1, w1);
+                T jf = (T)j;                              // floor(d1), exactly
+                const T *__restrict__ p = Vi + t + i0 + (int64_t)vn0 * j;
+                T Xa = lerp<T>(__ldg(p), __ldg(p + 1), w0);
+                p += vn0;
+                T Xb = lerp<T>(__ldg(p), __ldg(p + 1), w0);
+#pragma unroll 2
+                for (int k = 0; k < P.K; ++k) {
+                    d1 = fma(S1, C.u1[k], D1);
+                    while (d1 >= jf + T(1)) {                 // next cell row of the column
+                        jf += T(1);
+                        Xa = Xb;
+                        p += vn0;
+                        Xb = lerp<T>(__ldg(p), __ldg(p + 1), w0);
+                    }
+                    const T I = lerp<T>(Xa, Xb, d1 - jf);
+                    const T ck = KRUZ ? base : fma(hlr, C.csq[k], base);
+                    best = fmin(best, fma(P.beta, I, ck));
+                }
+            } else {
+                const int64_t o[3] = {vw.o[0], vw.o[1], 0};
+                const int64_t vn[3] = {vn0, vn1, 1};
+#pragma unroll 1
+                for (int k = 0; k < P.K; ++k) {
+                    const T delta[3] = {fma(S0, P.ctrl[k][0], D0), fma(S1, P.ctrl[k][1], D1),
+                                        T(0)};
+                    const T I = interp<T, T, 2>(Vi, o, vn, P.n, P.periodic, gi, delta, P.v_out);
+                    const T ck = KRUZ ? base : fma(hlr, P.csq[k], base);
+                    best = fmin(best, fma(P.beta, I, ck));
+                }
+            }
+            vnew = best;
+            if (P.monotone) vnew = fmin(vnew, vin);
+            ++evaluated;
+        }
+        Vo[t] = vnew;
+        const T dv = vnew > vin ? vnew - vin : vin - vnew;
+        rmax = dv > rmax ? dv : rmax;
+        changed |= !same_bits(vnew, vin);
+    }
+    }
+    changed_ = tile_finish(G, v, tile, it, rmax, changed, evaluated);
+    HJ_LIST_END(G, it)
+}
+
+// ---------------------------------------------------------------------------
 // Dubins car (§2 dynamics family; BASELINE config 4): the (x,y) part of
 // every foot, h v (cos th, sin th), is the same for all controls of a node and
 // only the heading moves with the control (h w a_k).  When |h w a_k| <= 1 heading
@@ -807,6 +921,8 @@ struct SweepLaunch {
     LocalCtrl<T> ctrl;
     int evals = 0;                      // brackets evaluated per interior node and sweep
                                         // (the control count unless a kernel prunes)
+    bool col = false;                   // FIELD2D via k_sweep_field2d_col (shared u0)
+    ColCtrl<T> colctrl;
 };
 
 // bytes of change flags a view needs under the smallest tiling (32 x 8 x 1)
@@ -935,7 +1051,7 @@ hj_status sweep_prepare(const hj_grid &g, const hj_problem &p, const hj_fields &
             if (p.A[d][e] != 0) iso = false;
     }
     const int want = p.sweep_kernel;
-    if (want < HJ_SWEEP_AUTO || want > HJ_SWEEP_DUBINS_COOP) {
+    if (want < HJ_SWEEP_AUTO || want > HJ_SWEEP_FIELD_COL) {
         set_error("unknown sweep_kernel %d", want);
         return HJ_ERR_INVALID;
     }
@@ -1041,7 +1157,8 @@ hj_status sweep_prepare(const hj_grid &g, const hj_problem &p, const hj_fields &
         want != HJ_SWEEP_LOCAL_COOP) {   // (FIELD_COOP: decided with FIELD2D)
         if (g.dim == 2 && (p.dynamics == HJ_DYN_AFFINE || p.dynamics == HJ_DYN_VANDERPOL) &&
             !g.periodic[0] && !g.periodic[1] &&
-            (want == HJ_SWEEP_AUTO || want == HJ_SWEEP_FIELD2D || want == HJ_SWEEP_FIELD_COOP))
+            (want == HJ_SWEEP_AUTO || want == HJ_SWEEP_FIELD2D || want == HJ_SWEEP_FIELD_COOP ||
+             want == HJ_SWEEP_FIELD_COL))
             L.kind = SWEEP_FIELD2D;
         else if (p.dynamics == HJ_DYN_DUBINS && H[2] <= 1.0 && !g.periodic[0] && !g.periodic[1] &&
                  (want == HJ_SWEEP_AUTO || want == HJ_SWEEP_DUBINS ||
@@ -1082,6 +1199,37 @@ hj_status sweep_prepare(const hj_grid &g, const hj_problem &p, const hj_fields &
     if (L.kind == SWEEP_FIELD2D && p.cost == HJ_COST_DISCOUNTED) {
         tile_dim[0] = 32;      // dense problems: 32 x 32 tiles (k_sweep_field2d<.., 4>)
         tile_dim[1] = 32;
+    }
+    if (L.kind == SWEEP_FIELD2D && !L.coop && p.dynamics == HJ_DYN_AFFINE && !f.speed &&
+        (want == HJ_SWEEP_AUTO || want == HJ_SWEEP_FIELD_COL)) {
+        // every control moves the foot by the same amount along axis 0: one x-lerped
+        // column per node (k_sweep_field2d_col)
+        bool shared = true;
+        for (int k = 1; k < p.n_controls; ++k)
+            if (p.controls[k][0] != p.controls[0][0]) shared = false;
+        if (shared) {
+            std::vector<int> ord(p.n_controls);
+            for (int k = 0; k < p.n_controls; ++k) ord[k] = k;
+            std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) {
+                return p.controls[a][1] < p.controls[b][1];
+            });
+            L.col = true;
+            memset(&L.colctrl, 0, sizeof(L.colctrl));
+            L.colctrl.u0 = (T)p.controls[0][0];
+            for (int k = 0; k < p.n_controls; ++k) {
+                const int q = ord[k];
+                L.colctrl.u1[k] = (T)p.controls[q][1];
+                double a2 = 0;
+                for (int c = 0; c < 3; ++c) a2 += p.controls[q][c] * p.controls[q][c];
+                L.colctrl.csq[k] = (T)a2;
+            }
+        }
+    }
+    if (want == HJ_SWEEP_FIELD_COL && !L.col) {
+        set_error("sweep_kernel %d requested, but the problem does not qualify for it "
+                  "(2-D affine, no speed field, every control with the same axis-0 "
+                  "component, feet beyond one cell)", want);
+        return HJ_ERR_UNSUPPORTED;
     }
     if ((want == HJ_SWEEP_FIELD2D && L.kind != SWEEP_FIELD2D) ||
         (want == HJ_SWEEP_DUBINS && L.kind != SWEEP_DUBINS)) {
@@ -1427,6 +1575,19 @@ hj_status sweep_coop(const DevProblem<T, T> &P, const SweepLaunch<T> &L, int64_t
 template <typename T, int DYN, bool KRUZ>
 static void launch_field(const DevProblem<T, T> &P, const SweepLaunch<T> &L, int64_t it,
                          double tol, cudaStream_t s) {
+    if constexpr (DYN == HJ_DYN_AFFINE) {
+        if (L.col) {
+            if (L.dense)
+                k_sweep_field2d_col<T, KRUZ, 4>
+                    <<<grid_for(k_sweep_field2d_col<T, KRUZ, 4>, 256, 0, L.total_tiles, true),
+                       256, 0, s>>>(P, L.colctrl, L.d_group, it, tol);
+            else
+                k_sweep_field2d_col<T, KRUZ, 1>
+                    <<<grid_for(k_sweep_field2d_col<T, KRUZ, 1>, 256, 0, L.total_tiles), 256, 0,
+                       s>>>(P, L.colctrl, L.d_group, it, tol);
+            return;
+        }
+    }
     if (L.dense)   // 32 x 32 tiles
         k_sweep_field2d<T, DYN, KRUZ, 4>
             <<<grid_for(k_sweep_field2d<T, DYN, KRUZ, 4>, 256, 0, L.total_tiles, true), 256, 0,

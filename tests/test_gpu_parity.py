@@ -23,9 +23,9 @@ TIE = 1e-9          # north_star: labels bit-exact where the oracle's control ma
 GEO_TIE = 1e-12     # R11: Dubins positions go through cos/sin (libm vs CUDA may differ by
                     # an ulp): a rounding/box decision that close to its threshold is a tie
 # upper bounds on the fraction of margin-tie coarse nodes (measured with the oracle at the
-# test sizes, R11): exact ties of the discrete problem, e.g. trajectories
+# test sizes and the full coarse grids, R11): exact ties of the discrete problem, e.g. trajectories
 # crossing regions where every foot leaves the box (all brackets = beta v_out + c)
-MAX_TIE_FRAC = {1: 0.12, 2: 0.06, 3: 0.12, 4: 0.45, 5: 0.02}
+MAX_TIE_FRAC = {1: 0.12, 2: 0.25, 3: 0.12, 4: 0.45, 5: 0.02}
 
 
 def compare_labels(tie_report, what, idx, lab, lab_o, mar_o, geo_o, steps=None, steps_o=None):
@@ -98,7 +98,7 @@ def test_solve_matches_oracle(idx, dtype, oracle_cache):
 KERNELS = {1: ("generic", "field2d", "local_scalar", "local_packed", "local_tb", "local_coop"),
            2: ("generic", "field2d", "local_scalar", "local_packed", "local_tb", "local_coop"),
            3: ("generic", "field2d", "field_coop"), 4: ("generic", "dubins", "dubins_coop"),
-           5: ("generic", "field2d")}
+           5: ("generic", "field2d", "field_col")}
 
 
 @pytest.mark.parametrize("idx", [1, 2, 3, 4, 5])
@@ -130,6 +130,10 @@ def test_sweep_kernels_match_oracle(idx, dtype, oracle_cache):
         if k in out:
             assert torch.equal(out["local_scalar"][0], out[k][0]), k
             assert out["local_scalar"][1] == out[k][1], k
+    # the column kernel forms exactly k_sweep_field2d's lerps (one column per node)
+    if "field_col" in out:
+        assert torch.equal(out["field2d"][0], out["field_col"][0])
+        assert out["field2d"][1] == out["field_col"][1]
     # the cooperative Dubins sweep evaluates only the extreme controls of each sign group
     # (Kruzkov: exact, the bracket is monotone in |d_k|) — same iterates as the full loop
     if "dubins" in out and "dubins_coop" in out:
@@ -199,6 +203,37 @@ def test_coop_cluster_mode_matches_grid_mode(idx, monkeypatch):
     for o in out[1:]:
         assert torch.equal(out[0][0], o[0])
         assert out[0][1] == o[1]
+
+
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+@pytest.mark.parametrize("case", ["shifted_u0", "reversed_order", "discounted_lr"])
+def test_field_col_bit_identical_to_field2d(case, dtype):
+    """k_sweep_field2d_col (controls sharing their axis-0 component, walked in ascending
+    axis-1 order) against k_sweep_field2d and the oracle: same iterates bit for bit for
+    unsorted control tables, a nonzero shared u0 and per-control costs."""
+    A = np.zeros((3, 3))
+    A[0, 1], A[1, 0] = 1.0, -0.5
+    ctrl = W.interval_controls(17, axis=1)
+    kw = dict(A=A, cost=W.COST_DISCOUNTED, lam=1.0, lq=1.0, v_out=60.0, tol=1e-9, h=0.09)
+    if case == "shifted_u0":
+        ctrl[:, 0] = 0.3
+    elif case == "reversed_order":
+        ctrl = ctrl[::-1].copy()
+    else:
+        kw["lr"] = 0.7
+    g = W.Grid((77, 61), (-2.0, -2.0), (2.0, 2.0), (False, False))
+    piece = W.sector_pieces(g, 0.3, 4)
+    p = _tiny((77, 61), lo=(-2.0, -2.0), hi=(2.0, 2.0), ctrl=ctrl, piece=piece, **kw)
+    if dtype == "f32":
+        p.tol = 1e-6
+    Vo, it_o, _ = oracle.OracleProblem(p).solve()
+    out = {}
+    for kernel in ("field2d", "field_col"):
+        V, rep = hj.hj_solve(hj.DeviceProblem(p, dtype, sweep_kernel=kernel))
+        assert np.abs(V.double().cpu().numpy() - Vo).max() <= TOL[dtype] * 60
+        out[kernel] = (V.cpu(), rep["iterations"])
+    assert torch.equal(out["field2d"][0], out["field_col"][0])
+    assert out["field2d"][1] == out["field_col"][1]
 
 
 def test_local_kernel_refuses_nonlocal_problem():

@@ -16,7 +16,7 @@ METRICS = {
     "duration_ms": ("gpu__time_duration.sum", 1e-6),
     "dram_read": ("dram__bytes_read.sum", 1.0),
     "dram_write": ("dram__bytes_write.sum", 1.0),
-    "lts_bytes": ("lts__t_bytes.sum", 1.0),
+    "lts_sectors": ("lts__t_sectors.sum", 1.0),
     "issue_active_pct": ("smsp__issue_active.avg.pct_of_peak_sustained_active", 1.0),
     "sm_throughput_pct": ("sm__throughput.avg.pct_of_peak_sustained_elapsed", 1.0),
     "fma_pipe_pct": ("sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active", 1.0),
@@ -29,7 +29,7 @@ METRICS = {
     "warp_inst": ("smsp__inst_executed.sum", 1.0),
     "threads_per_inst": ("smsp__thread_inst_executed_per_inst_executed.ratio", 1.0),
 }
-UNIT_SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12,
+UNIT_SCALE = {"ms": 1e6, "us": 1e3, "ns": 1, "sector": 1, "byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12,
               "nsecond": 1, "usecond": 1e3, "msecond": 1e6, "second": 1e9,
               "inst": 1, "Kinst": 1e3, "Minst": 1e6, "Ginst": 1e9}
 
@@ -60,7 +60,8 @@ def main(path, workload, out, want=None):
     t = d["duration_ms"] / 1e3
     d["dram_bytes_per_launch"] = d.get("dram_read", 0) + d.get("dram_write", 0)
     d["dram_gbs"] = d["dram_bytes_per_launch"] / t / 1e9
-    d["l2_gbs"] = d.get("lts_bytes", 0) / t / 1e9
+    d["lts_bytes"] = 32.0 * d.get("lts_sectors", 0)        # 32-byte L2 sectors
+    d["l2_gbs"] = d["lts_bytes"] / t / 1e9
     stalls = {h: r[i] for i, h in enumerate(hdr) if h.startswith("smsp__pcsamp_warps_issue_stalled_")
               and not h.endswith("_not_issued")}
     tot = sum(float(v.replace(",", "") or 0) for v in stalls.values())
