@@ -335,10 +335,12 @@ def main():
     if lab.get("label") is not None:
         mar = lab["margin"]
         bits = res["mask"]
-        cover = int(sum(int(((bits >> k) & 1).sum()) for k in range(cfg.m)))
+        cover = int(sum(int(((bits >> k) & 1).sum()) for k in range(res["n_sets"])))
         labels = {"coarse_nodes": int(mar.numel()),
                   "margin_ties": int((mar <= 1e-9).sum()),
-                  "unlabelled": int((lab["label"] < 0).sum()),
+                  "unlabelled_all_sets": int((lab["label"] == -1).sum()),
+                  "exit_set": int((lab["label"] == -2).sum()),
+                  "sets": res["n_sets"],
                   "subdomain_nodes_over_N": round(cover / fine.N, 3)}
 
     if rank != 0:

@@ -55,7 +55,8 @@ extern "C" {
 
 #define HJ_MAX_DIM 3
 #define HJ_MAX_CONTROLS 128
-#define HJ_MAX_SUBDOMAINS 32
+#define HJ_MAX_SUBDOMAINS 64    /* sets of a membership mask (its uint64 bits): the
+                                   target pieces plus, optionally, the exit set */
 
 typedef enum {
     HJ_OK = 0,
@@ -220,16 +221,25 @@ hj_status hj_coarse_feedback(const hj_grid *grid, const hj_problem *prob,
  *     (floor(g + 1/2) in index space) is a target node; -1 if y leaves the box or
  *     n_max steps pass.  (Independent sub-domain: PAPER.md Definition 2.2 line
  *     150-152, Proposition 2.3 line 156-163 — optimal trajectories stay in it.)
+ *     Exit set (reading R9b): with Vexit given, an unlabelled node whose value needs no
+ *     target, Vc(z) >= Vexit(z) - exit_tol, is labelled -2: it belongs to the
+ *     sub-domain of the box-boundary piece of Gamma (exit cost v_out), set m.
  * (b) Prolongation with overlap band (R9; ISA step 2, line 398-418): fine node i
- *     is in S_k iff a coarse node I labelled k (or -1) has |i_d - R_d I_d| <=
- *     R_d + band on every axis; fine target nodes of piece k are always in S_k.
+ *     is in S_k iff a coarse node I labelled k has |i_d - R_d I_d| <= R_d + band on
+ *     every axis; a node labelled -1 counts for every set (all m pieces, and the exit
+ *     set when enabled), a node labelled -2 for the exit set m only; fine target nodes
+ *     of piece k are always in S_k.
  *
  * coarse_grid/prob/coarse_fields/dtype/Vc  the coarse problem and its solution
  *     (device Vc); the trajectory uses coarse_prob.h.
+ * Vexit          device, N_c values of dtype: the coarse solution with NO target node
+ *                (the exit is the only way the cost ends), or NULL (no exit set: -1
+ *                labels join every piece's set, R9)
+ * exit_tol       >= 0, the exit test's threshold (ignored without Vexit)
  * n_max          step budget per trajectory (>= 0)
  * fine_grid      nested fine grid: (n_f - 1) = R (n_c - 1), or n_f = R n_c periodic
  * ratio[3]       R per axis (1 for unused axes); band >= 0 in fine cells
- * m              number of target pieces / sub-domains, 1..32
+ * m              number of target pieces, 1..64 (1..63 with Vexit: the exit set is bit m)
  * fine_piece     device int8[N_f] target pieces on the fine grid; piece values must
  *                lie in [-1, m): a piece >= m (not checked on the device) belongs to
  *                no sub-domain bit
@@ -240,15 +250,17 @@ hj_status hj_coarse_feedback(const hj_grid *grid, const hj_problem *prob,
  * Outputs (device): label int32[N_c]; margin double[N_c] = min control margin
  *     along the trajectory; geo double[N_c] = min distance (index units) of a
  *     rounding / box decision to its threshold; steps int32[N_c];
- *     fine_mask uint32[N_f] bit k = node in S_k.  margin/geo/steps may be NULL.
+ *     fine_mask uint64[N_f] bit k = node in S_k (k = m: the exit set).
+ *     margin/geo/steps may be NULL.
  * Asynchronous on `stream`.
  * ------------------------------------------------------------------------- */
 hj_status hj_label_subdomains(const hj_grid *coarse_grid, const hj_problem *coarse_prob,
                               const hj_fields *coarse_fields, int32_t dtype, const void *Vc,
-                              int64_t n_max, const hj_grid *fine_grid, const int32_t ratio[3],
-                              int32_t band, int32_t m, const int8_t *fine_piece, int32_t *label,
+                              const void *Vexit, double exit_tol, int64_t n_max,
+                              const hj_grid *fine_grid, const int32_t ratio[3], int32_t band,
+                              int32_t m, const int8_t *fine_piece, int32_t *label,
                               double *margin, double *geo, int32_t *steps,
-                              uint32_t *fine_mask, void *stream);
+                              uint64_t *fine_mask, void *stream);
 
 /* ---------------------------------------------------------------------------
  * hj_ra_subdomains — the paper's own reconstruction algorithm RA (PAPER.md
@@ -261,8 +273,8 @@ hj_status hj_label_subdomains(const hj_grid *coarse_grid, const hj_problem *coar
  * then, if fine_mask != NULL, ISA step 2: the sets are prolonged to the nested fine grid
  * with the overlap band exactly as hj_label_subdomains does with labels (R9).
  * Vaux: device, m * N_c values of dtype (V_i of piece i at [i * N_c]); Vmin: device
- * N_c values; coarse_mask: device uint32[N_c], bit i = node in Sigma_i; fine_mask:
- * device uint32[N_f] or NULL.  workspace: device, >= hj_ra_workspace_bytes().
+ * N_c values; coarse_mask: device uint64[N_c], bit i = node in Sigma_i; fine_mask:
+ * device uint64[N_f] or NULL.  workspace: device, >= hj_ra_workspace_bytes().
  * reports: host hj_report[m] (one per auxiliary solve), may be NULL.
  * Returns HJ_ERR_NOT_CONVERGED if an auxiliary solve hit max_iter.  Synchronises.
  * ------------------------------------------------------------------------- */
@@ -273,17 +285,18 @@ hj_status hj_ra_subdomains(const hj_grid *coarse_grid, const hj_problem *coarse_
                            double M, double q, double tol, int64_t max_iter,
                            const hj_grid *fine_grid, const int32_t ratio[3], int32_t band,
                            const int8_t *fine_piece, void *Vaux, void *Vmin,
-                           uint32_t *coarse_mask, uint32_t *fine_mask, void *workspace,
+                           uint64_t *coarse_mask, uint64_t *fine_mask, void *workspace,
                            size_t ws_bytes, void *stream, hj_report *reports);
 
 /* ---------------------------------------------------------------------------
- * hj_partition_plan — sizes of the fine sub-domains S_0..S_{m-1} from the mask.
- * fine_mask: device uint32[N]; plan: host hj_subdomain[m] (output).
+ * hj_partition_plan — sizes of the fine sub-domains S_0..S_{m-1} from the mask
+ * (m = the number of sets: the pieces, plus one for the exit set when labelled with it).
+ * fine_mask: device uint64[N]; plan: host hj_subdomain[m] (output).
  * *ws_bytes (output) = workspace hj_solve_partitioned needs to solve ALL m
  * sub-domains with this dtype/max_iter (a subset needs no more).
  * Synchronises the stream.
  * ------------------------------------------------------------------------- */
-hj_status hj_partition_plan(const hj_grid *fine_grid, const uint32_t *fine_mask, int32_t m,
+hj_status hj_partition_plan(const hj_grid *fine_grid, const uint64_t *fine_mask, int32_t m,
                             int32_t dtype, int64_t max_iter, hj_subdomain *plan,
                             size_t *ws_bytes, void *stream);
 
@@ -301,7 +314,7 @@ hj_status hj_assign_subdomains(int32_t m, const hj_subdomain *plan, int32_t n_ra
  * For every k with bit k of solve_set: value iteration (as hj_solve) on S_k, with
  * nodes outside S_k acting as ghost nodes holding v_out (R10) and every target
  * node inside S_k holding g; all selected sub-domains iterate concurrently and
- * stop independently.  Then
+ * stop independently (in groups of up to 32 at a time).  Then
  *     Vbar[j] = min { V_k[j] : k in solve_set, bit k of fine_mask[j] }   (v_out if none).
  * Multi-GPU: each rank passes its own solve_set; the element-wise MIN of the
  * ranks' Vbar over NCCL is the ISA result (no exchange during the solves).
@@ -313,8 +326,8 @@ hj_status hj_assign_subdomains(int32_t m, const hj_subdomain *plan, int32_t n_ra
  * ------------------------------------------------------------------------- */
 hj_status hj_solve_partitioned(const hj_grid *fine_grid, const hj_problem *prob,
                                const hj_fields *fine_fields, int32_t dtype,
-                               const uint32_t *fine_mask, int32_t m, const hj_subdomain *plan,
-                               uint32_t solve_set, double tol, int64_t max_iter, void *Vbar,
+                               const uint64_t *fine_mask, int32_t m, const hj_subdomain *plan,
+                               uint64_t solve_set, double tol, int64_t max_iter, void *Vbar,
                                void *workspace, size_t ws_bytes, void *stream,
                                hj_report *reports);
 

@@ -75,7 +75,7 @@ class _Prob(ctypes.Structure):
 _dp = ctypes.POINTER(ctypes.c_double)
 _ip = ctypes.POINTER(ctypes.c_int)
 _lp = ctypes.POINTER(ctypes.c_long)
-_up = ctypes.POINTER(ctypes.c_uint)
+_up = ctypes.POINTER(ctypes.c_ulonglong)    # uint64 membership masks
 _bp = ctypes.POINTER(ctypes.c_byte)
 
 
@@ -107,7 +107,8 @@ def _load():
             lib.or_label_nodes.argtypes = [P, _dp, _lp, ctypes.c_long, ctypes.c_long, _ip, _lp,
                                            _dp, _dp]
             lib.or_prolong.argtypes = [_lp, _lp, _ip, ctypes.c_int, _lp, ctypes.c_long, _ip,
-                                       ctypes.c_int, _bp, _up]
+                                       ctypes.c_int, ctypes.c_int, _bp, _up]
+            lib.or_exit_labels.argtypes = [ctypes.c_long, _ip, _dp, _dp, ctypes.c_double]
             lib.or_prolong_mask.argtypes = [_lp, _lp, _ip, ctypes.c_int, _lp, ctypes.c_long, _up,
                                             ctypes.c_int, _bp, _up]
             lib.or_ra_masks.argtypes = [ctypes.c_long, ctypes.c_int, ctypes.POINTER(_dp), _dp, _bp,
@@ -196,7 +197,7 @@ class OracleProblem:
 
     def classes(self, mask=None, k=0):
         cls = np.empty(self.N, np.int8)
-        mp = _ptr(np.ascontiguousarray(mask, np.uint32), _up) if mask is not None else _up()
+        mp = _ptr(np.ascontiguousarray(mask, np.uint64), _up) if mask is not None else _up()
         self._keep = mask
         self.lib.or_classes(self.ref, mp, int(k), _ptr(cls, _bp))
         return cls
@@ -253,7 +254,7 @@ class OracleProblem:
         return lab, st, mar, geo
 
     def solve_subdomain(self, mask, k, tol=None, max_iter=None):
-        mask = np.ascontiguousarray(mask, np.uint32)
+        mask = np.ascontiguousarray(mask, np.uint64)
         tol = self.prob.tol if tol is None else tol
         max_iter = self.prob.max_iter if max_iter is None else max_iter
         V = np.empty(self.N)
@@ -263,8 +264,9 @@ class OracleProblem:
         return V, int(it), res.value
 
 
-def prolong(coarse_grid, fine_grid, ratio, band, coarse_label, m, fine_piece):
-    """ISA step 2 with the overlap band (R9).  Returns the uint32 membership mask."""
+def prolong(coarse_grid, fine_grid, ratio, band, coarse_label, m, fine_piece, exit_set=False):
+    """ISA step 2 with the overlap band (R9; R9b with exit_set: label -2 -> set m, -1 ->
+    all m + 1 sets).  Returns the uint64 membership mask."""
     lib = _load()
     dim = fine_grid.dim
     nc = np.ones(3, np.int64)
@@ -275,10 +277,20 @@ def prolong(coarse_grid, fine_grid, ratio, band, coarse_label, m, fine_piece):
         nc[d], nf[d], per[d], rr[d] = coarse_grid.n[d], fine_grid.n[d], fine_grid.periodic[d], ratio[d]
     lab = np.ascontiguousarray(coarse_label, np.int32)
     fp = np.ascontiguousarray(fine_piece, np.int8)
-    out = np.empty(fine_grid.size, np.uint32)
+    out = np.empty(fine_grid.size, np.uint64)
     lib.or_prolong(_ptr(nc, _lp), _ptr(nf, _lp), _ptr(per, _ip), dim, _ptr(rr, _lp), int(band),
-                   _ptr(lab, _ip), int(m), _ptr(fp, _bp), _ptr(out, _up))
+                   _ptr(lab, _ip), int(m), int(bool(exit_set)), _ptr(fp, _bp), _ptr(out, _up))
     return out
+
+
+def exit_labels(labels, Vc, Vexit, tol):
+    """Reading R9b: unlabelled (-1) coarse nodes with Vc >= Vexit - tol -> -2 (exit set)."""
+    lib = _load()
+    lab = np.array(labels, np.int32, copy=True)
+    Vc = np.ascontiguousarray(Vc, np.float64)
+    Vexit = np.ascontiguousarray(Vexit, np.float64)
+    lib.or_exit_labels(len(lab), _ptr(lab, _ip), _ptr(Vc, _dp), _ptr(Vexit, _dp), float(tol))
+    return lab
 
 
 def prolong_mask(coarse_grid, fine_grid, ratio, band, coarse_mask, m, fine_piece):
@@ -291,9 +303,9 @@ def prolong_mask(coarse_grid, fine_grid, ratio, band, coarse_mask, m, fine_piece
     rr = np.ones(3, np.int64)
     for d in range(dim):
         nc[d], nf[d], per[d], rr[d] = coarse_grid.n[d], fine_grid.n[d], fine_grid.periodic[d], ratio[d]
-    cm = np.ascontiguousarray(coarse_mask, np.uint32)
+    cm = np.ascontiguousarray(coarse_mask, np.uint64)
     fp = np.ascontiguousarray(fine_piece, np.int8)
-    out = np.empty(fine_grid.size, np.uint32)
+    out = np.empty(fine_grid.size, np.uint64)
     lib.or_prolong_mask(_ptr(nc, _lp), _ptr(nf, _lp), _ptr(per, _ip), dim, _ptr(rr, _lp),
                         int(band), _ptr(cm, _up), int(m), _ptr(fp, _bp), _ptr(out, _up))
     return out
@@ -318,7 +330,7 @@ def ra(problem, m, C, M, q, tol=None, max_iter=None):
     thr = 2.0 * (C * dx ** q + M * dx)
     arrs = [np.ascontiguousarray(v, np.float64) for v in Vs]
     ptrs = (_dp * m)(*[_ptr(a, _dp) for a in arrs])
-    mask = np.empty(problem.grid.size, np.uint32)
+    mask = np.empty(problem.grid.size, np.uint64)
     lib.or_ra_masks(problem.grid.size, int(m), ptrs, _ptr(np.ascontiguousarray(Vmin), _dp),
                     _ptr(np.ascontiguousarray(piece), _bp), float(thr), _ptr(mask, _up))
     return Vs, Vmin, mask, its
@@ -333,7 +345,7 @@ def ra_masks(Vs, V, piece, thr):
     ptrs = (_dp * m)(*[_ptr(a, _dp) for a in arrs])
     V = np.ascontiguousarray(V, np.float64)
     piece = np.ascontiguousarray(piece, np.int8)
-    mask = np.empty(len(V), np.uint32)
+    mask = np.empty(len(V), np.uint64)
     lib.or_ra_masks(len(V), int(m), ptrs, _ptr(V, _dp), _ptr(piece, _bp), float(thr),
                     _ptr(mask, _up))
     return mask
@@ -348,7 +360,7 @@ def threads():
 def assemble(mask, Vks, v_out):
     """ISA step 4: min over the sub-domains containing each node."""
     lib = _load()
-    mask = np.ascontiguousarray(mask, np.uint32)
+    mask = np.ascontiguousarray(mask, np.uint64)
     arrs = [np.ascontiguousarray(v, np.float64) for v in Vks]
     ptrs = (_dp * len(arrs))(*[_ptr(a, _dp) for a in arrs])
     out = np.empty(len(mask))
@@ -356,21 +368,39 @@ def assemble(mask, Vks, v_out):
     return out
 
 
-def isa(fine_problem, coarse_problem, ratio, band, m, n_max):
-    """The full oracle pipeline: coarse solve -> labels -> prolong -> sub-domain
-    solves -> assembly (§4 ISA with the north_star labelling)."""
+EXIT_TOL_FACTOR = 10.0     # R9b: exit test threshold = 10 x the coarse tolerance
+
+
+def exit_solution(coarse_problem):
+    """Vexit: the coarse problem with no target node (reading R9b)."""
+    import dataclasses
+    pe = dataclasses.replace(coarse_problem,
+                             piece=np.full(coarse_problem.grid.size, -1, np.int8))
+    V, _, _ = OracleProblem(pe).solve()
+    return V
+
+
+def isa(fine_problem, coarse_problem, ratio, band, m, n_max, exit_set=True):
+    """The full oracle pipeline: coarse solve -> labels (-> exit set, R9b) -> prolong ->
+    sub-domain solves -> assembly (§4 ISA with the north_star labelling)."""
     oc = OracleProblem(coarse_problem)
     Vc, itc, _ = oc.solve()
     lab, steps, mar, geo = oc.label(Vc, np.arange(oc.N), n_max)
+    Vexit = None
+    if exit_set:
+        Vexit = exit_solution(coarse_problem)
+        lab = exit_labels(lab, Vc, Vexit, EXIT_TOL_FACTOR * coarse_problem.tol)
+    sets = m + (1 if exit_set else 0)
     mask = prolong(coarse_problem.grid, fine_problem.grid, ratio, band, lab, m,
-                   fine_problem.piece)
+                   fine_problem.piece, exit_set=exit_set)
     of = OracleProblem(fine_problem)
     Vks = []
     iters = []
-    for k in range(m):
+    for k in range(sets):
         V, it, _ = of.solve_subdomain(mask, k)
         Vks.append(V)
         iters.append(it)
     Vbar = assemble(mask, Vks, fine_problem.v_out)
     return dict(Vc=Vc, coarse_iters=itc, labels=lab, label_margin=mar, label_geo=geo,
-                label_steps=steps, mask=mask, Vk=Vks, iters=iters, Vbar=Vbar)
+                label_steps=steps, mask=mask, Vk=Vks, iters=iters, Vbar=Vbar, Vexit=Vexit,
+                n_sets=sets)

@@ -205,11 +205,11 @@ static double or_node_g(const or_problem *p, long idx) { return p->g ? p->g[idx]
 
 /* Node classes for a (possibly masked) solve: a node outside the sub-domain mask
  * is a ghost holding v_out (R10); a target node holds g (Tdef line 242). */
-void or_classes(const or_problem *p, const unsigned int *mask, int k, signed char *cls) {
+void or_classes(const or_problem *p, const unsigned long long *mask, int k, signed char *cls) {
     long N = or_size(p);
 #pragma omp parallel for schedule(static)
     for (long i = 0; i < N; ++i) {
-        int in = mask ? ((mask[i] >> k) & 1u) : 1;
+        int in = mask ? (int)((mask[i] >> k) & 1ull) : 1;
         if (!in) cls[i] = OR_GHOST;
         else cls[i] = (p->piece[i] >= 0) ? OR_TARGET : OR_INTERIOR;
     }
@@ -380,9 +380,9 @@ void or_label_nodes(const or_problem *p, const double *V, const long *nodes, lon
  * coarse node I with bit k has |i_d - R_d I_d| <= R_d + band on every axis; fine target
  * nodes of piece k are always in S_k. */
 void or_prolong_mask(const long nc[3], const long nf[3], const int periodic[3], int dim,
-                     const long ratio[3], long band, const unsigned int *coarse_mask, int m,
-                     const signed char *fine_piece, unsigned int *fine_mask) {
-    unsigned int all = (m >= 32) ? 0xffffffffu : ((1u << m) - 1u);
+                     const long ratio[3], long band, const unsigned long long *coarse_mask,
+                     int m, const signed char *fine_piece, unsigned long long *fine_mask) {
+    unsigned long long all = (m >= 64) ? ~0ull : ((1ull << m) - 1ull);
     long Nf = 1;
     for (int d = 0; d < dim; ++d) Nf *= nf[d];
 #pragma omp parallel for schedule(static)
@@ -399,7 +399,7 @@ void or_prolong_mask(const long nc[3], const long nf[3], const int periodic[3], 
             lo[d] = (long)ceil((double)(ii[d] - reach) / (double)ratio[d]);
             hi[d] = (long)floor((double)(ii[d] + reach) / (double)ratio[d]);
         }
-        unsigned int bits = 0;
+        unsigned long long bits = 0;
         long I[3];
         for (I[2] = lo[2]; I[2] <= hi[2]; ++I[2])
             for (I[1] = lo[1]; I[1] <= hi[1]; ++I[1])
@@ -421,42 +421,59 @@ void or_prolong_mask(const long nc[3], const long nf[3], const int periodic[3], 
                     for (int d = dim - 1; d >= 0; --d) cidx = cidx * nc[d] + J[d];
                     bits |= coarse_mask[cidx];
                 }
-        if (fine_piece[idx] >= 0) bits |= 1u << fine_piece[idx];
+        if (fine_piece[idx] >= 0) bits |= 1ull << fine_piece[idx];
         fine_mask[idx] = bits & all;
     }
 }
 
-/* ISA step 2 from trajectory labels (R8, R9): label k -> bit k, label -1 (the
- * trajectory left the box or ran out of steps) -> every bit ("automatically included in
- * each approximation"). */
+/* ISA step 2 from trajectory labels (R8, R9, R9b): label k -> bit k; label -1 (the
+ * trajectory left the box or ran out of steps) -> every set ("automatically included in
+ * each approximation"): the m pieces and, with exit_set, the exit set;
+ * label -2 (exit set, or_exit_labels) -> bit m only. */
 void or_prolong(const long nc[3], const long nf[3], const int periodic[3], int dim,
-                const long ratio[3], long band, const int *coarse_label, int m,
-                const signed char *fine_piece, unsigned int *fine_mask) {
-    unsigned int all = (m >= 32) ? 0xffffffffu : ((1u << m) - 1u);
+                const long ratio[3], long band, const int *coarse_label, int m, int exit_set,
+                const signed char *fine_piece, unsigned long long *fine_mask) {
+    int sets = m + (exit_set ? 1 : 0);
+    unsigned long long all = (sets >= 64) ? ~0ull : ((1ull << sets) - 1ull);
     long Nc = 1;
     for (int d = 0; d < dim; ++d) Nc *= nc[d];
-    unsigned int *cm = (unsigned int *)malloc(sizeof(unsigned int) * (size_t)Nc);
-    for (long j = 0; j < Nc; ++j) cm[j] = coarse_label[j] < 0 ? all : (1u << coarse_label[j]);
-    or_prolong_mask(nc, nf, periodic, dim, ratio, band, cm, m, fine_piece, fine_mask);
+    unsigned long long *cm = (unsigned long long *)malloc(sizeof(unsigned long long) * (size_t)Nc);
+    for (long j = 0; j < Nc; ++j) {
+        int l = coarse_label[j];
+        if (l >= 0) cm[j] = 1ull << l;
+        else if (l == -2) cm[j] = exit_set ? (1ull << m) : 0ull;
+        else cm[j] = all;
+    }
+    or_prolong_mask(nc, nf, periodic, dim, ratio, band, cm, sets, fine_piece, fine_mask);
     free(cm);
+}
+
+/* Exit set (reading R9b): the box boundary is a piece of Gamma of its own (exit cost
+ * v_out, Tdef line 243; Theorem 2.1 decomposes all of Gamma).  An unlabelled node (-1)
+ * whose value needs no target — Vc >= Vexit - tol, Vexit the solution with no target
+ * node (RA's test of line 325 for that piece, with a solver-level threshold) — belongs
+ * to the exit piece's set: label -2. */
+void or_exit_labels(long N, int *labels, const double *Vc, const double *Vexit, double tol) {
+    for (long j = 0; j < N; ++j)
+        if (labels[j] == -1 && Vc[j] >= Vexit[j] - tol) labels[j] = -2;
 }
 
 /* RA step 3: Sigma_i = X_i plus every node j with
  * |V_i(j) - V(j)| <= thr, thr = 2 (C dx^q + M dx); bit i of mask[j]. */
 void or_ra_masks(long N, int m, const double *const *Vi, const double *V,
-                 const signed char *piece, double thr, unsigned int *mask) {
+                 const signed char *piece, double thr, unsigned long long *mask) {
 #pragma omp parallel for schedule(static)
     for (long j = 0; j < N; ++j) {
-        unsigned int bits = 0;
+        unsigned long long bits = 0;
         for (int i = 0; i < m; ++i)
-            if (piece[j] == i || fabs(Vi[i][j] - V[j]) <= thr) bits |= 1u << i;
+            if (piece[j] == i || fabs(Vi[i][j] - V[j]) <= thr) bits |= 1ull << i;
         mask[j] = bits;
     }
 }
 
 /* ISA step 3 for one sub-domain (§4): value iteration
  * restricted to the mask of sub-domain k (outside = ghost, R10). */
-long or_solve_subdomain(const or_problem *p, const unsigned int *mask, int k, double *V,
+long or_solve_subdomain(const or_problem *p, const unsigned long long *mask, int k, double *V,
                         double tol, long max_iter, double *res_out) {
     long N = or_size(p);
     signed char *cls = (signed char *)malloc(N);
@@ -467,14 +484,15 @@ long or_solve_subdomain(const or_problem *p, const unsigned int *mask, int k, do
 }
 
 /* ISA step 4 (§4): Vbar(j) = min { V_k(j) : x_j in S_k }. */
-void or_assemble(long N, int m, const unsigned int *mask, const double *const *Vk, double v_out,
+void or_assemble(long N, int m, const unsigned long long *mask, const double *const *Vk,
+                 double v_out,
                  double *Vbar) {
 #pragma omp parallel for schedule(static)
     for (long j = 0; j < N; ++j) {
         double v = v_out;
         int any = 0;
         for (int k = 0; k < m; ++k)
-            if ((mask[j] >> k) & 1u) {
+            if ((mask[j] >> k) & 1ull) {
                 if (!any || Vk[k][j] < v) v = Vk[k][j];
                 any = 1;
             }

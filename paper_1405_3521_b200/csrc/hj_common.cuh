@@ -11,6 +11,11 @@
 
 namespace hj {
 
+// views one sweep launch (or one cooperative launch) iterates together: the cooperative
+// kernel keeps one view per lane of a warp (stopping decisions, residual reads); larger
+// sets of sub-domains are solved in groups of this size, one group after the other
+#define HJ_GROUP_VIEWS 32
+
 // Problem constants as the kernels see them: everything prescaled on the host
 // (in fp64, then rounded to Tc) so the inner loop only multiplies and adds.
 //   Tc = arithmetic type, Ts = storage type of the node fields (speed, g, V).

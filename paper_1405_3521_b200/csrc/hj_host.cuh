@@ -141,6 +141,7 @@ double *pinned_scratch(size_t count);
 // ISA step 2 (R9): coarse labels (is_mask = false) or membership masks onto the fine grid
 hj_status prolong_launch(const hj_grid &cg, const hj_grid &fg, const int32_t ratio[3],
                          int32_t band, int32_t m, const void *coarse, bool is_mask,
-                         const int8_t *fine_piece, uint32_t *fine_mask, cudaStream_t s);
+                         const int8_t *fine_piece, uint64_t *fine_mask, cudaStream_t s,
+                         bool exit_set = false);
 
 }  // namespace hj

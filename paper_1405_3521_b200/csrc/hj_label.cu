@@ -351,7 +351,8 @@ template <typename Ts, int DIM, bool THREAD = false>
 __global__ void __launch_bounds__(256)
     k_label_warp(const DevProblem<double, Ts> P, const Ts *__restrict__ V,
                  const int8_t *__restrict__ piece, int64_t N, int64_t n_max, int32_t *label,
-                 double *margin_out, double *geo_out, int32_t *steps_out) {
+                 double *margin_out, double *geo_out, int32_t *steps_out,
+                 const Ts *__restrict__ Vexit, double exit_tol) {
     const int64_t o[3] = {0, 0, 0};
     const int64_t vn[3] = {P.n[0], P.n[1], P.n[2]};
     const int lane = THREAD ? 0 : (int)(threadIdx.x & 31);
@@ -434,6 +435,8 @@ __global__ void __launch_bounds__(256)
                 break;
             }
         }
+        // exit set (R9b): an unlabelled node whose value needs no target
+        if (lab < 0 && Vexit && (double)V[t] >= (double)Vexit[t] - exit_tol) lab = -2;
         if (lane == 0) {
             label[t] = lab;
             if (margin_out) margin_out[t] = mm;
@@ -448,8 +451,15 @@ struct ProlongArgs {
     int64_t nc[3], nf[3], R[3];
     int periodic[3];
     int64_t band;
-    uint32_t all;
+    uint64_t all;       // every set: the m pieces (and the exit set when enabled)
+    uint64_t exit_bit;  // bit of the exit set (label -2), 0 when disabled
 };
+
+// the sets a coarse label stands for (R9, R9b)
+__device__ __forceinline__ uint64_t label_bits(const ProlongArgs &A, int32_t l) {
+    if (l >= 0) return l < 64 ? (1ull << l) : 0ull;
+    return l == -2 ? A.exit_bit : A.all;
+}
 
 __device__ __forceinline__ int64_t floordiv(int64_t a, int64_t b) {
     int64_t q = a / b;
@@ -460,9 +470,9 @@ __device__ __forceinline__ int64_t floordiv(int64_t a, int64_t b) {
 // MASK = true: coarse membership bit masks (the RA sets)
 template <bool MASK>
 __global__ void k_prolong(const ProlongArgs A, const void *__restrict__ coarse,
-                          const int8_t *__restrict__ fine_piece, int64_t Nf, uint32_t *mask) {
+                          const int8_t *__restrict__ fine_piece, int64_t Nf, uint64_t *mask) {
     const int32_t *lab = (const int32_t *)coarse;
-    const uint32_t *cmask = (const uint32_t *)coarse;
+    const uint64_t *cmask = (const uint64_t *)coarse;
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < Nf;
          t += (int64_t)gridDim.x * blockDim.x) {
         int64_t ii[3] = {t % A.nf[0], (t / A.nf[0]) % A.nf[1], t / (A.nf[0] * A.nf[1])};
@@ -472,7 +482,7 @@ __global__ void k_prolong(const ProlongArgs A, const void *__restrict__ coarse,
             lo[d] = -floordiv(-(ii[d] - reach), A.R[d]);  // ceil
             hi[d] = floordiv(ii[d] + reach, A.R[d]);
         }
-        uint32_t bits = 0;
+        uint64_t bits = 0;
         for (int64_t I2 = lo[2]; I2 <= hi[2]; ++I2)
             for (int64_t I1 = lo[1]; I1 <= hi[1]; ++I1)
                 for (int64_t I0 = lo[0]; I0 <= hi[0]; ++I0) {
@@ -490,15 +500,13 @@ __global__ void k_prolong(const ProlongArgs A, const void *__restrict__ coarse,
                     }
                     if (!ok) continue;
                     const int64_t cidx = J[0] + A.nc[0] * (J[1] + A.nc[1] * J[2]);
-                    if (MASK) {
+                    if (MASK)
                         bits |= cmask[cidx];
-                    } else {
-                        const int32_t l = lab[cidx];
-                        bits |= (l < 0) ? A.all : (l < 32 ? (1u << l) : 0u);
-                    }
+                    else
+                        bits |= label_bits(A, lab[cidx]);
                 }
         int8_t p = fine_piece[t];
-        if (p >= 0 && p < 32) bits |= 1u << p;
+        if (p >= 0 && p < 64) bits |= 1ull << p;
         mask[t] = bits & A.all;
     }
 }
@@ -520,10 +528,10 @@ __device__ __forceinline__ bool prolong_wrap(const ProlongArgs &A, int d, int64_
 template <bool MASK>
 __global__ void __launch_bounds__(256)
     k_prolong_rows(const ProlongArgs A, const void *__restrict__ coarse,
-                   const int8_t *__restrict__ fine_piece, uint32_t *mask) {
-    extern __shared__ uint32_t ryz[];                 // [nc0]
+                   const int8_t *__restrict__ fine_piece, uint64_t *mask) {
+    extern __shared__ uint64_t ryz[];                 // [nc0]
     const int32_t *lab = (const int32_t *)coarse;
-    const uint32_t *cmask = (const uint32_t *)coarse;
+    const uint64_t *cmask = (const uint64_t *)coarse;
     const int64_t rows = A.nf[1] * A.nf[2];
     for (int64_t row = blockIdx.x; row < rows; row += gridDim.x) {
         const int64_t i12[2] = {row % A.nf[1], row / A.nf[1]};
@@ -537,7 +545,7 @@ __global__ void __launch_bounds__(256)
         }
         __syncthreads();                                   // the previous row's reads
         for (int64_t J0 = threadIdx.x; J0 < A.nc[0]; J0 += blockDim.x) {
-            uint32_t b = 0;
+            uint64_t b = 0;
             for (int64_t I2 = lo[1]; I2 <= hi[1]; ++I2) {
                 int64_t J2 = I2;
                 if (A.dim > 2 && !prolong_wrap(A, 2, J2)) continue;
@@ -545,12 +553,10 @@ __global__ void __launch_bounds__(256)
                     int64_t J1 = I1;
                     if (A.dim > 1 && !prolong_wrap(A, 1, J1)) continue;
                     const int64_t cidx = J0 + A.nc[0] * (J1 + A.nc[1] * J2);
-                    if (MASK) {
+                    if (MASK)
                         b |= cmask[cidx];
-                    } else {
-                        const int32_t l = lab[cidx];
-                        b |= (l < 0) ? A.all : (l < 32 ? (1u << l) : 0u);
-                    }
+                    else
+                        b |= label_bits(A, lab[cidx]);
                 }
             }
             ryz[J0] = b;
@@ -559,7 +565,7 @@ __global__ void __launch_bounds__(256)
         const int64_t reach0 = A.R[0] + A.band;
         for (int64_t i0 = threadIdx.x; i0 < A.nf[0]; i0 += blockDim.x) {
             const int64_t lo0 = -floordiv(-(i0 - reach0), A.R[0]), hi0 = floordiv(i0 + reach0, A.R[0]);
-            uint32_t bits = 0;
+            uint64_t bits = 0;
             for (int64_t I0 = lo0; I0 <= hi0; ++I0) {
                 int64_t J0 = I0;
                 if (!prolong_wrap(A, 0, J0)) continue;
@@ -567,7 +573,7 @@ __global__ void __launch_bounds__(256)
             }
             const int64_t t = i0 + A.nf[0] * (i12[0] + A.nf[1] * i12[1]);
             const int8_t p = fine_piece[t];
-            if (p >= 0 && p < 32) bits |= 1u << p;
+            if (p >= 0 && p < 64) bits |= 1ull << p;
             mask[t] = bits & A.all;
         }
     }
@@ -576,7 +582,8 @@ __global__ void __launch_bounds__(256)
 // ISA step 2 (R9) from labels or masks of the coarse grid cg onto the nested fine grid fg
 hj_status prolong_launch(const hj_grid &cg, const hj_grid &fg, const int32_t ratio[3],
                          int32_t band, int32_t m, const void *coarse, bool is_mask,
-                         const int8_t *fine_piece, uint32_t *fine_mask, cudaStream_t s) {
+                         const int8_t *fine_piece, uint64_t *fine_mask, cudaStream_t s,
+                         bool exit_set) {
     ProlongArgs A;
     memset(&A, 0, sizeof(A));
     A.dim = fg.dim;
@@ -587,12 +594,14 @@ hj_status prolong_launch(const hj_grid &cg, const hj_grid &fg, const int32_t rat
         A.periodic[d] = d < fg.dim ? fg.periodic[d] : 0;
     }
     A.band = band;
-    A.all = m >= 32 ? 0xffffffffu : ((1u << m) - 1u);
+    const int sets = m + (exit_set ? 1 : 0);
+    A.all = sets >= 64 ? ~0ull : ((1ull << sets) - 1ull);
+    A.exit_bit = exit_set ? (1ull << m) : 0ull;
     const int64_t Nf = grid_nodes(fg);
-    if (A.nc[0] <= 8192) {                  // row scheme (ryz fits in shared memory)
+    if (A.nc[0] <= 4096) {                  // row scheme (ryz fits in shared memory)
         const int64_t rows = A.nf[1] * A.nf[2];
         const int rb = (int)std::min<int64_t>(rows, 148 * 8);
-        const size_t sm = (size_t)A.nc[0] * sizeof(uint32_t);
+        const size_t sm = (size_t)A.nc[0] * sizeof(uint64_t);
         if (is_mask)
             k_prolong_rows<true><<<rb, 256, sm, s>>>(A, coarse, fine_piece, fine_mask);
         else
@@ -625,8 +634,9 @@ static hj_status feedback_impl(const hj_grid &g, const hj_problem &p, const hj_f
 
 template <typename Ts>
 static hj_status label_impl(const hj_grid &g, const hj_problem &p, const hj_fields &f,
-                            const Ts *V, int64_t n_max, int32_t *label, double *margin,
-                            double *geo, int32_t *steps, cudaStream_t s) {
+                            const Ts *V, const Ts *Vexit, double exit_tol, int64_t n_max,
+                            int32_t *label, double *margin, double *geo, int32_t *steps,
+                            cudaStream_t s) {
     auto P = make_dev_problem<double, Ts>(g, p, f);
     int64_t N = grid_nodes(g);
     // one warp per coarse node; one thread per node for small control sets
@@ -636,17 +646,17 @@ static hj_status label_impl(const hj_grid &g, const hj_problem &p, const hj_fiel
     if (g.dim == 2) {
         if (thread)
             k_label_warp<Ts, 2, true><<<blocks, 256, 0, s>>>(P, V, f.piece, N, n_max, label,
-                                                             margin, geo, steps);
+                                                             margin, geo, steps, Vexit, exit_tol);
         else
             k_label_warp<Ts, 2><<<blocks, 256, 0, s>>>(P, V, f.piece, N, n_max, label, margin,
-                                                       geo, steps);
+                                                       geo, steps, Vexit, exit_tol);
     } else {
         if (thread)
             k_label_warp<Ts, 3, true><<<blocks, 256, 0, s>>>(P, V, f.piece, N, n_max, label,
-                                                             margin, geo, steps);
+                                                             margin, geo, steps, Vexit, exit_tol);
         else
             k_label_warp<Ts, 3><<<blocks, 256, 0, s>>>(P, V, f.piece, N, n_max, label, margin,
-                                                       geo, steps);
+                                                       geo, steps, Vexit, exit_tol);
     }
     HJ_CUDA(cudaGetLastError());
     return HJ_OK;
@@ -675,10 +685,11 @@ hj_status hj_coarse_feedback(const hj_grid *grid, const hj_problem *prob,
 }
 
 hj_status hj_label_subdomains(const hj_grid *cg, const hj_problem *cp, const hj_fields *cf,
-                              int32_t dtype, const void *Vc, int64_t n_max, const hj_grid *fg,
-                              const int32_t ratio[3], int32_t band, int32_t m,
-                              const int8_t *fine_piece, int32_t *label, double *margin,
-                              double *geo, int32_t *steps, uint32_t *fine_mask, void *stream) {
+                              int32_t dtype, const void *Vc, const void *Vexit, double exit_tol,
+                              int64_t n_max, const hj_grid *fg, const int32_t ratio[3],
+                              int32_t band, int32_t m, const int8_t *fine_piece, int32_t *label,
+                              double *margin, double *geo, int32_t *steps, uint64_t *fine_mask,
+                              void *stream) {
     clear_error();
     hj_status st;
     if ((st = validate_grid(cg)) != HJ_OK) return st;
@@ -686,8 +697,10 @@ hj_status hj_label_subdomains(const hj_grid *cg, const hj_problem *cp, const hj_
     if ((st = validate_problem(cg, cp)) != HJ_OK) return st;
     HJ_CHECK(cf && cf->piece, "coarse fields.piece is required");
     HJ_CHECK(Vc && label && fine_mask && fine_piece && ratio, "NULL argument");
-    HJ_CHECK(m >= 1 && m <= HJ_MAX_SUBDOMAINS, "m must be in [1, %d]", HJ_MAX_SUBDOMAINS);
+    HJ_CHECK(m >= 1 && m + (Vexit ? 1 : 0) <= HJ_MAX_SUBDOMAINS,
+             "m must be in [1, %d] (one set fewer with the exit set)", HJ_MAX_SUBDOMAINS);
     HJ_CHECK(band >= 0 && n_max >= 0, "band and n_max must be >= 0");
+    HJ_CHECK(exit_tol >= 0, "exit_tol must be >= 0");
     HJ_CHECK(cg->dim == fg->dim, "coarse and fine grids differ in dim");
     HJ_CHECK(dtype == HJ_F32 || dtype == HJ_F64, "dtype must be HJ_F32 or HJ_F64");
     for (int d = 0; d < cg->dim; ++d) {
@@ -699,12 +712,15 @@ hj_status hj_label_subdomains(const hj_grid *cg, const hj_problem *cp, const hj_
             HJ_CHECK(fg->n[d] - 1 == ratio[d] * (cg->n[d] - 1), "axis %d not nested", d);
     }
     cudaStream_t s = (cudaStream_t)stream;
-    st = dtype == HJ_F64 ? label_impl<double>(*cg, *cp, *cf, (const double *)Vc, n_max, label,
+    st = dtype == HJ_F64 ? label_impl<double>(*cg, *cp, *cf, (const double *)Vc,
+                                              (const double *)Vexit, exit_tol, n_max, label,
                                               margin, geo, steps, s)
-                         : label_impl<float>(*cg, *cp, *cf, (const float *)Vc, n_max, label,
+                         : label_impl<float>(*cg, *cp, *cf, (const float *)Vc,
+                                             (const float *)Vexit, exit_tol, n_max, label,
                                              margin, geo, steps, s);
     if (st != HJ_OK) return st;
-    return prolong_launch(*cg, *fg, ratio, band, m, label, false, fine_piece, fine_mask, s);
+    return prolong_launch(*cg, *fg, ratio, band, m, label, false, fine_piece, fine_mask, s,
+                          Vexit != nullptr);
 }
 
 }  // extern "C"

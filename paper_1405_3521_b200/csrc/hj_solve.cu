@@ -48,7 +48,7 @@ __global__ void k_count_interior(const SweepView<T> *views, unsigned long long *
 }
 
 // class array of sub-domain k over its box: piece inside S_k, -2 (ghost) outside
-__global__ void k_subdomain_classes(const uint32_t *__restrict__ mask,
+__global__ void k_subdomain_classes(const uint64_t *__restrict__ mask,
                                     const int8_t *__restrict__ piece, int k, int64_t o0,
                                     int64_t o1, int64_t o2, int64_t vn0, int64_t vn1,
                                     int64_t nodes, int64_t n0, int64_t n1, int8_t *cls) {
@@ -57,7 +57,7 @@ __global__ void k_subdomain_classes(const uint32_t *__restrict__ mask,
         int64_t li = t % vn0, r = t / vn0;
         int64_t lj = r % vn1, lk = r / vn1;
         int64_t gi = (li + o0) + n0 * ((lj + o1) + n1 * (lk + o2));
-        cls[t] = ((mask[gi] >> k) & 1u) ? piece[gi] : (int8_t)-2;
+        cls[t] = ((mask[gi] >> k) & 1ull) ? piece[gi] : (int8_t)-2;
     }
 }
 
@@ -70,17 +70,17 @@ struct AsmView {
 
 template <typename T>
 __global__ void k_assemble(const AsmView<T> *__restrict__ av, int nv,
-                           const uint32_t *__restrict__ mask, int64_t n0, int64_t n1,
+                           const uint64_t *__restrict__ mask, int64_t n0, int64_t n1,
                            int64_t N, T v_out, T *Vbar) {
     for (int64_t gi = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; gi < N;
          gi += (int64_t)gridDim.x * blockDim.x) {
-        uint32_t bits = mask[gi];
+        const uint64_t bits = mask[gi];
         int64_t i = gi % n0, r = gi / n0;
         int64_t j = r % n1, k = r / n1;
         T v = v_out;
         for (int q = 0; q < nv; ++q) {
             const AsmView<T> &a = av[q];
-            if (!((bits >> a.sub) & 1u)) continue;
+            if (!((bits >> a.sub) & 1ull)) continue;
             int64_t li = i - a.o[0], lj = j - a.o[1], lk = k - a.o[2];
             if (li < 0 || lj < 0 || lk < 0 || li >= a.vn[0] || lj >= a.vn[1] || lk >= a.vn[2])
                 continue;
@@ -96,7 +96,7 @@ __global__ void k_assemble(const AsmView<T> *__restrict__ av, int nv,
 // coordinate bound and one shared update per warp (a node of reading R9 carries every
 // bit, so per-node shared atomics contended on the same m addresses).
 __global__ void __launch_bounds__(256)
-    k_plan(const uint32_t *__restrict__ mask, int64_t N, int64_t n0, int64_t n1, int m,
+    k_plan(const uint64_t *__restrict__ mask, int64_t N, int64_t n0, int64_t n1, int m,
            int *bb /* [m][6]: lo0..2, hi0..2 */, unsigned long long *cnt) {
     __shared__ int s_lo[HJ_MAX_SUBDOMAINS][3], s_hi[HJ_MAX_SUBDOMAINS][3];
     __shared__ unsigned s_cnt[HJ_MAX_SUBDOMAINS];
@@ -109,13 +109,14 @@ __global__ void __launch_bounds__(256)
     }
     __syncthreads();
     const int lane = threadIdx.x & 31;
-    const uint32_t mm = m >= 32 ? 0xffffffffu : ((1u << m) - 1u);
+    const uint64_t mm = m >= 64 ? ~0ull : ((1ull << m) - 1ull);
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t w0 = blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31); w0 < N;
          w0 += stride) {
         const int64_t gi = w0 + lane;
-        const uint32_t bits = gi < N ? (mask[gi] & mm) : 0u;
-        uint32_t any = __reduce_or_sync(0xffffffffu, bits);
+        const uint64_t bits = gi < N ? (mask[gi] & mm) : 0ull;
+        uint64_t any = ((uint64_t)__reduce_or_sync(0xffffffffu, (unsigned)(bits >> 32)) << 32) |
+                       (uint64_t)__reduce_or_sync(0xffffffffu, (unsigned)bits);
         if (!any) continue;
         int c[3];
         c[0] = (int)(gi % n0);
@@ -123,9 +124,9 @@ __global__ void __launch_bounds__(256)
         c[1] = (int)(r % n1);
         c[2] = (int)(r / n1);
         while (any) {
-            const int k = __ffs(any) - 1;
+            const int k = __ffsll((long long)any) - 1;
             any &= any - 1;
-            const bool has = (bits >> k) & 1u;
+            const bool has = (bits >> k) & 1ull;
             const unsigned cntk = __popc(__ballot_sync(0xffffffffu, has));
             int lo[3], hi[3];
 #pragma unroll
@@ -483,8 +484,8 @@ static PartLayout part_layout(int m, const hj_subdomain *plan, int64_t max_iter)
 
 template <typename T>
 static hj_status partitioned_impl(const hj_grid &grid, const hj_problem &prob,
-                                  const hj_fields &f, const uint32_t *mask, int m,
-                                  const hj_subdomain *plan, uint32_t solve_set, double tol,
+                                  const hj_fields &f, const uint64_t *mask, int m,
+                                  const hj_subdomain *plan, uint64_t solve_set, double tol,
                                   int64_t max_iter, T *Vbar, void *ws, size_t ws_bytes,
                                   cudaStream_t s, hj_report *reps) {
     PartLayout L = part_layout<T>(m, plan, max_iter);
@@ -503,9 +504,8 @@ static hj_status partitioned_impl(const hj_grid &grid, const hj_problem &prob,
     std::vector<SweepView<T>> hv;
     std::vector<uint8_t *> chgs;
     std::vector<int> subs;
-    int64_t max_nodes = 1;
     for (int k = 0; k < m; ++k) {
-        if (!((solve_set >> k) & 1u) || plan[k].n_nodes == 0) continue;
+        if (!((solve_set >> k) & 1ull) || plan[k].n_nodes == 0) continue;
         SweepView<T> v;
         memset(&v, 0, sizeof(v));
         v.nodes = 1;
@@ -528,7 +528,6 @@ static hj_status partitioned_impl(const hj_grid &grid, const hj_problem &prob,
         k_subdomain_classes<<<blocks, 256, 0, s>>>(mask, f.piece, k, v.o[0], v.o[1], v.o[2],
                                                    v.vn[0], v.vn[1], v.nodes, n0, n1,
                                                    (int8_t *)v.cls);
-        max_nodes = std::max(max_nodes, v.nodes);
         hv.push_back(v);
         chgs.push_back((uint8_t *)(base + L.off_chg[k]));
         subs.push_back(k);
@@ -544,19 +543,45 @@ static hj_status partitioned_impl(const hj_grid &grid, const hj_problem &prob,
     }
     HJ_CUDA(cudaMemsetAsync(res, 0, (size_t)nv * max_iter * sizeof(double), s));
     HJ_CUDA(cudaMemsetAsync(cnt, 0, (size_t)2 * m * sizeof(unsigned long long), s));
-    SweepLaunch<T> SL;
-    hj_status st = sweep_prepare(grid, prob, f, hv, chgs, group, base + L.off_wl, s, SL);
-    if (st != HJ_OK) return st;
-    const SweepView<T> *d_views = &SL.d_group->v[0];
-    int blocks = (int)std::min<int64_t>((max_nodes + 255) / 256, 148 * 16);
     auto P = make_dev_problem<T, T>(grid, prob, f);
-    k_init_view<T><<<dim3(blocks, nv), 256, 0, s>>>(d_views, (T)prob.v_out, (const T *)f.g, n0,
-                                                    n1);
-    k_count_interior<T><<<dim3(blocks, nv), 256, 0, s>>>(d_views, cnt);
-    HJ_CUDA(cudaGetLastError());
+    // the views iterate together in groups of up to HJ_GROUP_VIEWS (one sweep launch, or
+    // one cooperative launch, per group); the groups run one after the other
     IterResult r;
-    st = iterate<T>(P, SL, nv, res, max_iter, tol, max_iter, s, r);
-    if (st != HJ_OK) return st;
+    r.buf.assign(nv, 0);
+    r.iters.assign(nv, 0);
+    r.converged.assign(nv, 0);
+    r.resid.assign(nv, 0.0);
+    r.ms = 0;
+    r.launches = 0;
+    int evals = prob.n_controls;
+    for (int c0 = 0; c0 < nv; c0 += HJ_GROUP_VIEWS) {
+        const int cn = std::min(nv - c0, HJ_GROUP_VIEWS);
+        std::vector<SweepView<T>> hvc(hv.begin() + c0, hv.begin() + c0 + cn);
+        std::vector<uint8_t *> chc(chgs.begin() + c0, chgs.begin() + c0 + cn);
+        int64_t mx = 1;
+        for (auto &v : hvc) mx = std::max(mx, v.nodes);
+        SweepLaunch<T> SL;
+        hj_status st = sweep_prepare(grid, prob, f, hvc, chc, group, base + L.off_wl, s, SL);
+        if (st != HJ_OK) return st;
+        evals = SL.evals;
+        const SweepView<T> *d_views = &SL.d_group->v[0];
+        int blocks = (int)std::min<int64_t>((mx + 255) / 256, 148 * 16);
+        k_init_view<T><<<dim3(blocks, cn), 256, 0, s>>>(d_views, (T)prob.v_out, (const T *)f.g,
+                                                        n0, n1);
+        k_count_interior<T><<<dim3(blocks, cn), 256, 0, s>>>(d_views, cnt + c0);
+        HJ_CUDA(cudaGetLastError());
+        IterResult rc;
+        st = iterate<T>(P, SL, cn, res + (size_t)c0 * max_iter, max_iter, tol, max_iter, s, rc);
+        if (st != HJ_OK) return st;
+        for (int q = 0; q < cn; ++q) {
+            r.buf[c0 + q] = rc.buf[q];
+            r.iters[c0 + q] = rc.iters[q];
+            r.converged[c0 + q] = rc.converged[q];
+            r.resid[c0 + q] = rc.resid[q];
+        }
+        r.ms += rc.ms;
+        r.launches += rc.launches;
+    }
     std::vector<AsmView<T>> ha(nv);
     for (int q = 0; q < nv; ++q) {
         for (int d = 0; d < 3; ++d) {
@@ -582,7 +607,7 @@ static hj_status partitioned_impl(const hj_grid &grid, const hj_problem &prob,
             rp.residual = r.resid[q];
             rp.converged = r.converged[q];
             rp.node_updates = (int64_t)interior[q] * prob.n_controls * r.iters[q];
-            rp.evaluated_updates = (int64_t)interior[m + q] * SL.evals;
+            rp.evaluated_updates = (int64_t)interior[m + q] * evals;
             rp.device_ms = r.ms;
             rp.launches = q == 0 ? r.launches + nv + 3 + (f.speed ? 1 : 0) : 0;  // counted once
         }
@@ -608,15 +633,15 @@ __global__ void k_piece_only(const int8_t *__restrict__ piece, int i, int64_t N,
 template <typename T>
 __global__ void k_ra_masks(const T *__restrict__ Vaux, int m, int64_t N,
                            const int8_t *__restrict__ piece, double thr, T *Vmin,
-                           uint32_t *mask) {
+                           uint64_t *mask) {
     for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < N;
          j += (int64_t)gridDim.x * blockDim.x) {
         T v = Vaux[j];
         for (int i = 1; i < m; ++i) v = fmin(v, Vaux[(int64_t)i * N + j]);
-        uint32_t bits = 0;
+        uint64_t bits = 0;
         for (int i = 0; i < m; ++i) {
             const double d = fabs((double)Vaux[(int64_t)i * N + j] - (double)v);
-            if (piece[j] == i || d <= thr) bits |= 1u << i;
+            if (piece[j] == i || d <= thr) bits |= 1ull << i;
         }
         Vmin[j] = v;
         mask[j] = bits;
@@ -632,8 +657,8 @@ template <typename T>
 static hj_status ra_impl(const hj_grid &cg, const hj_problem &cp, const hj_fields &cf, int m,
                          double C, double M, double q, double tol, int64_t max_iter,
                          const hj_grid &fg, const int32_t ratio[3], int32_t band,
-                         const int8_t *fine_piece, T *Vaux, T *Vmin, uint32_t *cmask,
-                         uint32_t *fmask, void *ws, size_t ws_bytes, cudaStream_t s,
+                         const int8_t *fine_piece, T *Vaux, T *Vmin, uint64_t *cmask,
+                         uint64_t *fmask, void *ws, size_t ws_bytes, cudaStream_t s,
                          hj_report *reps) {
     const int64_t N = grid_nodes(cg);
     if (ws_bytes < ra_ws<T>(cg, max_iter)) {
@@ -718,7 +743,7 @@ hj_status hj_ra_subdomains(const hj_grid *cg, const hj_problem *cp, const hj_fie
                            int32_t dtype, int32_t m, double C, double M, double q, double tol,
                            int64_t max_iter, const hj_grid *fg, const int32_t ratio[3],
                            int32_t band, const int8_t *fine_piece, void *Vaux, void *Vmin,
-                           uint32_t *coarse_mask, uint32_t *fine_mask, void *workspace,
+                           uint64_t *coarse_mask, uint64_t *fine_mask, void *workspace,
                            size_t ws_bytes, void *stream, hj_report *reports) {
     clear_error();
     hj_status st;
@@ -753,7 +778,7 @@ hj_status hj_ra_subdomains(const hj_grid *cg, const hj_problem *cp, const hj_fie
                           ws_bytes, s, reports);
 }
 
-hj_status hj_partition_plan(const hj_grid *grid, const uint32_t *fine_mask, int32_t m,
+hj_status hj_partition_plan(const hj_grid *grid, const uint64_t *fine_mask, int32_t m,
                             int32_t dtype, int64_t max_iter, hj_subdomain *plan,
                             size_t *ws_bytes, void *stream) {
     clear_error();
@@ -816,8 +841,8 @@ hj_status hj_partition_plan(const hj_grid *grid, const uint32_t *fine_mask, int3
 }
 
 hj_status hj_solve_partitioned(const hj_grid *grid, const hj_problem *prob,
-                               const hj_fields *fields, int32_t dtype, const uint32_t *fine_mask,
-                               int32_t m, const hj_subdomain *plan, uint32_t solve_set, double tol,
+                               const hj_fields *fields, int32_t dtype, const uint64_t *fine_mask,
+                               int32_t m, const hj_subdomain *plan, uint64_t solve_set, double tol,
                                int64_t max_iter, void *Vbar, void *workspace, size_t ws_bytes,
                                void *stream, hj_report *reports) {
     clear_error();

@@ -54,8 +54,8 @@ struct WorkList {
 
 template <typename T>
 struct SweepGroup {        // device-resident description of one launch
-    SweepView<T> v[HJ_MAX_SUBDOMAINS];
-    TileView<T> t[HJ_MAX_SUBDOMAINS];
+    SweepView<T> v[HJ_GROUP_VIEWS];
+    TileView<T> t[HJ_GROUP_VIEWS];
     WorkList wl;
     int total_tiles;
     int dense;             // 1: visit every tile every sweep, one CTA per tile, no list
@@ -673,29 +673,33 @@ __global__ void __launch_bounds__(256, 4)
 
 // ---------------------------------------------------------------------------
 // k_sweep_field2d for the affine problems whose controls all move the foot by the same
-// amount along axis 0 (u_k = (u0, u1_k): config 5's f = (x2, a - x1/2)).  Then
-// d0 = D0 + S0 u0, its cell i0 and weight w0 are the node's, not the control's, and the
-// bilinear interpolant of control k is  lerp(X(i1_k), X(i1_k + 1), w1_k)  with
+// amount along axis 0 (u_k = (u0, u1_k), no speed field: config 5's f = (x2, a - x1/2)).
+// Then d0 = D0 + S0 u0, its cell i0 and weight w0 are the node's, not the control's, and
+// the bilinear interpolant of control k is  lerp(X(i1_k), X(i1_k + 1), w1_k)  with
 // X(j) = lerp(V(i0, j), V(i0 + 1, j), w0) the x-interpolated column at the node's foot
-// abscissa — exactly the two inner lerps k_sweep_field2d computes.  With the controls
-// sorted by u1 (host; the min over controls is order-free), d1_k is non-decreasing, so
-// the node walks its column once: each X(j) is formed once (one pair of loads + one
-// lerp per row instead of four gathers + two lerps per control) and the cell index
-// i1_k = floor(d1_k) advances by comparison instead of a floor per control.  Every value
-// is the one k_sweep_field2d forms: bit-identical iterates (asserted in the parity
-// suite).  Tiles whose footprint leaves the view take k_sweep_field2d's general path.
+// abscissa — exactly the two inner lerps k_sweep_field2d forms.  With the controls sorted
+// by u1 (host; the min over controls is order-free) the rows the controls touch are
+// [i1_first, i1_last + 1]: the node forms that column once (two loads and one lerp per
+// row, into its own column of shared memory — lane = bank, conflict-free) and then each
+// control costs one floor, two shared loads and the y-lerp instead of four gathers and
+// three lerps.  Every value is the one k_sweep_field2d forms: bit-identical iterates
+// (asserted in the parity suite).  Tiles whose footprint leaves the view take
+// k_sweep_field2d's general path.
 // ---------------------------------------------------------------------------
 template <typename T>
 struct ColCtrl {
     T u0;                              // the shared axis-0 control component
     T u1[HJ_MAX_CONTROLS];             // axis-1 components, ascending
     T csq[HJ_MAX_CONTROLS];            // |a_k|^2 in the same order
+    int rows;                          // column rows per node the shared buffer holds
 };
 
 template <typename T, bool KRUZ, int RY>
 __global__ void __launch_bounds__(256, 4)
     k_sweep_field2d_col(const DevProblem<T, T> P, const ColCtrl<T> C,
                         const SweepGroup<T> *__restrict__ G, int64_t it, double tol) {
+    extern __shared__ __align__(16) unsigned char col_dyn[];
+    T *__restrict__ X = reinterpret_cast<T *>(col_dyn) + threadIdx.x;   // row r at X[256 r]
     HJ_LIST_BEGIN(G, it, tol)
     const int vn0 = (int)vw.vn[0], vn1 = (int)vw.vn[1];
     const T *__restrict__ Vi = vw.V[it & 1];
@@ -723,10 +727,9 @@ __global__ void __launch_bounds__(256, 4)
             vnew = P.g ? P.g[gidx] : T(0);
         } else {
             const T x0 = fma((T)gi[0], P.dx[0], P.lo[0]), x1 = fma((T)gi[1], P.dx[1], P.lo[1]);
-            const T cs = P.speed ? P.speed[gidx] : T(1);
             const T D0 = P.hdx[0] * fma(P.A[0], x0, fma(P.A[1], x1, P.b[0]));
             const T D1 = P.hdx[1] * fma(P.A[3], x0, fma(P.A[4], x1, P.b[1]));
-            const T S0 = P.hdx[0] * cs, S1 = P.hdx[1] * cs;
+            const T S0 = P.hdx[0], S1 = P.hdx[1];       // (no speed field: c = 1)
             T base;
             if (KRUZ) {
                 base = P.kcost;
@@ -736,26 +739,23 @@ __global__ void __launch_bounds__(256, 4)
             }
             const T hlr = P.h * P.lr;
             T best = (T)INFINITY;
-            if (fast) {
-                T w0, w1;
-                const int i0 = floor_split(fma(S0, C.u0, D0), w0);
-                T d1 = fma(S1, C.u1[0], D1);
-                const int j = floor_split(d1, w1);
-                T jf = (T)j;                              // floor(d1), exactly
-                const T *__restrict__ p = Vi + t + i0 + (int64_t)vn0 * j;
-                T Xa = lerp<T>(__ldg(p), __ldg(p + 1), w0);
-                p += vn0;
-                T Xb = lerp<T>(__ldg(p), __ldg(p + 1), w0);
-#pragma unroll 2
+            T w0, wl, wh;
+            const int i0 = floor_split(fma(S0, C.u0, D0), w0);
+            const int jlo = floor_split(fma(S1, C.u1[0], D1), wl);
+            const int nrows = floor_split(fma(S1, C.u1[P.K - 1], D1), wh) + 2 - jlo;
+            if (fast && nrows <= C.rows) {
+                // the column X(jlo .. jlo + nrows - 1) at the foot abscissa
+                const T *__restrict__ p = Vi + t + i0 + (int64_t)vn0 * jlo;
+#pragma unroll 4
+                for (int r = 0; r < nrows; ++r) {
+                    X[256 * r] = lerp<T>(__ldg(p), __ldg(p + 1), w0);
+                    p += vn0;
+                }
+#pragma unroll 4
                 for (int k = 0; k < P.K; ++k) {
-                    d1 = fma(S1, C.u1[k], D1);
-                    while (d1 >= jf + T(1)) {                 // next cell row of the column
-                        jf += T(1);
-                        Xa = Xb;
-                        p += vn0;
-                        Xb = lerp<T>(__ldg(p), __ldg(p + 1), w0);
-                    }
-                    const T I = lerp<T>(Xa, Xb, d1 - jf);
+                    T w1;
+                    const int j = floor_split(fma(S1, C.u1[k], D1), w1) - jlo;
+                    const T I = lerp<T>(X[256 * j], X[256 * j + 256], w1);
                     const T ck = KRUZ ? base : fma(hlr, C.csq[k], base);
                     best = fmin(best, fma(P.beta, I, ck));
                 }
@@ -784,6 +784,7 @@ __global__ void __launch_bounds__(256, 4)
     changed_ = tile_finish(G, v, tile, it, rmax, changed, evaluated);
     HJ_LIST_END(G, it)
 }
+
 
 // ---------------------------------------------------------------------------
 // Dubins car (§2 dynamics family; BASELINE config 4): the (x,y) part of
@@ -944,7 +945,7 @@ inline int64_t tiles_finest(const int64_t vn[3]) {
 // shares the same region, so the larger of the two is reserved
 inline int64_t wl_bytes_for(int64_t T) {
     const int64_t lists = 3 * 4 * T + 2 * 4 * ((T + 31) / 32) + 64 + 4 * 256;
-    const int64_t coop = 4 * T * (4 * 8 + 2 * 4) + 16 * 256 + 8 * HJ_MAX_SUBDOMAINS;
+    const int64_t coop = 4 * T * (4 * 8 + 2 * 4) + 16 * 256 + 8 * HJ_GROUP_VIEWS;
     return std::max(lists, coop);
 }
 
@@ -1207,6 +1208,15 @@ hj_status sweep_prepare(const hj_grid &g, const hj_problem &p, const hj_fields &
         bool shared = true;
         for (int k = 1; k < p.n_controls; ++k)
             if (p.controls[k][0] != p.controls[0][0]) shared = false;
+        // column rows per node: the feet's axis-1 span plus the cell's upper row and a
+        // floor's worth of slack; the shared column buffer is rows x 256 values
+        double u1min = INFINITY, u1max = -INFINITY;
+        for (int k = 0; k < p.n_controls; ++k) {
+            u1min = std::min(u1min, p.controls[k][1]);
+            u1max = std::max(u1max, p.controls[k][1]);
+        }
+        const int rows = (int)std::ceil(p.h / grid_spacing(g, 1) * (u1max - u1min)) + 3;
+        if (rows * 256 * (int)sizeof(T) > 160 * 1024) shared = false;
         if (shared) {
             std::vector<int> ord(p.n_controls);
             for (int k = 0; k < p.n_controls; ++k) ord[k] = k;
@@ -1215,6 +1225,7 @@ hj_status sweep_prepare(const hj_grid &g, const hj_problem &p, const hj_fields &
             });
             L.col = true;
             memset(&L.colctrl, 0, sizeof(L.colctrl));
+            L.colctrl.rows = rows;
             L.colctrl.u0 = (T)p.controls[0][0];
             for (int k = 0; k < p.n_controls; ++k) {
                 const int q = ord[k];
@@ -1241,6 +1252,11 @@ hj_status sweep_prepare(const hj_grid &g, const hj_problem &p, const hj_fields &
         set_error("sweep_kernel %d requested, but the problem does not qualify for the local "
                   "kernel (2-D, f = c(x) u_a, foot within one cell, no periodic axis)", want);
         return HJ_ERR_UNSUPPORTED;
+    }
+    if (views.empty() || views.size() > HJ_GROUP_VIEWS) {
+        set_error("internal: a sweep group holds 1..%d views (got %zu)", HJ_GROUP_VIEWS,
+                  views.size());
+        return HJ_ERR_INVALID;
     }
     SweepGroup<T> hg;
     memset(&hg, 0, sizeof(hg));
@@ -1537,7 +1553,7 @@ hj_status sweep_coop(const DevProblem<T, T> &P, const SweepLaunch<T> &L, int64_t
     S.items[0] = (int32_t *)c.take(4 * tot);
     S.items[1] = (int32_t *)c.take(4 * tot);
     S.count = (int32_t *)c.take(16);
-    S.stop = (int64_t *)c.take(8 * HJ_MAX_SUBDOMAINS);
+    S.stop = (int64_t *)c.take(8 * HJ_GROUP_VIEWS);
     HJ_CUDA(cudaMemsetAsync(S.count, 0, 16, s));
     if (tot > 0) {
         const int blocks = (int)std::min<int64_t>((tot + 255) / 256, 148 * 8);
@@ -1572,19 +1588,30 @@ hj_status sweep_coop(const DevProblem<T, T> &P, const SweepLaunch<T> &L, int64_t
     return HJ_OK;
 }
 
+template <typename T, bool KRUZ, int RY>
+static void launch_col(const DevProblem<T, T> &P, const SweepLaunch<T> &L, int64_t it, double tol,
+                       cudaStream_t s) {
+    auto kern = k_sweep_field2d_col<T, KRUZ, RY>;
+    const size_t smem = (size_t)L.colctrl.rows * 256 * sizeof(T);
+    static size_t attr[64] = {0};      // dynamic shared memory opted in, per device
+    const int dev = current_device();
+    if (smem > attr[dev]) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr[dev] = smem;
+    }
+    kern<<<grid_for(kern, 256, smem, L.total_tiles, L.dense), 256, smem, s>>>(P, L.colctrl,
+                                                                              L.d_group, it, tol);
+}
+
 template <typename T, int DYN, bool KRUZ>
 static void launch_field(const DevProblem<T, T> &P, const SweepLaunch<T> &L, int64_t it,
                          double tol, cudaStream_t s) {
     if constexpr (DYN == HJ_DYN_AFFINE) {
         if (L.col) {
             if (L.dense)
-                k_sweep_field2d_col<T, KRUZ, 4>
-                    <<<grid_for(k_sweep_field2d_col<T, KRUZ, 4>, 256, 0, L.total_tiles, true),
-                       256, 0, s>>>(P, L.colctrl, L.d_group, it, tol);
+                launch_col<T, KRUZ, 4>(P, L, it, tol, s);
             else
-                k_sweep_field2d_col<T, KRUZ, 1>
-                    <<<grid_for(k_sweep_field2d_col<T, KRUZ, 1>, 256, 0, L.total_tiles), 256, 0,
-                       s>>>(P, L.colctrl, L.d_group, it, tol);
+                launch_col<T, KRUZ, 1>(P, L, it, tol, s);
             return;
         }
     }

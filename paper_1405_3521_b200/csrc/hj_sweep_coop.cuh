@@ -34,8 +34,8 @@ __device__ __forceinline__ void opaque(float &x) { asm volatile("" : "+f"(x)); }
 __device__ __forceinline__ void opaque(double &x) { asm volatile("" : "+d"(x)); }
 
 struct CoopState {
-    int64_t mt_base[HJ_MAX_SUBDOMAINS + 1];   // first global mini-tile id of each view
-    int32_t mt0[HJ_MAX_SUBDOMAINS], mt1[HJ_MAX_SUBDOMAINS], mt2[HJ_MAX_SUBDOMAINS];
+    int64_t mt_base[HJ_GROUP_VIEWS + 1];   // first global mini-tile id of each view
+    int32_t mt0[HJ_GROUP_VIEWS], mt1[HJ_GROUP_VIEWS], mt2[HJ_GROUP_VIEWS];
     unsigned long long *imask;      // [total] fast interior nodes (class -1)
     unsigned long long *emask;      // [total] interior nodes on the box edge (class -3)
     unsigned long long *dmask[2];   // [total] nodes to evaluate in sweep n (parity n)
@@ -46,7 +46,7 @@ struct CoopState {
     int dubins;                     // 3-D Dubins views: 8 x 8 mini-tiles per heading plane
     int n_views;
     int64_t total;
-    int32_t vorder[HJ_MAX_SUBDOMAINS];   // cluster mode: views by decreasing size
+    int32_t vorder[HJ_GROUP_VIEWS];   // cluster mode: views by decreasing size
     int cluster;                    // 1: cluster mode (k_sweep_local2d_coop<..., CL>)
 };
 
@@ -598,11 +598,11 @@ __global__ void __launch_bounds__(CoopNW<T>::nw * 32, CoopNW<T>::minb)
     __shared__ int wcnt[COOP_NW];
     // per-CTA max of the sweep's |V^{n+1} - V^n| as the bits of a T >= 0 (monotone as
     // unsigned: native shared atomicMax, no CAS loop), evaluated-node count
-    __shared__ typename CoopBits<T>::U cres[HJ_MAX_SUBDOMAINS];
-    __shared__ unsigned cwork[HJ_MAX_SUBDOMAINS];
+    __shared__ typename CoopBits<T>::U cres[HJ_GROUP_VIEWS];
+    __shared__ unsigned cwork[HJ_GROUP_VIEWS];
     // the views, copied once: the grid barrier invalidates L1, so reading G every sweep
     // would put a global round trip in front of every dependent load
-    __shared__ SweepView<T> sview[HJ_MAX_SUBDOMAINS];
+    __shared__ SweepView<T> sview[HJ_GROUP_VIEWS];
     // local class: the quadrant control tables ax | ay | ck, [3][4][KQ]
     __shared__ T sctl[EV == 0 ? 12 * KQ : 1];
     // Dubins: extreme |h w a_k / dth| of each sign group (coop_eval_dubins)
@@ -666,7 +666,7 @@ __global__ void __launch_bounds__(CoopNW<T>::nw * 32, CoopNW<T>::minb)
             t_s = t_l = t_e = t_m = t_q = 0;
             qitems = 0;
         }
-        if (threadIdx.x < HJ_MAX_SUBDOMAINS) {
+        if (threadIdx.x < HJ_GROUP_VIEWS) {
             cres[threadIdx.x] = 0;
             cwork[threadIdx.x] = 0u;
         }

@@ -21,7 +21,7 @@ _lib = None
 HJ_OK, HJ_ERR_INVALID, HJ_ERR_CUDA, HJ_ERR_NOT_CONVERGED, HJ_ERR_UNSUPPORTED, HJ_ERR_WORKSPACE = range(6)
 HJ_F32, HJ_F64 = 0, 1
 MAX_CONTROLS = 128
-MAX_SUBDOMAINS = 32
+MAX_SUBDOMAINS = 64          # sets of a uint64 membership mask (pieces + exit set)
 
 
 class HJError(RuntimeError):
@@ -98,12 +98,13 @@ def lib():
         L.hj_solve_workspace_bytes.restype = ctypes.c_size_t
         L.hj_solve.argtypes = [G, P, F, i32, vp, ctypes.c_double, i64, vp, ctypes.c_size_t, vp, R]
         L.hj_coarse_feedback.argtypes = [G, P, F, i32, vp, vp, vp, vp]
-        L.hj_label_subdomains.argtypes = [G, P, F, i32, vp, i64, G, ctypes.POINTER(i32), i32, i32,
-                                          vp, vp, vp, vp, vp, vp, vp]
+        L.hj_label_subdomains.argtypes = [G, P, F, i32, vp, vp, ctypes.c_double, i64, G,
+                                          ctypes.POINTER(i32), i32, i32, vp, vp, vp, vp, vp, vp,
+                                          vp]
         L.hj_partition_plan.argtypes = [G, vp, i32, i32, i64, S, ctypes.POINTER(ctypes.c_size_t),
                                         vp]
         L.hj_assign_subdomains.argtypes = [i32, S, i32, ctypes.POINTER(i32)]
-        L.hj_solve_partitioned.argtypes = [G, P, F, i32, vp, i32, S, ctypes.c_uint32,
+        L.hj_solve_partitioned.argtypes = [G, P, F, i32, vp, i32, S, ctypes.c_uint64,
                                            ctypes.c_double, i64, vp, vp, ctypes.c_size_t, vp, R]
         L.hj_ra_workspace_bytes.argtypes = [G, i32, i64]
         L.hj_ra_workspace_bytes.restype = ctypes.c_size_t
@@ -245,21 +246,24 @@ def hj_coarse_feedback(dp: DeviceProblem, V, stream=None):
 
 
 def hj_label_subdomains(coarse: DeviceProblem, Vc, n_max, fine: DeviceProblem, ratio, band, m,
-                        stream=None):
+                        Vexit=None, exit_tol=0.0, stream=None):
+    """Labels (piece, -1 unlabelled, -2 exit set when Vexit is given) and the fine uint64
+    membership mask (returned as an int64 tensor holding the bits)."""
     Nc, Nf = coarse.N, fine.N
-    dev = coarse.device
     label = _buf(coarse, "label", Nc, torch.int32)
     margin = _buf(coarse, "margin", Nc, torch.float64)
     geo = _buf(coarse, "geo", Nc, torch.float64)
     steps = _buf(coarse, "steps", Nc, torch.int32)
-    mask = _buf(fine, "mask", Nf, torch.int32)   # uint32 bits
+    mask = _buf(fine, "mask", Nf, torch.int64)   # uint64 bits
     r = (ctypes.c_int32 * 3)(*[int(ratio[d]) if d < len(ratio) else 1 for d in range(3)])
     _check(lib().hj_label_subdomains(
         ctypes.byref(coarse.grid), ctypes.byref(coarse.cprob), ctypes.byref(coarse.fields),
-        _code(coarse.dtype), Vc.data_ptr(), int(n_max), ctypes.byref(fine.grid), r, int(band),
-        int(m), fine.piece.data_ptr(), label.data_ptr(), margin.data_ptr(), geo.data_ptr(),
+        _code(coarse.dtype), Vc.data_ptr(), Vexit.data_ptr() if Vexit is not None else None,
+        float(exit_tol), int(n_max), ctypes.byref(fine.grid), r, int(band), int(m),
+        fine.piece.data_ptr(), label.data_ptr(), margin.data_ptr(), geo.data_ptr(),
         steps.data_ptr(), mask.data_ptr(), _stream(stream)))
-    return dict(label=label, margin=margin, geo=geo, steps=steps, mask=mask)
+    return dict(label=label, margin=margin, geo=geo, steps=steps, mask=mask,
+                n_sets=m + (1 if Vexit is not None else 0))
 
 
 def hj_partition_plan(fine: DeviceProblem, mask, m, max_iter=None, stream=None):
@@ -292,7 +296,7 @@ def hj_solve_partitioned(fine: DeviceProblem, mask, m, plan, ws_bytes, solve_set
     reps = (hj_report * m)()
     _check(lib().hj_solve_partitioned(
         ctypes.byref(fine.grid), ctypes.byref(fine.cprob), ctypes.byref(fine.fields),
-        _code(fine.dtype), mask.data_ptr(), int(m), plan, ctypes.c_uint32(solve_set), float(tol),
+        _code(fine.dtype), mask.data_ptr(), int(m), plan, ctypes.c_uint64(solve_set), float(tol),
         int(max_iter), Vbar.data_ptr(), workspace.data_ptr(), workspace.numel(), _stream(stream),
         reps))
     return Vbar, [reps[k].as_dict() if (solve_set >> k) & 1 else None for k in range(m)]
@@ -311,13 +315,13 @@ def hj_ra_subdomains(coarse: DeviceProblem, m, C=1.0, M=1.0, q=0.5, fine: Device
     td = _torch_dtype(coarse.dtype)
     Vaux = _buf(coarse, "ra_Vaux", m * Nc, td)
     Vmin = _buf(coarse, "ra_Vmin", Nc, td)
-    cmask = _buf(coarse, "ra_cmask", Nc, torch.int32)
+    cmask = _buf(coarse, "ra_cmask", Nc, torch.int64)
     need = L.hj_ra_workspace_bytes(ctypes.byref(coarse.grid), _code(coarse.dtype), int(max_iter))
     ws = _buf(coarse, "ra_ws", need, torch.uint8)
     fmask = None
     r = (ctypes.c_int32 * 3)(1, 1, 1)
     if fine is not None:
-        fmask = _buf(fine, "mask", fine.N, torch.int32)
+        fmask = _buf(fine, "mask", fine.N, torch.int64)
         for d in range(len(ratio)):
             r[d] = int(ratio[d])
     reps = (hj_report * m)()

@@ -480,7 +480,7 @@ def test_p14_prolong_mask_matches_label_prolongation():
     lab = rng.integers(-1, m, size=cg.size).astype(np.int32)
     fpiece = np.full(fg.size, -1, np.int8)
     fpiece[rng.choice(fg.size, 10, replace=False)] = rng.integers(0, m, 10)
-    cmask = np.where(lab < 0, (1 << m) - 1, 1 << np.maximum(lab, 0)).astype(np.uint32)
+    cmask = np.where(lab < 0, (1 << m) - 1, 1 << np.maximum(lab, 0)).astype(np.uint64)
     for band in (0, 2):
         a = oracle.prolong(cg, fg, (4, 4), band, lab, m, fpiece)
         b = oracle.prolong_mask(cg, fg, (4, 4), band, cmask, m, fpiece)
@@ -703,7 +703,7 @@ def test_p19_subdomain_ghosts_and_targets():
     allowed[5, 7] = True            # ... with one gap
     allowed[2, 8:] = False          # and the far piece-1 node's row cut off
     allowed[2, 9] = False
-    mask = allowed.reshape(-1).astype(np.uint32)     # bit 0 = S_0
+    mask = allowed.reshape(-1).astype(np.uint64)     # bit 0 = S_0
     mask[piece.reshape(-1) == 1] |= 2
     p = mk_problem(grid, W.axis_controls(), piece.reshape(-1), tol=1e-14)
     o = oracle.OracleProblem(p)
@@ -759,3 +759,69 @@ def test_p21_box_tolerance_only_moves_exact_box_feet():
             foot = np.array([i, j]) + snapped[k, :2]     # h = dx: one cell per unit
             if np.any(foot < 0) or np.any(foot > n - 1):
                 assert b == beta * p.v_out + (1 - beta)
+
+
+# ---------------------------------------------------------------------------
+# P22  the exit set (reading R9b): the box boundary is a piece of Gamma of its own
+#      (Theorem 2.1 decomposes all of Gamma; exit cost v_out, Tdef line 243).
+#  (a) the exit test: an unlabelled node joins the exit set iff Vc >= Vexit - tol
+#      (inclusive), labelled nodes never;
+#  (b) prolongation: label -2 -> the exit set (bit m) only, -1 -> all m + 1 sets, by
+#      brute-force dilation;
+#  (c) Kruzkov with no target: Vexit = 1 = "never reached" everywhere (to rounding);
+#  (d) Proposition 4.1 still holds with the exit set on the regulator geometry
+#      (config 5, reduced): the assembled field is never below the whole-grid solution
+#      and within O(dx) of it, the exit set is used, and it shrinks the sets.
+# ---------------------------------------------------------------------------
+def test_p22a_exit_test_inclusive():
+    lab = np.array([-1, -1, -1, 3, -1, 0], np.int32)
+    Vc = np.array([0.5, 0.5, 0.75, 0.0, 1.0, 2.0])
+    Vexit = np.array([0.75, 0.75 + 2 ** -30, 0.75, 9.0, 1.0, 2.0])
+    out = oracle.exit_labels(lab, Vc, Vexit, 0.25)
+    assert list(out) == [-2, -1, -2, 3, -2, 0]
+
+
+def test_p22b_prolong_exit_set_bruteforce():
+    rng = np.random.default_rng(22)
+    cg = W.Grid((9, 7), (0.0, 0.0), (1.0, 0.75), (False, False))
+    fg = W.Grid((33, 25), (0.0, 0.0), (1.0, 0.75), (False, False))
+    m = 4
+    lab = rng.integers(-2, m, size=cg.size).astype(np.int32)
+    fpiece = np.full(fg.size, -1, np.int8)
+    fpiece[rng.choice(fg.size, 8, replace=False)] = rng.integers(0, m, 8)
+    band = 2
+    mask = oracle.prolong(cg, fg, (4, 4), band, lab, m, fpiece, exit_set=True).reshape(25, 33)
+    L = lab.reshape(7, 9)
+    for k in range(m + 1):
+        seed = np.zeros((25, 33), bool)
+        member = (L == k) if k < m else (L == -2)
+        seed[::4, ::4] = member | (L == -1)
+        rad = 4 + band
+        dil = ndimage.binary_dilation(seed, structure=np.ones((2 * rad + 1, 2 * rad + 1), bool))
+        if k < m:
+            dil |= (fpiece.reshape(25, 33) == k)
+        got = ((mask >> np.uint64(k)) & np.uint64(1)).astype(bool)
+        assert np.array_equal(got, dil), k
+    assert int(mask.max()) < (1 << (m + 1))
+
+
+def test_p22c_kruzkov_exit_solution_is_one():
+    cfg = W.make(2, scale=32 / 1024, ratio=1)
+    Ve = oracle.exit_solution(cfg.coarse)
+    assert np.abs(Ve - 1.0).max() <= 1e-15       # beta * 1 + (1 - beta), rounded
+
+
+def test_p22d_isa_with_exit_set_proposition_4_1():
+    cfg = W.make(5, scale=128 / 16384, ratio=4)
+    V, _, _ = oracle.OracleProblem(cfg.fine).solve()
+    res = oracle.isa(cfg.fine, cfg.coarse, cfg.ratio, cfg.band, cfg.m, cfg.n_max_steps,
+                     exit_set=True)
+    r9 = oracle.isa(cfg.fine, cfg.coarse, cfg.ratio, cfg.band, cfg.m, cfg.n_max_steps,
+                    exit_set=False)
+    assert res["n_sets"] == cfg.m + 1 and (res["labels"] == -2).sum() > 0
+    d = res["Vbar"] - V
+    dxc = cfg.coarse.grid.spacing(0)
+    assert d.min() >= -10 * cfg.fine.tol and d.max() <= dxc
+    cover = lambda r: sum(int(((r["mask"] >> np.uint64(k)) & np.uint64(1)).sum())
+                          for k in range(r["n_sets"]))
+    assert cover(res) < 0.9 * cover(r9)

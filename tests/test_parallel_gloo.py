@@ -52,10 +52,10 @@ def _worker(rank, world, port, cfg_args, ret):
             Vk.append(of.solve_subdomain(mask, k)[0])
         else:
             Vk.append(np.full(of.N, cfg.fine.v_out))
-    owned_mask = np.where(((mask[:, None] >> np.arange(cfg.m)) & 1).astype(bool) &
+    owned_mask = np.where(((mask[:, None] >> np.arange(cfg.m, dtype=np.uint64)) & np.uint64(1)).astype(bool) &
                           np.array([(mine >> k) & 1 for k in range(cfg.m)], bool)[None, :],
                           1, 0)
-    bits = (owned_mask * (1 << np.arange(cfg.m))).sum(axis=1).astype(np.uint32)
+    bits = (owned_mask * (1 << np.arange(cfg.m))).sum(axis=1).astype(np.uint64)
     local = oracle.assemble(bits, Vk, cfg.fine.v_out)
     t = torch.from_numpy(local.copy())
     pipeline.gather_min(t)
@@ -75,5 +75,6 @@ def test_two_ranks_min_gather_reproduces_single_process():
     assert mine0 & mine1 == 0 and (mine0 | mine1) == (1 << 4) - 1   # a partition of the set
     assert set(owners) == {0, 1}
     cfg = W.make(*cfg_args)
-    full = oracle.isa(cfg.fine, cfg.coarse, cfg.ratio, cfg.band, cfg.m, cfg.n_max_steps)
+    full = oracle.isa(cfg.fine, cfg.coarse, cfg.ratio, cfg.band, cfg.m, cfg.n_max_steps,
+                      exit_set=False)
     assert np.array_equal(V0, full["Vbar"])

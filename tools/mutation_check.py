@@ -38,8 +38,13 @@ MUTATIONS_ALL = [
      "                if (!any || Vk[k][j] > v) v = Vk[k][j];"),
     ("prolongation radius -1", "            long reach = ratio[d] + band;",
      "            long reach = ratio[d] + band - 1;"),
-    ("label -1 -> no bits", "cm[j] = coarse_label[j] < 0 ? all : (1u << coarse_label[j]);",
-     "cm[j] = coarse_label[j] < 0 ? 0u : (1u << coarse_label[j]);"),
+    ("label -1 -> no bits", "        else cm[j] = all;", "        else cm[j] = 0ull;"),
+    ("label -2 -> all sets", "        else if (l == -2) cm[j] = exit_set ? (1ull << m) : 0ull;",
+     "        else if (l == -2) cm[j] = all;"),
+    ("exit test strict", "if (labels[j] == -1 && Vc[j] >= Vexit[j] - tol) labels[j] = -2;",
+     "if (labels[j] == -1 && Vc[j] > Vexit[j] - tol) labels[j] = -2;"),
+    ("exit test on labelled nodes", "if (labels[j] == -1 && Vc[j] >= Vexit[j] - tol) labels[j] = -2;",
+     "if (labels[j] < 0 || Vc[j] >= Vexit[j] - tol) labels[j] = -2;"),
     ("box tolerance 1e-2", "#define OR_BOX_EPS 1e-6", "#define OR_BOX_EPS 1e-2"),
     ("beta = exp(-lambda h)", "return 1.0 / (1.0 + p->lam * p->h);", "return exp(-p->lam * p->h);"),
     ("Kruzkov cost dropped", "(p->cost == OR_COST_KRUZKOV) ? (1.0 - beta)",
