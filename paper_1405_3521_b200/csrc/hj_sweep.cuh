@@ -557,15 +557,14 @@ __global__ void __launch_bounds__(256, 2)
 // Tile 32 x 8, one node per thread.
 // ---------------------------------------------------------------------------
 // floor(d) and d - floor(d) without the conversion (XU) pipe, |d| < 2^22:
-// t = RN(d + 1.5 2^23) carries round(d) in its mantissa.  Same values as
-// floor() / d - floor(d) (fp64 keeps floor(): the double pipes are not the limit there).
+// t = RM(d + 1.5 2^23) (rounded toward -inf: the sum's ulp is 1, so t = 1.5 2^23 +
+// floor(d) exactly) carries floor(d) in its mantissa.  Same values as floor() /
+// d - floor(d) (fp64 keeps floor(): the double pipes are not the limit there).
 __device__ __forceinline__ int floor_split(float d, float &w) {
-    const float t = __fadd_rn(d, 12582912.0f);
-    const float r = __fsub_rn(t, 12582912.0f);
-    const bool up = r > d;
-    const float fl = up ? r - 1.0f : r;
+    const float t = __fadd_rd(d, 12582912.0f);
+    const float fl = __fsub_rn(t, 12582912.0f);
     w = d - fl;
-    return (__float_as_int(t) - 0x4B400000) - (up ? 1 : 0);
+    return __float_as_int(t) - 0x4B400000;
 }
 __device__ __forceinline__ int floor_split(double d, double &w) {
     const double fl = floor(d);
@@ -694,12 +693,15 @@ struct ColCtrl {
     int rows;                          // column rows per node the shared buffer holds
 };
 
-template <typename T, bool KRUZ, int RY>
+// KC > 0: the control count, known at compile time (the loop unrolls and the control
+// table becomes immediate constant-bank operands); 0: any count
+template <typename T, bool KRUZ, int RY, int KC>
 __global__ void __launch_bounds__(256, 4)
     k_sweep_field2d_col(const DevProblem<T, T> P, const ColCtrl<T> C,
                         const SweepGroup<T> *__restrict__ G, int64_t it, double tol) {
     extern __shared__ __align__(16) unsigned char col_dyn[];
-    T *__restrict__ X = reinterpret_cast<T *>(col_dyn) + threadIdx.x;   // row r at X[256 r]
+    T *__restrict__ const colbuf = reinterpret_cast<T *>(col_dyn);     // [rows][256]
+    const int K = KC > 0 ? KC : P.K;
     HJ_LIST_BEGIN(G, it, tol)
     const int vn0 = (int)vw.vn[0], vn1 = (int)vw.vn[1];
     const T *__restrict__ Vi = vw.V[it & 1];
@@ -742,22 +744,36 @@ __global__ void __launch_bounds__(256, 4)
             T w0, wl, wh;
             const int i0 = floor_split(fma(S0, C.u0, D0), w0);
             const int jlo = floor_split(fma(S1, C.u1[0], D1), wl);
-            const int nrows = floor_split(fma(S1, C.u1[P.K - 1], D1), wh) + 2 - jlo;
+            const int nrows = floor_split(fma(S1, C.u1[K - 1], D1), wh) + 2 - jlo;
             if (fast && nrows <= C.rows) {
-                // the column X(jlo .. jlo + nrows - 1) at the foot abscissa
+                // the column X(jlo .. jlo + nrows - 1) at the foot abscissa, row r of this
+                // thread at colbuf[256 r + threadIdx.x]
                 const T *__restrict__ p = Vi + t + i0 + (int64_t)vn0 * jlo;
+                T *__restrict__ xw = colbuf + threadIdx.x;
 #pragma unroll 4
                 for (int r = 0; r < nrows; ++r) {
-                    X[256 * r] = lerp<T>(__ldg(p), __ldg(p + 1), w0);
+                    xw[256 * r] = lerp<T>(__ldg(p), __ldg(p + 1), w0);
                     p += vn0;
                 }
-#pragma unroll 4
-                for (int k = 0; k < P.K; ++k) {
+                const int xoff = (int)threadIdx.x - 256 * jlo;   // row j at colbuf[xoff + 256 j]
+#pragma unroll
+                for (int k = 0; k < (KC > 0 ? KC : 1); ++k) {
+                    if (KC == 0) break;
                     T w1;
-                    const int j = floor_split(fma(S1, C.u1[k], D1), w1) - jlo;
-                    const T I = lerp<T>(X[256 * j], X[256 * j + 256], w1);
+                    const int q = xoff + 256 * floor_split(fma(S1, C.u1[k], D1), w1);
+                    const T I = lerp<T>(colbuf[q], colbuf[q + 256], w1);
                     const T ck = KRUZ ? base : fma(hlr, C.csq[k], base);
                     best = fmin(best, fma(P.beta, I, ck));
+                }
+                if (KC == 0) {
+#pragma unroll 4
+                    for (int k = 0; k < K; ++k) {
+                        T w1;
+                        const int q = xoff + 256 * floor_split(fma(S1, C.u1[k], D1), w1);
+                        const T I = lerp<T>(colbuf[q], colbuf[q + 256], w1);
+                        const T ck = KRUZ ? base : fma(hlr, C.csq[k], base);
+                        best = fmin(best, fma(P.beta, I, ck));
+                    }
                 }
             } else {
                 const int64_t o[3] = {vw.o[0], vw.o[1], 0};
@@ -1236,6 +1252,8 @@ hj_status sweep_prepare(const hj_grid &g, const hj_problem &p, const hj_fields &
             }
         }
     }
+    if (L.col && p.cost == HJ_COST_DISCOUNTED)
+        tile_dim[1] = 64;      // dense column kernel: 32 x 64 tiles (k_sweep_field2d_col<.., 8>)
     if (want == HJ_SWEEP_FIELD_COL && !L.col) {
         set_error("sweep_kernel %d requested, but the problem does not qualify for it "
                   "(2-D affine, no speed field, every control with the same axis-0 "
@@ -1588,10 +1606,10 @@ hj_status sweep_coop(const DevProblem<T, T> &P, const SweepLaunch<T> &L, int64_t
     return HJ_OK;
 }
 
-template <typename T, bool KRUZ, int RY>
-static void launch_col(const DevProblem<T, T> &P, const SweepLaunch<T> &L, int64_t it, double tol,
-                       cudaStream_t s) {
-    auto kern = k_sweep_field2d_col<T, KRUZ, RY>;
+template <typename T, bool KRUZ, int RY, int KC>
+static void launch_col_kc(const DevProblem<T, T> &P, const SweepLaunch<T> &L, int64_t it,
+                          double tol, cudaStream_t s) {
+    auto kern = k_sweep_field2d_col<T, KRUZ, RY, KC>;
     const size_t smem = (size_t)L.colctrl.rows * 256 * sizeof(T);
     static size_t attr[64] = {0};      // dynamic shared memory opted in, per device
     const int dev = current_device();
@@ -1603,13 +1621,25 @@ static void launch_col(const DevProblem<T, T> &P, const SweepLaunch<T> &L, int64
                                                                               L.d_group, it, tol);
 }
 
+// control counts with an unrolled instantiation: the 2^n + 1 point sets of a linspace
+template <typename T, bool KRUZ, int RY>
+static void launch_col(const DevProblem<T, T> &P, const SweepLaunch<T> &L, int64_t it, double tol,
+                       cudaStream_t s) {
+    switch (P.K) {
+        case 17: return launch_col_kc<T, KRUZ, RY, 17>(P, L, it, tol, s);
+        case 33: return launch_col_kc<T, KRUZ, RY, 33>(P, L, it, tol, s);
+        case 65: return launch_col_kc<T, KRUZ, RY, 65>(P, L, it, tol, s);
+        default: return launch_col_kc<T, KRUZ, RY, 0>(P, L, it, tol, s);
+    }
+}
+
 template <typename T, int DYN, bool KRUZ>
 static void launch_field(const DevProblem<T, T> &P, const SweepLaunch<T> &L, int64_t it,
                          double tol, cudaStream_t s) {
     if constexpr (DYN == HJ_DYN_AFFINE) {
         if (L.col) {
             if (L.dense)
-                launch_col<T, KRUZ, 4>(P, L, it, tol, s);
+                launch_col<T, KRUZ, 8>(P, L, it, tol, s);
             else
                 launch_col<T, KRUZ, 1>(P, L, it, tol, s);
             return;

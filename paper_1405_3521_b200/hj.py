@@ -266,8 +266,14 @@ def hj_label_subdomains(coarse: DeviceProblem, Vc, n_max, fine: DeviceProblem, r
                 n_sets=m + (1 if Vexit is not None else 0))
 
 
+def _check_mask(mask, N):
+    if mask.dtype != torch.int64 or mask.numel() < N or not mask.is_cuda:
+        raise ValueError("fine_mask must be a CUDA int64 tensor (the uint64 set bits) of N nodes")
+
+
 def hj_partition_plan(fine: DeviceProblem, mask, m, max_iter=None, stream=None):
     max_iter = fine.prob.max_iter if max_iter is None else max_iter
+    _check_mask(mask, fine.N)
     plan = (hj_subdomain * m)()
     ws = ctypes.c_size_t()
     _check(lib().hj_partition_plan(ctypes.byref(fine.grid), mask.data_ptr(), int(m),
@@ -289,6 +295,7 @@ def hj_solve_partitioned(fine: DeviceProblem, mask, m, plan, ws_bytes, solve_set
     tol = prob.tol if tol is None else tol
     max_iter = prob.max_iter if max_iter is None else max_iter
     solve_set = ((1 << m) - 1) if solve_set is None else solve_set
+    _check_mask(mask, fine.N)
     if Vbar is None:
         Vbar = _buf(fine, "Vbar", fine.N, _torch_dtype(fine.dtype))
     if workspace is None or workspace.numel() < ws_bytes:

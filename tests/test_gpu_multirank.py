@@ -36,7 +36,8 @@ def test_rank_shares_min_reproduce_single_rank(idx, world):
     MIN all-reduce's arithmetic): bit-identical to world = 1; the shares partition the
     sub-domains."""
     cfg = _cfg(idx)
-    ref = pipeline.run_isa(cfg, cfg.dtype)["V"].clone()
+    r1 = pipeline.run_isa(cfg, cfg.dtype)
+    ref, n_sets = r1["V"].clone(), r1["n_sets"]
     acc, sets = None, []
     for r in range(world):
         out = pipeline.run_isa(cfg, cfg.dtype, rank=r, world=world, gather=False)
@@ -47,7 +48,7 @@ def test_rank_shares_min_reproduce_single_rank(idx, world):
     for s in sets:
         assert s & u == 0
         u |= s
-    assert u == (1 << cfg.m) - 1
+    assert u == (1 << n_sets) - 1
 
 
 def _port():
@@ -82,11 +83,12 @@ def _worker(rank, world, port, idx, ret):
 def test_two_processes_gloo_min_allreduce_on_cuda_tensors():
     idx = 2
     cfg = _cfg(idx)
-    ref = pipeline.run_isa(cfg, cfg.dtype)["V"].cpu().numpy()
+    r1 = pipeline.run_isa(cfg, cfg.dtype)
+    ref, n_sets = r1["V"].cpu().numpy(), r1["n_sets"]
     mgr = mp.Manager()
     ret = mgr.dict()
     mp.spawn(_worker, args=(2, _port(), idx, ret), nprocs=2, join=True)
     V0, s0 = ret[0]
     V1, s1 = ret[1]
     assert np.array_equal(V0, V1) and np.array_equal(V0, ref)
-    assert s0 & s1 == 0 and (s0 | s1) == (1 << cfg.m) - 1
+    assert s0 & s1 == 0 and (s0 | s1) == (1 << n_sets) - 1

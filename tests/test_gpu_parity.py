@@ -300,7 +300,7 @@ def test_partitioned_matches_oracle(idx, dtype):
     err = np.abs(res["V"].double().cpu().numpy() - Vbar_o).max()
     assert err <= TOL[dtype], (idx, dtype, err)
     for k in range(res["n_sets"]):
-        if dtype == "f64" and res["reports"][k] is not None:
+        if dtype == "f64" and res["plan"][k].n_nodes > 0:     # (an empty set is not solved)
             assert res["reports"][k]["iterations"] == its[k]
     # the independence invariant (Proposition 4.1): ISA reproduces the whole-grid
     # solution up to the scheme's own O(dx) error; restriction never lowers a value
@@ -391,7 +391,7 @@ def test_errors_are_reported_not_fatal():
 def test_partitioned_empty_set_and_single_subdomain():
     cfg = _cfg(1)
     fine = hj.DeviceProblem(cfg.fine, "f64")
-    mask = torch.ones(fine.N, dtype=torch.int32, device="cuda")
+    mask = torch.ones(fine.N, dtype=torch.int64, device="cuda")
     plan, ws = hj.hj_partition_plan(fine, mask, 1)
     Vbar, reps = hj.hj_solve_partitioned(fine, mask, 1, plan, ws, solve_set=0)
     assert torch.all(Vbar == cfg.fine.v_out)

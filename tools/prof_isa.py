@@ -24,3 +24,11 @@ for r in range(reps):
           f"{ {k: round(v, 2) for k, v in res['timings'].items()} }  sweeps per sub-domain "
           f"{[x['iterations'] for x in reps_]}  box nodes {[p.box_nodes for p in res['plan']][:8]}...  "
           f"evaluated {sum(x['evaluated_updates'] for x in reps_):.3e}", flush=True)
+    lab = res["labels"]
+    if lab.get("label") is not None:
+        n = res["n_sets"]
+        bits = res["mask"]
+        cover = [int(((bits >> k) & 1).sum()) for k in range(n)]
+        print(f"  sets {n}, labels -1: {int((lab['label'] == -1).sum())}, exit set (-2): "
+              f"{int((lab['label'] == -2).sum())}, sum|S_k|/N = {sum(cover) / fine.N:.3f}, "
+              f"sum box/N = {sum(p.box_nodes for p in res['plan']) / fine.N:.3f}", flush=True)
