@@ -226,9 +226,8 @@ hj_status hj_coarse_feedback(const hj_grid *grid, const hj_problem *prob,
  *     sub-domain of the box-boundary piece of Gamma (exit cost v_out), set m.
  * (b) Prolongation with overlap band (R9; ISA step 2, line 398-418): fine node i
  *     is in S_k iff a coarse node I labelled k has |i_d - R_d I_d| <= R_d + band on
- *     every axis; a node labelled -1 counts for every set (all m pieces, and the exit
- *     set when enabled), a node labelled -2 for the exit set m only; fine target nodes
- *     of piece k are always in S_k.
+ *     every axis; a node labelled -1 counts for every piece's set (0..m-1), a node
+ *     labelled -2 for the exit set m only; fine target nodes of piece k are always in S_k.
  *
  * coarse_grid/prob/coarse_fields/dtype/Vc  the coarse problem and its solution
  *     (device Vc); the trajectory uses coarse_prob.h.

@@ -427,14 +427,14 @@ void or_prolong_mask(const long nc[3], const long nf[3], const int periodic[3], 
 }
 
 /* ISA step 2 from trajectory labels (R8, R9, R9b): label k -> bit k; label -1 (the
- * trajectory left the box or ran out of steps) -> every set ("automatically included in
- * each approximation"): the m pieces and, with exit_set, the exit set;
- * label -2 (exit set, or_exit_labels) -> bit m only. */
+ * trajectory left the box or ran out of steps) -> every piece's set ("automatically
+ * included in each approximation"); label -2 (exit set,
+ * or_exit_labels) -> bit m only. */
 void or_prolong(const long nc[3], const long nf[3], const int periodic[3], int dim,
                 const long ratio[3], long band, const int *coarse_label, int m, int exit_set,
                 const signed char *fine_piece, unsigned long long *fine_mask) {
     int sets = m + (exit_set ? 1 : 0);
-    unsigned long long all = (sets >= 64) ? ~0ull : ((1ull << sets) - 1ull);
+    unsigned long long pieces = (m >= 64) ? ~0ull : ((1ull << m) - 1ull);
     long Nc = 1;
     for (int d = 0; d < dim; ++d) Nc *= nc[d];
     unsigned long long *cm = (unsigned long long *)malloc(sizeof(unsigned long long) * (size_t)Nc);
@@ -442,7 +442,7 @@ void or_prolong(const long nc[3], const long nf[3], const int periodic[3], int d
         int l = coarse_label[j];
         if (l >= 0) cm[j] = 1ull << l;
         else if (l == -2) cm[j] = exit_set ? (1ull << m) : 0ull;
-        else cm[j] = all;
+        else cm[j] = pieces;
     }
     or_prolong_mask(nc, nf, periodic, dim, ratio, band, cm, sets, fine_piece, fine_mask);
     free(cm);

@@ -452,13 +452,15 @@ struct ProlongArgs {
     int periodic[3];
     int64_t band;
     uint64_t all;       // every set: the m pieces (and the exit set when enabled)
+    uint64_t pieces;    // the m pieces' sets
     uint64_t exit_bit;  // bit of the exit set (label -2), 0 when disabled
 };
 
-// the sets a coarse label stands for (R9, R9b)
+// the sets a coarse label stands for: piece k -> set k; -1 -> every piece's set (R9);
+// -2 -> the exit set only (R9b)
 __device__ __forceinline__ uint64_t label_bits(const ProlongArgs &A, int32_t l) {
     if (l >= 0) return l < 64 ? (1ull << l) : 0ull;
-    return l == -2 ? A.exit_bit : A.all;
+    return l == -2 ? A.exit_bit : A.pieces;
 }
 
 __device__ __forceinline__ int64_t floordiv(int64_t a, int64_t b) {
@@ -597,6 +599,7 @@ hj_status prolong_launch(const hj_grid &cg, const hj_grid &fg, const int32_t rat
     const int sets = m + (exit_set ? 1 : 0);
     A.all = sets >= 64 ? ~0ull : ((1ull << sets) - 1ull);
     A.exit_bit = exit_set ? (1ull << m) : 0ull;
+    A.pieces = m >= 64 ? ~0ull : ((1ull << m) - 1ull);
     const int64_t Nf = grid_nodes(fg);
     if (A.nc[0] <= 4096) {                  // row scheme (ryz fits in shared memory)
         const int64_t rows = A.nf[1] * A.nf[2];

@@ -940,6 +940,8 @@ struct SweepLaunch {
                                         // (the control count unless a kernel prunes)
     bool col = false;                   // FIELD2D via k_sweep_field2d_col (shared u0)
     ColCtrl<T> colctrl;
+    int seg = 0, seg_nup = 0;           // FIELD_COOP segmented control order (CoopState)
+    int16_t seg_order[HJ_MAX_CONTROLS];
 };
 
 // bytes of change flags a view needs under the smallest tiling (32 x 8 x 1)
@@ -1252,6 +1254,23 @@ hj_status sweep_prepare(const hj_grid &g, const hj_problem &p, const hj_fields &
             }
         }
     }
+    if (L.kind == SWEEP_FIELD2D && L.coop && p.dynamics == HJ_DYN_AFFINE && !f.speed &&
+        p.A[1][0] == 0 && p.A[1][1] == 0 && p.A[1][2] == 0 && p.b[1] == 0 &&
+        !getenv("HJ_NO_SEG")) {
+        // drift along axis 0 only: d1 = h/dy u1 has the control's sign — two groups
+        // (u1 >= 0, u1 < 0 in the kernel's arithmetic), each sorted by u0 (coop_eval_field)
+        std::vector<int> up, lo;
+        for (int k = 0; k < p.n_controls; ++k)
+            ((T)p.controls[k][1] < T(0) ? lo : up).push_back(k);
+        auto by_u0 = [&](int a, int b) { return (T)p.controls[a][0] < (T)p.controls[b][0]; };
+        std::stable_sort(up.begin(), up.end(), by_u0);
+        std::stable_sort(lo.begin(), lo.end(), by_u0);
+        L.seg = 1;
+        L.seg_nup = (int)up.size();
+        int i = 0;
+        for (int k : up) L.seg_order[i++] = (int16_t)k;
+        for (int k : lo) L.seg_order[i++] = (int16_t)k;
+    }
     if (L.col && p.cost == HJ_COST_DISCOUNTED)
         tile_dim[1] = 64;      // dense column kernel: 32 x 64 tiles (k_sweep_field2d_col<.., 8>)
     if (want == HJ_SWEEP_FIELD_COL && !L.col) {
@@ -1536,6 +1555,9 @@ hj_status sweep_coop(const DevProblem<T, T> &P, const SweepLaunch<T> &L, int64_t
     S.n_views = nv;
     int64_t tot = 0;
     S.dubins = L.kind == SWEEP_DUBINS ? 1 : 0;
+    S.seg = L.seg;
+    S.seg_nup = L.seg_nup;
+    memcpy(S.seg_order, L.seg_order, sizeof(S.seg_order));
     for (int v = 0; v < nv; ++v) {
         S.mt_base[v] = tot;
         S.mt0[v] = (int32_t)((L.vn0[v] + 7) / 8);

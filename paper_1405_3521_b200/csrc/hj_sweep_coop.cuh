@@ -48,6 +48,17 @@ struct CoopState {
     int64_t total;
     int32_t vorder[HJ_GROUP_VIEWS];   // cluster mode: views by decreasing size
     int cluster;                    // 1: cluster mode (k_sweep_local2d_coop<..., CL>)
+    // field class with a drift along axis 0 only and no speed field (config 3): the sign
+    // of d1 is the control's, so the controls are kept as two groups (u1 >= 0, then
+    // u1 < 0), each sorted by u0 — d0 < 0 on a prefix of each (coop_eval_field)
+    int seg, seg_nup;
+    int16_t seg_order[HJ_MAX_CONTROLS];
+};
+
+// one entry of the segmented control table (shared memory)
+template <typename T>
+struct SegCtl {
+    T u0, w1, csq;
 };
 
 __device__ __forceinline__ int coop_view(const CoopState &S, int64_t gid) {
@@ -281,7 +292,8 @@ __device__ __forceinline__ void coop_eval_field(const DevProblem<T, T> &P, const
                                                 unsigned long long di, unsigned long long de,
                                                 int64_t x0, int64_t y0, T *__restrict__ Vo,
                                                 T &rmax_out, unsigned long long &cm_out,
-                                                int &evald_out) {
+                                                int &evald_out, const SegCtl<T> *__restrict__ seg,
+                                                int seg_nup) {
     constexpr int BP = 10;
     const int lane = threadIdx.x & 31;
     const bool mono = P.monotone != 0;
@@ -340,6 +352,41 @@ __device__ __forceinline__ void coop_eval_field(const DevProblem<T, T> &P, const
             const T X01 = beta * ((q0[-BP + 1] - Vp0) - (V0m - V00));   // +x -y
             const T X11 = beta * ((q0[-BP - 1] - Vm0) - (V0m - V00));   // -x -y
             const T C0 = fma(beta, V00, base);
+            if (DYN == HJ_DYN_AFFINE && seg) {
+                // segmented control loop (CoopState::seg): per group, the controls with
+                // d0 = fma(S0, u0, D0) < 0 are a prefix of the u0-sorted order (fma is
+                // monotone in u0 for S0 > 0); each of the four (group, side) segments has
+                // fixed differences — the same bracket fma(w1, fma(w0, A3, A2),
+                // fma(w0, A1, ck)) per control as the select loop below, no sign tests
+                const int K = P.K;
+                int lo = 0, hi = seg_nup;
+                while (lo < hi) {
+                    const int mid = (lo + hi) >> 1;
+                    if (fma(S0, seg[mid].u0, D0) < T(0)) lo = mid + 1; else hi = mid;
+                }
+                const int sU = lo;
+                lo = seg_nup;
+                hi = K;
+                while (lo < hi) {
+                    const int mid = (lo + hi) >> 1;
+                    if (fma(S0, seg[mid].u0, D0) < T(0)) lo = mid + 1; else hi = mid;
+                }
+                const int sL = lo;
+                const int bnd[5] = {0, sU, seg_nup, sL, K};
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    // q = 0: -x +y, 1: +x +y, 2: -x -y, 3: +x -y
+                    const T A1 = (q & 1) ? Dxp : Dxm;
+                    const T A2 = (q & 2) ? Dym : Dyp;
+                    const T A3 = q == 0 ? X10 : (q == 1 ? X00 : (q == 2 ? X11 : X01));
+#pragma unroll 4
+                    for (int k = bnd[q]; k < bnd[q + 1]; ++k) {
+                        const T w0 = fabs(fma(S0, seg[k].u0, D0));
+                        const T ck = kruz ? C0 : C0 + hlr * seg[k].csq;
+                        best = fmin(best, fma(seg[k].w1, fma(w0, A3, A2), fma(w0, A1, ck)));
+                    }
+                }
+            } else {
             T dx8[8] = {Dxp, Dxm, Dyp, Dym, X00, X10, X01, X11};
 #pragma unroll
             for (int e = 0; e < 8; ++e) opaque(dx8[e]);
@@ -353,6 +400,7 @@ __device__ __forceinline__ void coop_eval_field(const DevProblem<T, T> &P, const
                 const T w0 = fabs(d0), w1 = fabs(d1);
                 const T ck = kruz ? C0 : C0 + hlr * P.csq[k];
                 best = fmin(best, fma(w1, fma(w0, A3, A2), fma(w0, A1, ck)));
+            }
             }
         } else {
             // box edge (R3): interp()'s arithmetic step for step (box test, clamp onto the
@@ -567,10 +615,13 @@ struct CoopBits<double> {
 
 // warps per CTA: fp32 one 512-thread CTA per SM (fewer barrier arrivals); fp64 (its
 // staged blocks are twice the size) two 256-thread CTAs per SM
+#ifndef HJ_COOP_MINB32
+#define HJ_COOP_MINB32 1     // resident 512-thread CTAs per SM asked of ptxas for fp32
+#endif
 template <typename T>
 struct CoopNW {
     static constexpr int nw = sizeof(T) == 4 ? 16 : 8;
-    static constexpr int minb = sizeof(T) == 4 ? 1 : 2;
+    static constexpr int minb = sizeof(T) == 4 ? HJ_COOP_MINB32 : 2;
 };
 
 // EV: 0 = local class (LocalCtrl, FFMA2 quadrants), HJ_DYN_AFFINE + 1 / HJ_DYN_VANDERPOL + 1
@@ -605,6 +656,15 @@ __global__ void __launch_bounds__(CoopNW<T>::nw * 32, CoopNW<T>::minb)
     __shared__ SweepView<T> sview[HJ_GROUP_VIEWS];
     // local class: the quadrant control tables ax | ay | ck, [3][4][KQ]
     __shared__ T sctl[EV == 0 ? 12 * KQ : 1];
+    // field class, drift along axis 0 only: the segmented control table (CoopState::seg)
+    __shared__ SegCtl<T> sseg[EV == 1 ? HJ_MAX_CONTROLS : 1];
+    if (EV == 1 && S.seg)
+        for (int i = threadIdx.x; i < P.K; i += blockDim.x) {
+            const int k = S.seg_order[i];
+            sseg[i].u0 = P.ctrl[k][0];
+            sseg[i].w1 = fabs(fma(P.hdx[1] * T(1), P.ctrl[k][1], T(0)));
+            sseg[i].csq = P.csq[k];
+        }
     // Dubins: extreme |h w a_k / dth| of each sign group (coop_eval_dubins)
     __shared__ T dub_wext[4];
     if (EV == 3 && threadIdx.x == 0) {
@@ -853,7 +913,8 @@ __global__ void __launch_bounds__(CoopNW<T>::nw * 32, CoopNW<T>::minb)
                 else
                     coop_eval_field<T, EV - 1>(P, vw, vw.V[n & 1], blk[warp][s2], spd[warp][s2],
                                                lst[warp][s2], d_s, e_s, x0, y0,
-                                               vw.V[(n + 1) & 1], rmax, cm, evald);
+                                               vw.V[(n + 1) & 1], rmax, cm, evald,
+                                               EV == 1 && S.seg ? sseg : nullptr, S.seg_nup);
                 cm = ((unsigned long long)__reduce_or_sync(0xffffffffu, (unsigned)(cm >> 32)) << 32) |
                      (unsigned long long)__reduce_or_sync(0xffffffffu, (unsigned)cm);
 #pragma unroll

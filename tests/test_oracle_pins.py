@@ -766,7 +766,7 @@ def test_p21_box_tolerance_only_moves_exact_box_feet():
 #      (Theorem 2.1 decomposes all of Gamma; exit cost v_out, Tdef line 243).
 #  (a) the exit test: an unlabelled node joins the exit set iff Vc >= Vexit - tol
 #      (inclusive), labelled nodes never;
-#  (b) prolongation: label -2 -> the exit set (bit m) only, -1 -> all m + 1 sets, by
+#  (b) prolongation: label -2 -> the exit set (bit m) only, -1 -> the m pieces' sets, by
 #      brute-force dilation;
 #  (c) Kruzkov with no target: Vexit = 1 = "never reached" everywhere (to rounding);
 #  (d) Proposition 4.1 still holds with the exit set on the regulator geometry
@@ -794,8 +794,8 @@ def test_p22b_prolong_exit_set_bruteforce():
     L = lab.reshape(7, 9)
     for k in range(m + 1):
         seed = np.zeros((25, 33), bool)
-        member = (L == k) if k < m else (L == -2)
-        seed[::4, ::4] = member | (L == -1)
+        member = ((L == k) | (L == -1)) if k < m else (L == -2)
+        seed[::4, ::4] = member
         rad = 4 + band
         dil = ndimage.binary_dilation(seed, structure=np.ones((2 * rad + 1, 2 * rad + 1), bool))
         if k < m:

@@ -38,9 +38,11 @@ MUTATIONS_ALL = [
      "                if (!any || Vk[k][j] > v) v = Vk[k][j];"),
     ("prolongation radius -1", "            long reach = ratio[d] + band;",
      "            long reach = ratio[d] + band - 1;"),
-    ("label -1 -> no bits", "        else cm[j] = all;", "        else cm[j] = 0ull;"),
+    ("label -1 -> no bits", "        else cm[j] = pieces;", "        else cm[j] = 0ull;"),
+    ("label -1 -> the exit set too", "        else cm[j] = pieces;",
+     "        else cm[j] = pieces | (exit_set ? (1ull << m) : 0ull);"),
     ("label -2 -> all sets", "        else if (l == -2) cm[j] = exit_set ? (1ull << m) : 0ull;",
-     "        else if (l == -2) cm[j] = all;"),
+     "        else if (l == -2) cm[j] = pieces | (1ull << m);"),
     ("exit test strict", "if (labels[j] == -1 && Vc[j] >= Vexit[j] - tol) labels[j] = -2;",
      "if (labels[j] == -1 && Vc[j] > Vexit[j] - tol) labels[j] = -2;"),
     ("exit test on labelled nodes", "if (labels[j] == -1 && Vc[j] >= Vexit[j] - tol) labels[j] = -2;",
@@ -79,8 +81,12 @@ def main():
             r = subprocess.run([sys.executable, "-m", "pytest", "-x", "-q", "-p", "no:cacheprovider",
                                 *TESTS], cwd=ROOT, capture_output=True, text=True, timeout=1800)
             failed = [l for l in r.stdout.splitlines() if l.startswith("FAILED")]
-            verdict = "caught by " + failed[0].split("::")[-1].split(" ")[0] if r.returncode else \
-                "NOT CAUGHT"
+            if not r.returncode:
+                verdict = "NOT CAUGHT"
+            elif failed:
+                verdict = "caught by " + failed[0].split("::")[-1].split(" ")[0]
+            else:
+                verdict = "ERROR (did not build/collect): " + r.stdout[-200:].replace("\n", " ")
             results.append((name, verdict))
             print(f"{name:55s} {verdict}", flush=True)
     finally:

@@ -10,14 +10,16 @@ import torch  # noqa: E402
 import hj_workloads as W  # noqa: E402
 from paper_1405_3521_b200 import hj, pipeline  # noqa: E402
 
-idx = int(sys.argv[1]) if len(sys.argv) > 1 else 2
-reps = int(sys.argv[2]) if len(sys.argv) > 2 else 1
+args = [a for a in sys.argv[1:] if not a.startswith("--")]
+idx = int(args[0]) if len(args) > 0 else 2
+reps = int(args[1]) if len(args) > 1 else 1
+exit_set = "--no-exit" not in sys.argv
 cfg = W.make(idx)
 fine = hj.DeviceProblem(cfg.fine, cfg.dtype)
 coarse = hj.DeviceProblem(cfg.coarse, cfg.dtype)
 for r in range(reps):
     t0 = time.perf_counter()
-    res = pipeline.run_isa(cfg, cfg.dtype, fine=fine, coarse=coarse)
+    res = pipeline.run_isa(cfg, cfg.dtype, fine=fine, coarse=coarse, exit_set=exit_set)
     torch.cuda.synchronize()
     reps_ = [x for x in res["reports"] if x]
     print(f"config {idx}: wall {1e3 * (time.perf_counter() - t0):.1f} ms  stages "
