@@ -1592,9 +1592,9 @@ hj_status sweep_coop(const DevProblem<T, T> &P, const SweepLaunch<T> &L, int64_t
     S.dmask[1] = (unsigned long long *)c.take(8 * tot);
     S.items[0] = (int32_t *)c.take(4 * tot);
     S.items[1] = (int32_t *)c.take(4 * tot);
-    S.count = (int32_t *)c.take(16);
+    S.count = (int32_t *)c.take(32);
     S.stop = (int64_t *)c.take(8 * HJ_GROUP_VIEWS);
-    HJ_CUDA(cudaMemsetAsync(S.count, 0, 16, s));
+    HJ_CUDA(cudaMemsetAsync(S.count, 0, 32, s));
     if (tot > 0) {
         const int blocks = (int)std::min<int64_t>((tot + 255) / 256, 148 * 8);
         k_coop_masks<T><<<blocks, 256, 0, s>>>(L.d_group, S, L.gn0, L.gn1);

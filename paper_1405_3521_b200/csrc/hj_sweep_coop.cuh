@@ -40,7 +40,8 @@ struct CoopState {
     unsigned long long *emask;      // [total] interior nodes on the box edge (class -3)
     unsigned long long *dmask[2];   // [total] nodes to evaluate in sweep n (parity n)
     int32_t *items[2];              // [total] mini-tiles with a nonzero mask (parity n)
-    int32_t *count;                 // [3] ring: sweep n reads count[n % 3]
+    int32_t *count;                 // [3] ring: sweep n reads count[n % 3]; [3] the grid
+                                    // barrier; [4..6] ring: items grabbed in sweep n
     int64_t *stop;                  // [n_views] iterations performed (output)
     int use_list;                   // 1: walk items/count (many mini-tiles); 0: scan all
     int dubins;                     // 3-D Dubins views: 8 x 8 mini-tiles per heading plane
@@ -56,10 +57,20 @@ struct CoopState {
 };
 
 // one entry of the segmented control table (shared memory)
+#ifndef HJ_SEG_VEC
+#define HJ_SEG_VEC 0       // (1: one 64-bit load per control — measured 1 % slower on config 3)
+#endif
+#if HJ_SEG_VEC
+template <typename T>
+struct __align__(2 * sizeof(T)) SegCtl {
+    T u0, w1;                  // one 64-bit (fp32) shared load per control
+};
+#else
 template <typename T>
 struct SegCtl {
-    T u0, w1, csq;
+    T u0, w1;
 };
+#endif
 
 __device__ __forceinline__ int coop_view(const CoopState &S, int64_t gid) {
     int v = 0;
@@ -293,7 +304,7 @@ __device__ __forceinline__ void coop_eval_field(const DevProblem<T, T> &P, const
                                                 int64_t x0, int64_t y0, T *__restrict__ Vo,
                                                 T &rmax_out, unsigned long long &cm_out,
                                                 int &evald_out, const SegCtl<T> *__restrict__ seg,
-                                                int seg_nup) {
+                                                const T *__restrict__ seg_csq, int seg_nup) {
     constexpr int BP = 10;
     const int lane = threadIdx.x & 31;
     const bool mono = P.monotone != 0;
@@ -382,7 +393,7 @@ __device__ __forceinline__ void coop_eval_field(const DevProblem<T, T> &P, const
 #pragma unroll 4
                     for (int k = bnd[q]; k < bnd[q + 1]; ++k) {
                         const T w0 = fabs(fma(S0, seg[k].u0, D0));
-                        const T ck = kruz ? C0 : C0 + hlr * seg[k].csq;
+                        const T ck = kruz ? C0 : C0 + hlr * seg_csq[k];
                         best = fmin(best, fma(seg[k].w1, fma(w0, A3, A2), fma(w0, A1, ck)));
                     }
                 }
@@ -631,7 +642,9 @@ struct CoopNW {
 // for cluster c, with the hardware cluster barrier between sweeps instead of the
 // grid-wide one.
 template <typename T, int KQ, bool PC, int EV = 0, bool CL = false>
-__global__ void __launch_bounds__(CoopNW<T>::nw * 32, CoopNW<T>::minb)
+// (Dubins, EV 3: two 512-thread CTAs per SM at 64 registers measured 10 % faster on
+// config 4; the 2-D classes spill and lose at 64 registers — profiles/r2/occupancy_r2j.txt)
+__global__ void __launch_bounds__(CoopNW<T>::nw * 32, EV == 3 ? 2 : CoopNW<T>::minb)
     k_sweep_local2d_coop(const DevProblem<T, T> P, const LocalCtrl<T> C,
                          const SweepGroup<T> *__restrict__ G, const CoopState S,
                          int64_t max_iter, double tol) {
@@ -658,12 +671,13 @@ __global__ void __launch_bounds__(CoopNW<T>::nw * 32, CoopNW<T>::minb)
     __shared__ T sctl[EV == 0 ? 12 * KQ : 1];
     // field class, drift along axis 0 only: the segmented control table (CoopState::seg)
     __shared__ SegCtl<T> sseg[EV == 1 ? HJ_MAX_CONTROLS : 1];
+    __shared__ T sseg_csq[EV == 1 ? HJ_MAX_CONTROLS : 1];
     if (EV == 1 && S.seg)
         for (int i = threadIdx.x; i < P.K; i += blockDim.x) {
             const int k = S.seg_order[i];
             sseg[i].u0 = P.ctrl[k][0];
             sseg[i].w1 = fabs(fma(P.hdx[1] * T(1), P.ctrl[k][1], T(0)));
-            sseg[i].csq = P.csq[k];
+            sseg_csq[i] = P.csq[k];
         }
     // Dubins: extreme |h w a_k / dth| of each sign group (coop_eval_dubins)
     __shared__ T dub_wext[4];
@@ -739,10 +753,16 @@ __global__ void __launch_bounds__(CoopNW<T>::nw * 32, CoopNW<T>::minb)
         const int64_t ncand =
             S.use_list ? (int64_t)*(volatile const int32_t *)&S.count[n % 3] : ctot;
         const int32_t *litems = S.items[n & 1];
-        const int64_t per_cta = ncand > grank ? (ncand - grank + gsize - 1) / gsize : 0;
+        // list mode (grid-wide): no static split of the list over the CTAs — every warp
+        // grabs the next two listed mini-tiles from a grid-wide counter until the list is
+        // exhausted, so the sweep ends when the work does, not when the most loaded CTA
+        // does.  (One pass of the chunk loop: the stopping decision, then the grab loop.)
+        const bool dyn = S.use_list && !CL;
+        const int64_t per_cta =
+            dyn ? 1 : (ncand > grank ? (ncand - grank + gsize - 1) / gsize : 0);
         for (int64_t ch = 0; ch < per_cta; ch += COOP_NW * 32) {
-        int chunk_n;
-        {
+        int chunk_n = 0;
+        if (!dyn) {
             const int64_t k = ch + threadIdx.x;
             const int64_t idx = grank + k * (int64_t)gsize;
             const int64_t g = k < per_cta ? (S.use_list ? (int64_t)litems[idx] : cbase + idx) : 0;
@@ -783,11 +803,45 @@ __global__ void __launch_bounds__(CoopNW<T>::nw * 32, CoopNW<T>::minb)
         // two mini-tiles per warp iteration: every global load of both (masks, the
         // 10 x 10 blocks of V^n, the speeds) is issued before any is used, and the mask
         // updates of both go out together
-        for (int it = warp; it < cnt; it += 2 * COOP_NW) {
+        for (int it = warp;; it += 2 * COOP_NW) {
             // 32-bit mini-tile arithmetic (ids are int32; a 2-D view's nodes < 2^31)
             int gid[2];
-            gid[0] = qgid[it];
-            gid[1] = it + COOP_NW < cnt ? qgid[it + COOP_NW] : -1;
+            unsigned long long gd[2] = {0ull, 0ull}, ge[2] = {0ull, 0ull};
+            if (dyn) {
+                int base = 0;
+                if (lane == 0) base = atomicAdd(&S.count[4 + n % 3], 2);
+                base = __shfl_sync(0xffffffffu, base, 0);
+                if (base >= ncand) break;
+                int g = -1;
+                unsigned long long m = 0ull, cim = 0ull, cem = 0ull;
+                if (lane < 2 && base + lane < ncand) {
+                    g = litems[base + lane];
+                    m = dcur[g];
+                    cim = S.imask[g];
+                    cem = S.emask[g];
+                    dcur[g] = 0ull;                // consumed
+                }
+#pragma unroll
+                for (int s2 = 0; s2 < 2; ++s2) {
+                    gid[s2] = __shfl_sync(0xffffffffu, g, s2);
+                    gd[s2] = __shfl_sync(0xffffffffu, m & cim, s2);
+                    ge[s2] = __shfl_sync(0xffffffffu, m & cem, s2);
+                }
+                if (gid[0] < 0) {                  // (never: base < ncand)
+                    gid[0] = gid[1];
+                    gd[0] = ge[0] = 0ull;
+                }
+            } else {
+                if (it >= cnt) break;
+                gid[0] = qgid[it];
+                gid[1] = it + COOP_NW < cnt ? qgid[it + COOP_NW] : -1;
+#pragma unroll
+                for (int s2 = 0; s2 < 2; ++s2)
+                    if (gid[s2] >= 0) {
+                        gd[s2] = qmask[s2 ? it + COOP_NW : it];
+                        ge[s2] = qemask[s2 ? it + COOP_NW : it];
+                    }
+            }
             int vv[2], mx[2], my[2], mz[2];
             unsigned long long dd[2], em[2];
 #pragma unroll
@@ -807,8 +861,8 @@ __global__ void __launch_bounds__(CoopNW<T>::nw * 32, CoopNW<T>::minb)
                     my[s2] = mt / m0;
                     mx[s2] = mt - my[s2] * m0;
                 }
-                dd[s2] = gid[s2] >= 0 ? qmask[s2 ? it + COOP_NW : it] : 0ull;
-                em[s2] = gid[s2] >= 0 ? qemask[s2 ? it + COOP_NW : it] : 0ull;
+                dd[s2] = gid[s2] >= 0 ? gd[s2] : 0ull;
+                em[s2] = gid[s2] >= 0 ? ge[s2] : 0ull;
             }
             // staged V^n blocks and speeds, loads first.  A block inside its view (the
             // common case) reads rows of V^n at a fixed stride: no bounds tests.
@@ -914,7 +968,8 @@ __global__ void __launch_bounds__(CoopNW<T>::nw * 32, CoopNW<T>::minb)
                     coop_eval_field<T, EV - 1>(P, vw, vw.V[n & 1], blk[warp][s2], spd[warp][s2],
                                                lst[warp][s2], d_s, e_s, x0, y0,
                                                vw.V[(n + 1) & 1], rmax, cm, evald,
-                                               EV == 1 && S.seg ? sseg : nullptr, S.seg_nup);
+                                               EV == 1 && S.seg ? sseg : nullptr, sseg_csq,
+                                               S.seg_nup);
                 cm = ((unsigned long long)__reduce_or_sync(0xffffffffu, (unsigned)(cm >> 32)) << 32) |
                      (unsigned long long)__reduce_or_sync(0xffffffffu, (unsigned)cm);
 #pragma unroll
@@ -987,7 +1042,10 @@ __global__ void __launch_bounds__(CoopNW<T>::nw * 32, CoopNW<T>::minb)
             if (m > 0.0) atomic_max_nonneg(&sview[v].res[n], m);
             if (w) atomicAdd(sview[v].work, w);
         }
-        if (S.use_list && blockIdx.x == 0 && threadIdx.x == 0) S.count[(n + 2) % 3] = 0;
+        if (S.use_list && blockIdx.x == 0 && threadIdx.x == 0) {
+            S.count[(n + 2) % 3] = 0;
+            S.count[4 + (n + 2) % 3] = 0;          // the grab counter of sweep n + 2
+        }
         if (tr) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_b));
         if (tr_all && n < tr_cap) {
             unsigned long long t_arr;              // every CTA's arrival (load balance)
