@@ -41,7 +41,7 @@ struct CoopState {
     unsigned long long *dmask[2];   // [total] nodes to evaluate in sweep n (parity n)
     int32_t *items[2];              // [total] mini-tiles with a nonzero mask (parity n)
     int32_t *count;                 // [3] ring: sweep n reads count[n % 3]; [3] the grid
-                                    // barrier; [4..6] ring: items grabbed in sweep n
+                                    // barrier
     int64_t *stop;                  // [n_views] iterations performed (output)
     int use_list;                   // 1: walk items/count (many mini-tiles); 0: scan all
     int dubins;                     // 3-D Dubins views: 8 x 8 mini-tiles per heading plane
@@ -753,16 +753,10 @@ __global__ void __launch_bounds__(CoopNW<T>::nw * 32, EV == 3 ? 2 : CoopNW<T>::m
         const int64_t ncand =
             S.use_list ? (int64_t)*(volatile const int32_t *)&S.count[n % 3] : ctot;
         const int32_t *litems = S.items[n & 1];
-        // list mode (grid-wide): no static split of the list over the CTAs — every warp
-        // grabs the next two listed mini-tiles from a grid-wide counter until the list is
-        // exhausted, so the sweep ends when the work does, not when the most loaded CTA
-        // does.  (One pass of the chunk loop: the stopping decision, then the grab loop.)
-        const bool dyn = S.use_list && !CL;
-        const int64_t per_cta =
-            dyn ? 1 : (ncand > grank ? (ncand - grank + gsize - 1) / gsize : 0);
+        const int64_t per_cta = ncand > grank ? (ncand - grank + gsize - 1) / gsize : 0;
         for (int64_t ch = 0; ch < per_cta; ch += COOP_NW * 32) {
-        int chunk_n = 0;
-        if (!dyn) {
+        int chunk_n;
+        {
             const int64_t k = ch + threadIdx.x;
             const int64_t idx = grank + k * (int64_t)gsize;
             const int64_t g = k < per_cta ? (S.use_list ? (int64_t)litems[idx] : cbase + idx) : 0;
@@ -803,45 +797,11 @@ __global__ void __launch_bounds__(CoopNW<T>::nw * 32, EV == 3 ? 2 : CoopNW<T>::m
         // two mini-tiles per warp iteration: every global load of both (masks, the
         // 10 x 10 blocks of V^n, the speeds) is issued before any is used, and the mask
         // updates of both go out together
-        for (int it = warp;; it += 2 * COOP_NW) {
+        for (int it = warp; it < cnt; it += 2 * COOP_NW) {
             // 32-bit mini-tile arithmetic (ids are int32; a 2-D view's nodes < 2^31)
             int gid[2];
-            unsigned long long gd[2] = {0ull, 0ull}, ge[2] = {0ull, 0ull};
-            if (dyn) {
-                int base = 0;
-                if (lane == 0) base = atomicAdd(&S.count[4 + n % 3], 2);
-                base = __shfl_sync(0xffffffffu, base, 0);
-                if (base >= ncand) break;
-                int g = -1;
-                unsigned long long m = 0ull, cim = 0ull, cem = 0ull;
-                if (lane < 2 && base + lane < ncand) {
-                    g = litems[base + lane];
-                    m = dcur[g];
-                    cim = S.imask[g];
-                    cem = S.emask[g];
-                    dcur[g] = 0ull;                // consumed
-                }
-#pragma unroll
-                for (int s2 = 0; s2 < 2; ++s2) {
-                    gid[s2] = __shfl_sync(0xffffffffu, g, s2);
-                    gd[s2] = __shfl_sync(0xffffffffu, m & cim, s2);
-                    ge[s2] = __shfl_sync(0xffffffffu, m & cem, s2);
-                }
-                if (gid[0] < 0) {                  // (never: base < ncand)
-                    gid[0] = gid[1];
-                    gd[0] = ge[0] = 0ull;
-                }
-            } else {
-                if (it >= cnt) break;
-                gid[0] = qgid[it];
-                gid[1] = it + COOP_NW < cnt ? qgid[it + COOP_NW] : -1;
-#pragma unroll
-                for (int s2 = 0; s2 < 2; ++s2)
-                    if (gid[s2] >= 0) {
-                        gd[s2] = qmask[s2 ? it + COOP_NW : it];
-                        ge[s2] = qemask[s2 ? it + COOP_NW : it];
-                    }
-            }
+            gid[0] = qgid[it];
+            gid[1] = it + COOP_NW < cnt ? qgid[it + COOP_NW] : -1;
             int vv[2], mx[2], my[2], mz[2];
             unsigned long long dd[2], em[2];
 #pragma unroll
@@ -861,8 +821,8 @@ __global__ void __launch_bounds__(CoopNW<T>::nw * 32, EV == 3 ? 2 : CoopNW<T>::m
                     my[s2] = mt / m0;
                     mx[s2] = mt - my[s2] * m0;
                 }
-                dd[s2] = gid[s2] >= 0 ? gd[s2] : 0ull;
-                em[s2] = gid[s2] >= 0 ? ge[s2] : 0ull;
+                dd[s2] = gid[s2] >= 0 ? qmask[s2 ? it + COOP_NW : it] : 0ull;
+                em[s2] = gid[s2] >= 0 ? qemask[s2 ? it + COOP_NW : it] : 0ull;
             }
             // staged V^n blocks and speeds, loads first.  A block inside its view (the
             // common case) reads rows of V^n at a fixed stride: no bounds tests.
@@ -1042,10 +1002,7 @@ __global__ void __launch_bounds__(CoopNW<T>::nw * 32, EV == 3 ? 2 : CoopNW<T>::m
             if (m > 0.0) atomic_max_nonneg(&sview[v].res[n], m);
             if (w) atomicAdd(sview[v].work, w);
         }
-        if (S.use_list && blockIdx.x == 0 && threadIdx.x == 0) {
-            S.count[(n + 2) % 3] = 0;
-            S.count[4 + (n + 2) % 3] = 0;          // the grab counter of sweep n + 2
-        }
+        if (S.use_list && blockIdx.x == 0 && threadIdx.x == 0) S.count[(n + 2) % 3] = 0;
         if (tr) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_b));
         if (tr_all && n < tr_cap) {
             unsigned long long t_arr;              // every CTA's arrival (load balance)
