@@ -1255,10 +1255,11 @@ hj_status sweep_prepare(const hj_grid &g, const hj_problem &p, const hj_fields &
         }
     }
     if (L.kind == SWEEP_FIELD2D && L.coop && p.dynamics == HJ_DYN_AFFINE && !f.speed &&
-        p.A[1][0] == 0 && p.A[1][1] == 0 && p.A[1][2] == 0 && p.b[1] == 0 &&
+        p.A[1][0] == 0 && p.A[1][1] == 0 && p.A[1][2] == 0 && p.b[1] == 0 && p.A[0][0] == 0 &&
         !getenv("HJ_NO_SEG")) {
-        // drift along axis 0 only: d1 = h/dy u1 has the control's sign — two groups
-        // (u1 >= 0, u1 < 0 in the kernel's arithmetic), each sorted by u0 (coop_eval_field)
+        // drift along axis 0 only, independent of x0: d1 = h/dy u1 has the control's sign —
+        // two groups (u1 >= 0, u1 < 0 in the kernel's arithmetic), each sorted by u0, and
+        // d0 depends on the row only (coop_eval_field: one split search per row)
         std::vector<int> up, lo;
         for (int k = 0; k < p.n_controls; ++k)
             ((T)p.controls[k][1] < T(0) ? lo : up).push_back(k);

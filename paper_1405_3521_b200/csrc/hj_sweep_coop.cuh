@@ -304,7 +304,8 @@ __device__ __forceinline__ void coop_eval_field(const DevProblem<T, T> &P, const
                                                 int64_t x0, int64_t y0, T *__restrict__ Vo,
                                                 T &rmax_out, unsigned long long &cm_out,
                                                 int &evald_out, const SegCtl<T> *__restrict__ seg,
-                                                const T *__restrict__ seg_csq, int seg_nup) {
+                                                const T *__restrict__ seg_csq, int seg_nup,
+                                                int16_t *__restrict__ rsplit) {
     constexpr int BP = 10;
     const int lane = threadIdx.x & 31;
     const bool mono = P.monotone != 0;
@@ -320,6 +321,22 @@ __device__ __forceinline__ void coop_eval_field(const DevProblem<T, T> &P, const
     const int plo = __popc(dlo), nN = plo + __popc(dhi);
     if ((dlo >> lane) & 1u) lstw[__popc(dlo & lt)] = (int8_t)lane;
     if ((dhi >> lane) & 1u) lstw[plo + __popc(dhi & lt)] = (int8_t)(32 + lane);
+    if (DYN == HJ_DYN_AFFINE && seg && lane < 16) {
+        // segmented mode (the drift moves along axis 0 only and does not depend on x0, no
+        // speed field): d0 depends on the row only, so the two split points of each of the
+        // mini-tile's 8 rows are found once (lanes 0-15: row lane & 7, group lane >> 3)
+        const int rr = lane & 7, grp = lane >> 3;
+        const T xx0 = fma((T)(x0 + vw.o[0]), P.dx[0], P.lo[0]);
+        const T xx1 = fma((T)(y0 + rr + vw.o[1]), P.dx[1], P.lo[1]);
+        const T D0r = P.hdx[0] * fma(P.A[0], xx0, fma(P.A[1], xx1, P.b[0]));
+        const T S0r = P.hdx[0] * T(1);
+        int lo = grp ? seg_nup : 0, hi = grp ? P.K : seg_nup;
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (fma(S0r, seg[mid].u0, D0r) < T(0)) lo = mid + 1; else hi = mid;
+        }
+        rsplit[lane] = (int16_t)lo;
+    }
     __syncwarp();
     T rmax = T(0);
     unsigned long long cm = 0;
@@ -370,20 +387,7 @@ __device__ __forceinline__ void coop_eval_field(const DevProblem<T, T> &P, const
                 // fixed differences — the same bracket fma(w1, fma(w0, A3, A2),
                 // fma(w0, A1, ck)) per control as the select loop below, no sign tests
                 const int K = P.K;
-                int lo = 0, hi = seg_nup;
-                while (lo < hi) {
-                    const int mid = (lo + hi) >> 1;
-                    if (fma(S0, seg[mid].u0, D0) < T(0)) lo = mid + 1; else hi = mid;
-                }
-                const int sU = lo;
-                lo = seg_nup;
-                hi = K;
-                while (lo < hi) {
-                    const int mid = (lo + hi) >> 1;
-                    if (fma(S0, seg[mid].u0, D0) < T(0)) lo = mid + 1; else hi = mid;
-                }
-                const int sL = lo;
-                const int bnd[5] = {0, sU, seg_nup, sL, K};
+                const int bnd[5] = {0, rsplit[r], seg_nup, rsplit[8 + r], K};
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
                     // q = 0: -x +y, 1: +x +y, 2: -x -y, 3: +x -y
@@ -672,6 +676,7 @@ __global__ void __launch_bounds__(CoopNW<T>::nw * 32, EV == 3 ? 2 : CoopNW<T>::m
     // field class, drift along axis 0 only: the segmented control table (CoopState::seg)
     __shared__ SegCtl<T> sseg[EV == 1 ? HJ_MAX_CONTROLS : 1];
     __shared__ T sseg_csq[EV == 1 ? HJ_MAX_CONTROLS : 1];
+    __shared__ int16_t srsplit[EV == 1 ? COOP_NW : 1][16];   // per warp: the row splits
     if (EV == 1 && S.seg)
         for (int i = threadIdx.x; i < P.K; i += blockDim.x) {
             const int k = S.seg_order[i];
@@ -929,7 +934,7 @@ __global__ void __launch_bounds__(CoopNW<T>::nw * 32, EV == 3 ? 2 : CoopNW<T>::m
                                                lst[warp][s2], d_s, e_s, x0, y0,
                                                vw.V[(n + 1) & 1], rmax, cm, evald,
                                                EV == 1 && S.seg ? sseg : nullptr, sseg_csq,
-                                               S.seg_nup);
+                                               S.seg_nup, srsplit[EV == 1 ? warp : 0]);
                 cm = ((unsigned long long)__reduce_or_sync(0xffffffffu, (unsigned)(cm >> 32)) << 32) |
                      (unsigned long long)__reduce_or_sync(0xffffffffu, (unsigned)cm);
 #pragma unroll
