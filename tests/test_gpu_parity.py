@@ -229,7 +229,8 @@ def test_coop_cluster_mode_matches_grid_mode(idx, monkeypatch):
 
 
 @pytest.mark.parametrize("dtype", ["f32", "f64"])
-@pytest.mark.parametrize("case", ["shifted_u0", "reversed_order", "discounted_lr"])
+@pytest.mark.parametrize("case", ["shifted_u0", "reversed_order", "discounted_lr", "a00",
+                                  "kruzkov"])
 def test_field_col_bit_identical_to_field2d(case, dtype):
     """k_sweep_field2d_col (controls sharing their axis-0 component, walked in ascending
     axis-1 order) against k_sweep_field2d and the oracle: same iterates bit for bit for
@@ -242,8 +243,12 @@ def test_field_col_bit_identical_to_field2d(case, dtype):
         ctrl[:, 0] = 0.3
     elif case == "reversed_order":
         ctrl = ctrl[::-1].copy()
-    else:
+    elif case == "discounted_lr":
         kw["lr"] = 0.7
+    elif case == "a00":           # axis-0 drift depends on x0: one node per thread (col)
+        A[0, 0] = 0.2
+    else:                         # Kruzkov (work-list mode, not dense)
+        kw.update(cost=W.COST_KRUZKOV, v_out=1.0, lq=0.0)
     g = W.Grid((77, 61), (-2.0, -2.0), (2.0, 2.0), (False, False))
     piece = W.sector_pieces(g, 0.3, 4)
     p = _tiny((77, 61), lo=(-2.0, -2.0), hi=(2.0, 2.0), ctrl=ctrl, piece=piece, **kw)
