@@ -939,7 +939,6 @@ struct SweepLaunch {
     int evals = 0;                      // brackets evaluated per interior node and sweep
                                         // (the control count unless a kernel prunes)
     bool col = false;                   // FIELD2D via k_sweep_field2d_col (shared u0)
-    bool col2 = false;                  // ... two nodes per thread (dense, A[0][0] = 0)
     ColCtrl<T> colctrl;
     int seg = 0, seg_nup = 0;           // FIELD_COOP segmented control order (CoopState)
     int16_t seg_order[HJ_MAX_CONTROLS];
@@ -1273,16 +1272,10 @@ hj_status sweep_prepare(const hj_grid &g, const hj_problem &p, const hj_fields &
         for (int k : up) L.seg_order[i++] = (int16_t)k;
         for (int k : lo) L.seg_order[i++] = (int16_t)k;
     }
-    if (L.col && p.cost == HJ_COST_DISCOUNTED) {
-        if (p.A[0][0] == 0 && !getenv("HJ_NO_COL2")) {
-            L.col2 = true;     // dense, paired column kernel: 64 x 32 tiles (col2<.., 4>)
-            L.colctrl.rows += 1;   // (the union of two nodes' rows)
-            tile_dim[0] = 64;
-            tile_dim[1] = 32;
-        } else {
-            tile_dim[1] = 64;  // dense column kernel: 32 x 64 tiles (k_sweep_field2d_col<.., 8>)
-        }
-    }
+    // (dense column kernel: 32 x 64 tiles, k_sweep_field2d_col<.., 8>.  Two adjacent nodes
+    // per thread sharing their column rows — 16 % fewer instructions — measured no faster:
+    // the row loads' latency, not issue, then bounds it; profiles/r2/README.)
+    if (L.col && p.cost == HJ_COST_DISCOUNTED) tile_dim[1] = 64;
     if (want == HJ_SWEEP_FIELD_COL && !L.col) {
         set_error("sweep_kernel %d requested, but the problem does not qualify for it "
                   "(2-D affine, no speed field, every control with the same axis-0 "
@@ -1638,223 +1631,6 @@ hj_status sweep_coop(const DevProblem<T, T> &P, const SweepLaunch<T> &L, int64_t
     return HJ_OK;
 }
 
-// Dense column kernel, two adjacent nodes per thread (x, x + 1) — when the axis-0 drift
-// does not depend on x0 (A[0][0] = 0, config 5) the two nodes share the foot abscissa's
-// cell i0 and weight w0, so one row of their two columns costs three loads
-// (V(x + i0 .. x + i0 + 2, j)) and two lerps; the two control loops run interleaved
-// (independent chains).  Same values as k_sweep_field2d_col / k_sweep_field2d, bit for
-// bit.  Tile 64 x 8 RY, 256 threads; column buffer [rows][512] (node x at [r][t],
-// node x + 1 at [r][256 + t]).
-template <typename T, bool KRUZ>
-__device__ __forceinline__ T col_node_general(const DevProblem<T, T> &P, const ColCtrl<T> &C,
-                                              const SweepView<T> &vw, const T *__restrict__ Vi,
-                                              int li, int lj, T *__restrict__ colbuf, int K,
-                                              bool fast, T &base_out, T &D1_out) {
-    // one node, k_sweep_field2d_col's arithmetic (fast: its column path; else the general
-    // interp() path); colbuf: this thread's column (stride 512)
-    const int64_t t = li + (int64_t)vw.vn[0] * lj;
-    const int64_t gi[3] = {li + vw.o[0], lj + vw.o[1], 0};
-    const T x0 = fma((T)gi[0], P.dx[0], P.lo[0]), x1 = fma((T)gi[1], P.dx[1], P.lo[1]);
-    const T D0 = P.hdx[0] * fma(P.A[0], x0, fma(P.A[1], x1, P.b[0]));
-    const T D1 = P.hdx[1] * fma(P.A[3], x0, fma(P.A[4], x1, P.b[1]));
-    const T S0 = P.hdx[0], S1 = P.hdx[1];
-    T base;
-    if (KRUZ) {
-        base = P.kcost;
-    } else {
-        const T x[3] = {x0, x1, T(0)};
-        base = P.h * cost_state(P, x);
-    }
-    base_out = base;
-    D1_out = D1;
-    const T hlr = P.h * P.lr;
-    T best = (T)INFINITY;
-    T w0, wl, wh;
-    const int i0 = floor_split(fma(S0, C.u0, D0), w0);
-    const int jlo = floor_split(fma(S1, C.u1[0], D1), wl);
-    const int nrows = floor_split(fma(S1, C.u1[K - 1], D1), wh) + 2 - jlo;
-    if (fast && nrows <= C.rows) {
-        const T *__restrict__ p = Vi + t + i0 + (int64_t)vw.vn[0] * jlo;
-        for (int r = 0; r < nrows; ++r) {
-            colbuf[512 * r] = lerp<T>(__ldg(p), __ldg(p + 1), w0);
-            p += vw.vn[0];
-        }
-        for (int k = 0; k < K; ++k) {
-            T w1;
-            const int q = 512 * (floor_split(fma(S1, C.u1[k], D1), w1) - jlo);
-            const T I = lerp<T>(colbuf[q], colbuf[q + 512], w1);
-            const T ck = KRUZ ? base : fma(hlr, C.csq[k], base);
-            best = fmin(best, fma(P.beta, I, ck));
-        }
-    } else {
-        const int64_t o[3] = {vw.o[0], vw.o[1], 0};
-        const int64_t vn[3] = {vw.vn[0], vw.vn[1], 1};
-        for (int k = 0; k < P.K; ++k) {
-            const T delta[3] = {fma(S0, P.ctrl[k][0], D0), fma(S1, P.ctrl[k][1], D1), T(0)};
-            const T I = interp<T, T, 2>(Vi, o, vn, P.n, P.periodic, gi, delta, P.v_out);
-            const T ck = KRUZ ? base : fma(hlr, P.csq[k], base);
-            best = fmin(best, fma(P.beta, I, ck));
-        }
-    }
-    return best;
-}
-
-#ifndef HJ_COL2_ROW_UNROLL
-#define HJ_COL2_ROW_UNROLL 4
-#endif
-constexpr int kCol2RowUnroll = HJ_COL2_ROW_UNROLL;
-template <typename T, bool KRUZ, int RY, int KC>
-__global__ void __launch_bounds__(256, 3)
-    k_sweep_field2d_col2(const DevProblem<T, T> P, const ColCtrl<T> C,
-                         const SweepGroup<T> *__restrict__ G, int64_t it, double tol) {
-    extern __shared__ __align__(16) unsigned char col_dyn[];
-    T *__restrict__ const colbuf = reinterpret_cast<T *>(col_dyn);     // [rows][512]
-    const int K = KC > 0 ? KC : P.K;
-    HJ_LIST_BEGIN(G, it, tol)
-    const int vn0 = (int)vw.vn[0], vn1 = (int)vw.vn[1];
-    const T *__restrict__ Vi = vw.V[it & 1];
-    T *__restrict__ Vo = vw.V[(it + 1) & 1];
-    constexpr int TY = 8 * RY;
-    const int lane = threadIdx.x & 31;
-    const int la = tc[0] * 64 + 2 * lane;                // node a = la, node b = la + 1
-    const int hx = G->halo[0], hy = G->halo[1];
-    const bool fast = tc[0] * 64 - hx >= 0 && tc[0] * 64 + 63 + hx + 1 <= vn0 - 1 &&
-                      tc[1] * TY - hy >= 0 && tc[1] * TY + TY - 1 + hy + 1 <= vn1 - 1;
-    T *__restrict__ xa = colbuf + threadIdx.x, *__restrict__ xb = colbuf + 256 + threadIdx.x;
-    T rmax = T(0);
-    int changed = 0, evaluated = 0;
-    const T hlr = P.h * P.lr;
-#pragma unroll 1
-    for (int rr = 0; rr < RY; ++rr) {
-        const int lj = tc[1] * TY + (threadIdx.x >> 5) + 8 * rr;
-        if (lj >= vn1 || la >= vn0) continue;
-        const bool hasb = la + 1 < vn0;
-        const int64_t ta = la + (int64_t)vn0 * lj;
-        const int8_t ca = vw.cls[ta], cb = hasb ? vw.cls[ta + 1] : (int8_t)-2;
-        const T vina = Vi[ta], vinb = hasb ? Vi[ta + 1] : T(0);
-        T va, vb;
-        bool done = false;
-        if (fast && ca == -1 && cb == -1) {
-            // the paired path
-            const int64_t gi1 = lj + vw.o[1];
-            const T x0a = fma((T)(la + vw.o[0]), P.dx[0], P.lo[0]);
-            const T x0b = fma((T)(la + 1 + vw.o[0]), P.dx[0], P.lo[0]);
-            const T x1 = fma((T)gi1, P.dx[1], P.lo[1]);
-            const T D0 = P.hdx[0] * fma(P.A[0], x0a, fma(P.A[1], x1, P.b[0]));   // = node b's
-            const T D1a = P.hdx[1] * fma(P.A[3], x0a, fma(P.A[4], x1, P.b[1]));
-            const T D1b = P.hdx[1] * fma(P.A[3], x0b, fma(P.A[4], x1, P.b[1]));
-            const T S0 = P.hdx[0], S1 = P.hdx[1];
-            T basea, baseb;
-            if (KRUZ) {
-                basea = baseb = P.kcost;
-            } else {
-                const T xa3[3] = {x0a, x1, T(0)}, xb3[3] = {x0b, x1, T(0)};
-                basea = P.h * cost_state(P, xa3);
-                baseb = P.h * cost_state(P, xb3);
-            }
-            T w0, wt;
-            const int i0 = floor_split(fma(S0, C.u0, D0), w0);
-            const int ja0 = floor_split(fma(S1, C.u1[0], D1a), wt);
-            const int jb0 = floor_split(fma(S1, C.u1[0], D1b), wt);
-            const int ja1 = floor_split(fma(S1, C.u1[K - 1], D1a), wt);
-            const int jb1 = floor_split(fma(S1, C.u1[K - 1], D1b), wt);
-            const int jlo = min(ja0, jb0);
-            const int nrows = max(ja1, jb1) + 2 - jlo;
-            if (nrows <= C.rows) {
-                const T *__restrict__ p = Vi + ta + i0 + (int64_t)vn0 * jlo;
-#pragma unroll kCol2RowUnroll
-                for (int r = 0; r < nrows; ++r) {
-                    const T v0 = __ldg(p), v1 = __ldg(p + 1), v2 = __ldg(p + 2);
-                    xa[512 * r] = lerp<T>(v0, v1, w0);
-                    xb[512 * r] = lerp<T>(v1, v2, w0);
-                    p += vn0;
-                }
-                const int off = (int)threadIdx.x - 512 * jlo;
-                T besta = (T)INFINITY, bestb = (T)INFINITY;
-#pragma unroll
-                for (int k = 0; k < (KC > 0 ? KC : 1); ++k) {
-                    if (KC == 0) break;
-                    T w1a, w1b;
-                    const int qa = off + 512 * floor_split(fma(S1, C.u1[k], D1a), w1a);
-                    const int qb = off + 256 + 512 * floor_split(fma(S1, C.u1[k], D1b), w1b);
-                    const T Ia = lerp<T>(colbuf[qa], colbuf[qa + 512], w1a);
-                    const T Ib = lerp<T>(colbuf[qb], colbuf[qb + 512], w1b);
-                    const T cka = KRUZ ? basea : fma(hlr, C.csq[k], basea);
-                    const T ckb = KRUZ ? baseb : fma(hlr, C.csq[k], baseb);
-                    besta = fmin(besta, fma(P.beta, Ia, cka));
-                    bestb = fmin(bestb, fma(P.beta, Ib, ckb));
-                }
-                if (KC == 0) {
-#pragma unroll 2
-                    for (int k = 0; k < K; ++k) {
-                        T w1a, w1b;
-                        const int qa = off + 512 * floor_split(fma(S1, C.u1[k], D1a), w1a);
-                        const int qb = off + 256 + 512 * floor_split(fma(S1, C.u1[k], D1b), w1b);
-                        const T Ia = lerp<T>(colbuf[qa], colbuf[qa + 512], w1a);
-                        const T Ib = lerp<T>(colbuf[qb], colbuf[qb + 512], w1b);
-                        const T cka = KRUZ ? basea : fma(hlr, C.csq[k], basea);
-                        const T ckb = KRUZ ? baseb : fma(hlr, C.csq[k], baseb);
-                        besta = fmin(besta, fma(P.beta, Ia, cka));
-                        bestb = fmin(bestb, fma(P.beta, Ib, ckb));
-                    }
-                }
-                va = besta;
-                vb = bestb;
-                done = true;
-            }
-        }
-        if (!done) {
-            // unpaired: each node on its own (classes, edge tiles, long columns)
-            T bse, d1;
-            if (ca == -2) va = P.v_out;
-            else if (ca >= 0) va = P.g ? P.g[(la + vw.o[0]) + P.n[0] * (lj + vw.o[1])] : T(0);
-            else va = col_node_general<T, KRUZ>(P, C, vw, Vi, la, lj, xa, K, fast, bse, d1);
-            if (hasb) {
-                if (cb == -2) vb = P.v_out;
-                else if (cb >= 0)
-                    vb = P.g ? P.g[(la + 1 + vw.o[0]) + P.n[0] * (lj + vw.o[1])] : T(0);
-                else
-                    vb = col_node_general<T, KRUZ>(P, C, vw, Vi, la + 1, lj, xb, K, fast, bse, d1);
-            }
-        }
-        if (ca == -1) {
-            if (P.monotone) va = fmin(va, vina);
-            ++evaluated;
-        }
-        Vo[ta] = va;
-        T dv = va > vina ? va - vina : vina - va;
-        rmax = dv > rmax ? dv : rmax;
-        changed |= !same_bits(va, vina);
-        if (hasb) {
-            if (cb == -1) {
-                if (P.monotone) vb = fmin(vb, vinb);
-                ++evaluated;
-            }
-            Vo[ta + 1] = vb;
-            dv = vb > vinb ? vb - vinb : vinb - vb;
-            rmax = dv > rmax ? dv : rmax;
-            changed |= !same_bits(vb, vinb);
-        }
-    }
-    changed_ = tile_finish(G, v, tile, it, rmax, changed, evaluated);
-    HJ_LIST_END(G, it)
-}
-
-template <typename T, bool KRUZ, int RY, int KC>
-static void launch_col2_kc(const DevProblem<T, T> &P, const SweepLaunch<T> &L, int64_t it,
-                           double tol, cudaStream_t s) {
-    auto kern = k_sweep_field2d_col2<T, KRUZ, RY, KC>;
-    const size_t smem = (size_t)L.colctrl.rows * 512 * sizeof(T);
-    static size_t attr[64] = {0};
-    const int dev = current_device();
-    if (smem > attr[dev]) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        attr[dev] = smem;
-    }
-    kern<<<grid_for(kern, 256, smem, L.total_tiles, L.dense), 256, smem, s>>>(P, L.colctrl,
-                                                                              L.d_group, it, tol);
-}
-
 template <typename T, bool KRUZ, int RY, int KC>
 static void launch_col_kc(const DevProblem<T, T> &P, const SweepLaunch<T> &L, int64_t it,
                           double tol, cudaStream_t s) {
@@ -1874,14 +1650,6 @@ static void launch_col_kc(const DevProblem<T, T> &P, const SweepLaunch<T> &L, in
 template <typename T, bool KRUZ, int RY>
 static void launch_col(const DevProblem<T, T> &P, const SweepLaunch<T> &L, int64_t it, double tol,
                        cudaStream_t s) {
-    if (L.col2) {
-        switch (P.K) {
-            case 17: return launch_col2_kc<T, KRUZ, 4, 17>(P, L, it, tol, s);
-            case 33: return launch_col2_kc<T, KRUZ, 4, 33>(P, L, it, tol, s);
-            case 65: return launch_col2_kc<T, KRUZ, 4, 65>(P, L, it, tol, s);
-            default: return launch_col2_kc<T, KRUZ, 4, 0>(P, L, it, tol, s);
-        }
-    }
     switch (P.K) {
         case 17: return launch_col_kc<T, KRUZ, RY, 17>(P, L, it, tol, s);
         case 33: return launch_col_kc<T, KRUZ, RY, 33>(P, L, it, tol, s);
