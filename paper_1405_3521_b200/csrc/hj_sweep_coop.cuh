@@ -664,6 +664,7 @@ __global__ void __launch_bounds__(CoopNW<T>::nw * 32, EV == 3 ? 2 : CoopNW<T>::m
     __shared__ int32_t qgid[COOP_NW * 32];
     __shared__ unsigned long long qmask[COOP_NW * 32], qemask[COOP_NW * 32];
     __shared__ int wcnt[COOP_NW];
+    __shared__ int qnext;          // the next unclaimed queue position (warps claim pairs)
     // per-CTA max of the sweep's |V^{n+1} - V^n| as the bits of a T >= 0 (monotone as
     // unsigned: native shared atomicMax, no CAS loop), evaluated-node count
     __shared__ typename CoopBits<T>::U cres[HJ_GROUP_VIEWS];
@@ -784,6 +785,7 @@ __global__ void __launch_bounds__(CoopNW<T>::nw * 32, EV == 3 ? 2 : CoopNW<T>::m
                 dcur[g] = 0ull;                    // consumed
             }
             chunk_n = __reduce_add_sync(0xffffffffu, wc);
+            if (threadIdx.x == 0) qnext = 0;
             __syncthreads();                       // the queue is complete
         }
         const int cnt = chunk_n;
@@ -802,13 +804,30 @@ __global__ void __launch_bounds__(CoopNW<T>::nw * 32, EV == 3 ? 2 : CoopNW<T>::m
         // two mini-tiles per warp iteration: every global load of both (masks, the
         // 10 x 10 blocks of V^n, the speeds) is issued before any is used, and the mask
         // updates of both go out together
-        for (int it = warp; it < cnt; it += 2 * COOP_NW) {
+        // the warps claim two queued mini-tiles at a time from a shared counter: a warp that
+        // finishes early takes the next pair instead of waiting at the CTA barrier
+        // (the Dubins class keeps the static split: (warp, warp + NW), (warp + 2 NW, ...))
+        constexpr bool DYNQ = EV != 3;
+        for (int itw = warp;; itw += 2 * COOP_NW) {
+            int it = itw;
+            if (DYNQ) {
+                if (lane == 0) it = atomicAdd(&qnext, 2);
+                it = __shfl_sync(0xffffffffu, it, 0);
+            }
+            if (it >= cnt) break;
+            const int it2 = DYNQ ? it + 1 : it + COOP_NW;    // the pair's second item
             // 32-bit mini-tile arithmetic (ids are int32; a 2-D view's nodes < 2^31)
             int gid[2];
             gid[0] = qgid[it];
-            gid[1] = it + COOP_NW < cnt ? qgid[it + COOP_NW] : -1;
+            gid[1] = it2 < cnt ? qgid[it2] : -1;
             int vv[2], mx[2], my[2], mz[2];
             unsigned long long dd[2], em[2];
+#ifdef HJ_DEBUG_BOUNDS
+            if (it < 0 || it >= COOP_NW * 32 || gid[0] < 0 || gid[0] >= S.total ||
+                gid[1] >= S.total)
+                printf("HJ_DEBUG pair: n %lld it %d cnt %d gid %d %d total %lld\n", (long long)n,
+                       it, cnt, gid[0], gid[1], (long long)S.total), __trap();
+#endif
 #pragma unroll
             for (int s2 = 0; s2 < 2; ++s2) {
                 const int g = gid[s2] < 0 ? gid[0] : gid[s2];
@@ -826,8 +845,8 @@ __global__ void __launch_bounds__(CoopNW<T>::nw * 32, EV == 3 ? 2 : CoopNW<T>::m
                     my[s2] = mt / m0;
                     mx[s2] = mt - my[s2] * m0;
                 }
-                dd[s2] = gid[s2] >= 0 ? qmask[s2 ? it + COOP_NW : it] : 0ull;
-                em[s2] = gid[s2] >= 0 ? qemask[s2 ? it + COOP_NW : it] : 0ull;
+                dd[s2] = gid[s2] >= 0 ? qmask[s2 ? it2 : it] : 0ull;
+                em[s2] = gid[s2] >= 0 ? qemask[s2 ? it2 : it] : 0ull;
             }
             // staged V^n blocks and speeds, loads first.  A block inside its view (the
             // common case) reads rows of V^n at a fixed stride: no bounds tests.
