@@ -633,9 +633,12 @@ struct CoopBits<double> {
 #ifndef HJ_COOP_MINB32
 #define HJ_COOP_MINB32 1     // resident 512-thread CTAs per SM asked of ptxas for fp32
 #endif
+#ifndef HJ_COOP_NW32
+#define HJ_COOP_NW32 16      // warps per CTA for fp32
+#endif
 template <typename T>
 struct CoopNW {
-    static constexpr int nw = sizeof(T) == 4 ? 16 : 8;
+    static constexpr int nw = sizeof(T) == 4 ? HJ_COOP_NW32 : 8;
     static constexpr int minb = sizeof(T) == 4 ? HJ_COOP_MINB32 : 2;
 };
 
@@ -648,7 +651,8 @@ struct CoopNW {
 template <typename T, int KQ, bool PC, int EV = 0, bool CL = false>
 // (Dubins, EV 3: two 512-thread CTAs per SM at 64 registers measured 10 % faster on
 // config 4; the 2-D classes spill and lose at 64 registers — profiles/r2/occupancy_r2j.txt)
-__global__ void __launch_bounds__(CoopNW<T>::nw * 32, EV == 3 ? 2 : CoopNW<T>::minb)
+__global__ void __launch_bounds__(CoopNW<T>::nw * 32,
+                                  EV == 3 && CoopNW<T>::nw <= 16 ? 2 : CoopNW<T>::minb)
     k_sweep_local2d_coop(const DevProblem<T, T> P, const LocalCtrl<T> C,
                          const SweepGroup<T> *__restrict__ G, const CoopState S,
                          int64_t max_iter, double tol) {
