@@ -94,7 +94,12 @@ enum { HJ_COST_KRUZKOV = 0, HJ_COST_DISCOUNTED = 1 };
  * scheme, the foot's cell picked by the signs of its offsets); FIELD_COL for the other 2-D
  * affine problems without a speed field whose controls share their axis-0 component
  * (config 5: one x-interpolated column per node, walked once over the controls sorted by
- * their axis-1 component — bit-identical iterates to FIELD2D); FIELD2D for the other 2-D
+ * their axis-1 component — bit-identical iterates to FIELD2D), and among those FIELD_LAT
+ * for discounted problems with 17/33/65 controls whose axis-1 feet are exactly one row
+ * apart and whose axis-1 drift does not depend on x1 (config 5: eight nodes of a column
+ * per thread stream the rows once; every control shares the foot's axis-1 weight —
+ * bit-identical to FIELD2D when the per-control foot sums are exact, as on config 5);
+ * FIELD2D for the other 2-D
  * affine / Van der Pol problems without periodic axes; DUBINS_COOP (the cooperative
  * scheme on 8x8 mini-tiles of each heading plane) for Dubins problems whose (x, y) and
  * heading steps stay within one cell; DUBINS for Dubins dynamics whose heading step is <= 1 cell; GENERIC
@@ -103,7 +108,7 @@ enum { HJ_COST_KRUZKOV = 0, HJ_COST_DISCOUNTED = 1 };
 enum { HJ_SWEEP_AUTO = 0, HJ_SWEEP_GENERIC = 1, HJ_SWEEP_LOCAL_SCALAR = 2,
        HJ_SWEEP_LOCAL_PACKED = 3, HJ_SWEEP_FIELD2D = 4, HJ_SWEEP_DUBINS = 5,
        HJ_SWEEP_LOCAL_TB = 6, HJ_SWEEP_LOCAL_COOP = 7, HJ_SWEEP_FIELD_COOP = 8,
-       HJ_SWEEP_DUBINS_COOP = 9, HJ_SWEEP_FIELD_COL = 10 };
+       HJ_SWEEP_DUBINS_COOP = 9, HJ_SWEEP_FIELD_COL = 10, HJ_SWEEP_FIELD_LAT = 11 };
 
 typedef struct {
     int32_t dim;            /* 2 or 3                                          */

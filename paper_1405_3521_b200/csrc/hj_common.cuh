@@ -166,6 +166,14 @@ __device__ __forceinline__ Tc cost_state(const DevProblem<Tc, Ts> &P, const Tc x
     return P.l0 + P.lq * x2 + P.ln * sqrt(x2);
 }
 
+// cost_state of a 2-D non-periodic problem (the same operations, no loop over the axes)
+template <typename Tc, typename Ts>
+__device__ __forceinline__ Tc cost_state_2d(const DevProblem<Tc, Ts> &P, Tc x0, Tc x1) {
+    Tc x2 = fma(x0, x0, Tc(0));
+    x2 = fma(x1, x1, x2);
+    return P.l0 + P.lq * x2 + P.ln * sqrt(x2);
+}
+
 __device__ __forceinline__ void atomic_max_nonneg(double *addr, double v) {
     atomicMax(reinterpret_cast<unsigned long long *>(addr),
               (unsigned long long)__double_as_longlong(v));

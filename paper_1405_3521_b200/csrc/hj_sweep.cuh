@@ -75,11 +75,22 @@ __device__ __forceinline__ int find_view(const SweepGroup<T> *__restrict__ G, in
     return v;
 }
 
+// the same for a warp-uniform tile id: lane v tests view v+1 (one load and a ballot)
+template <typename T>
+__device__ __forceinline__ int find_view_warp(const SweepGroup<T> *__restrict__ G, int64_t b) {
+    const int lane = threadIdx.x & 31;
+    return __popc(__ballot_sync(0xffffffffu,
+                                lane + 1 < G->n_views && G->t[lane + 1].tile_base <= b));
+}
+
+// (tile ids are int: SweepGroup::total_tiles — 32-bit divisions)
 template <typename T>
 __device__ __forceinline__ void tile_coords(const TileView<T> &tv, int64_t tile, int tc[3]) {
-    tc[0] = (int)(tile % tv.nt[0]);
-    tc[1] = (int)((tile / tv.nt[0]) % tv.nt[1]);
-    tc[2] = (int)(tile / ((int64_t)tv.nt[0] * tv.nt[1]));
+    const int t = (int)tile, n0 = tv.nt[0], n1 = tv.nt[1];
+    const int q = t / n0;
+    tc[0] = t - q * n0;
+    tc[1] = q % n1;
+    tc[2] = q / n1;
 }
 
 __device__ __forceinline__ void wl_push(const WorkList &wl, int64_t nit, int gid) {
@@ -124,7 +135,7 @@ __device__ __forceinline__ void push_neighbours(const SweepGroup<T> *__restrict_
     const int cnt_ = *(volatile const int *)&wl_.count[dense_ ? 3 : (it) % 3];              \
     for (int idx_ = blockIdx.x; idx_ < cnt_; idx_ += gridDim.x) {                          \
         const int gid_ = dense_ ? wl_.live[idx_] : wl_.items[(it) & 1][idx_];              \
-        const int v = find_view(G, gid_);                                                  \
+        const int v = find_view_warp(G, gid_);                                             \
         if (!dense_ && threadIdx.x == 0)                                                   \
             atomicAnd(&wl_.mark[(it) & 1][gid_ >> 5], ~(1u << (gid_ & 31)));                \
         const SweepView<T> &vw = (G)->v[v];                                                \
@@ -801,6 +812,165 @@ __global__ void __launch_bounds__(256, 4)
     HJ_LIST_END(G, it)
 }
 
+// ---------------------------------------------------------------------------
+// k_sweep_field2d_col for lattice-aligned controls: the axis-1 foot offsets of consecutive
+// (sorted) controls are exactly one cell apart, S1 (u1[k] - u1[0]) = k (config 5:
+// h/dy = 16, a_k = -1 + k/16 — the control step moves the foot by one row), and the
+// axis-1 drift does not depend on x1 (A[1][1] = 0).  Then every control of a node shares
+// the foot's axis-1 weight w1 and control k reads rows j0 + k, j0 + k + 1 of the node's
+// x-interpolated column X:
+//     bracket_k = beta lerp(X(j0 + k), X(j0 + k + 1), w1) + c_k,
+//     (j0, w1) = floor split of fma(S1, u1[0], D1),  X(j) = lerp(V(i0, j), V(i0 + 1, j), w0).
+// One thread takes R = 8 nodes of one column (consecutive rows): they share j0 and w1,
+// and node n's rows are node 0's shifted by n, so the thread streams the K + R rows once
+// (two loads each) and feeds every row to the nodes whose window holds it — per node and
+// control one y-lerp, the cost FMA, beta I + c and the min; per node and row one x-lerp.
+// The arithmetic is k_sweep_field2d's (same lerps, same fma for c_k, order-free min) with
+// control k's foot split as (j0 + k, w1) instead of splitting fma(S1, u1[k], D1): equal
+// whenever that fma is exactly fma(S1, u1[0], D1) + k (config 5: every operand is a
+// dyadic rational of few bits — bit-identical iterates, asserted), else equal up to the
+// rounding of the foot.  A thread whose nodes straddle an axis-0 cell boundary (i0 not
+// the same for its 8 rows) or whose tile's footprint leaves the view takes
+// k_sweep_field2d's per-control loop.
+// ---------------------------------------------------------------------------
+template <typename T, bool KRUZ, int KC>
+__global__ void __launch_bounds__(256, 2)
+    k_sweep_field2d_lat(const DevProblem<T, T> P, const ColCtrl<T> C,
+                        const SweepGroup<T> *__restrict__ G, int64_t it, double tol) {
+    constexpr int R = 8;                         // nodes per thread (rows), tile 32 x 64
+    constexpr int TY = 8 * R;
+    HJ_LIST_BEGIN(G, it, tol)
+    const int vn0 = (int)vw.vn[0], vn1 = (int)vw.vn[1];
+    const T *__restrict__ Vi = vw.V[it & 1];
+    T *__restrict__ Vo = vw.V[(it + 1) & 1];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int li = tc[0] * 32 + lane;
+    const int lj0 = tc[1] * TY + R * warp;
+    const int hx = G->halo[0], hy = G->halo[1];
+    const bool fast = tc[0] * 32 - hx >= 0 && tc[0] * 32 + 31 + hx + 1 <= vn0 - 1 &&
+                      tc[1] * TY - hy >= 0 && tc[1] * TY + TY - 1 + hy + 1 <= vn1 - 1;
+    T rmax = T(0);
+    int changed = 0, evaluated = 0;
+    if (li < vn0) {
+        const int64_t gi0 = li + vw.o[0];
+        const T x0 = fma((T)gi0, P.dx[0], P.lo[0]);
+        const T S0 = P.hdx[0], S1 = P.hdx[1];
+        const T hlr = P.h * P.lr;
+        // (view nodes < 2^31: host-checked — 32-bit node offsets)
+        const int tb = li + vn0 * lj0;
+        const int8_t *__restrict__ cp = vw.cls + tb;
+        const T *__restrict__ vp = Vi + tb;
+        int8_t cls[R];
+        T vin[R], w0[R], base[R], best[R];
+        int i0[R];
+        bool anyint = false, uni = true;
+#pragma unroll
+        for (int n = 0; n < R; ++n) {
+            const int lj = lj0 + n;
+            const bool in = lj < vn1;
+            cls[n] = in ? cp[n * vn0] : (int8_t)-3;
+            vin[n] = in ? vp[n * vn0] : T(0);
+            anyint |= cls[n] == -1;
+            const T x1 = fma((T)(lj + (int)vw.o[1]), P.dx[1], P.lo[1]);
+            const T D0 = P.hdx[0] * fma(P.A[0], x0, fma(P.A[1], x1, P.b[0]));
+            i0[n] = floor_split(fma(S0, C.u0, D0), w0[n]);
+            uni &= i0[n] == i0[0];
+            base[n] = KRUZ ? P.kcost : P.h * cost_state_2d(P, x0, x1);
+            best[n] = (T)INFINITY;
+        }
+        if (anyint) {
+            // D1 does not depend on x1 (A[1][1] = 0): the row of node 0 stands for all
+            const T x1r = fma((T)(lj0 + vw.o[1]), P.dx[1], P.lo[1]);
+            const T D1 = P.hdx[1] * fma(P.A[3], x0, fma(P.A[4], x1r, P.b[1]));
+            T w1;
+            const int j0 = floor_split(fma(S1, C.u1[0], D1), w1);
+            if (fast && uni) {
+                // rows lj0 + j0 + r, r = 0 .. KC + R - 1; node n uses r = n .. n + KC
+                const T *__restrict__ p = Vi + (li + i0[0]) + (int64_t)vn0 * (lj0 + j0);
+                T xprev[R];
+#pragma unroll
+                for (int r = 0; r < KC + R; ++r) {
+                    const T a = __ldg(p), b = __ldg(p + 1);
+                    p += vn0;
+#pragma unroll
+                    for (int n = 0; n < R; ++n) {
+                        const int m = r - n;             // X index of node n
+                        if (m < 0 || m > KC) continue;
+                        const T X = lerp<T>(a, b, w0[n]);
+                        if (m >= 1) {
+                            const int k = m - 1;
+                            const T I = lerp<T>(xprev[n], X, w1);
+                            const T ck = KRUZ ? base[n] : fma(hlr, C.csq[k], base[n]);
+                            best[n] = fmin(best[n], fma(P.beta, I, ck));
+                        }
+                        xprev[n] = X;
+                    }
+                }
+            } else {
+                // k_sweep_field2d's per-control loop, node by node (unrolled: the
+                // per-node arrays stay in registers)
+                const int64_t o[3] = {vw.o[0], vw.o[1], 0};
+                const int64_t vn[3] = {vn0, vn1, 1};
+#pragma unroll
+                for (int n = 0; n < R; ++n) {
+                    if (cls[n] != -1) continue;
+                    const int lj = lj0 + n;
+                    const int64_t gi[3] = {gi0, lj + vw.o[1], 0};
+                    const T x1 = fma((T)gi[1], P.dx[1], P.lo[1]);
+                    const T D0 = P.hdx[0] * fma(P.A[0], x0, fma(P.A[1], x1, P.b[0]));
+                    const T D1n = P.hdx[1] * fma(P.A[3], x0, fma(P.A[4], x1, P.b[1]));
+                    T bn = (T)INFINITY;
+                    if (fast) {
+                        const T *__restrict__ Vn = Vi + li + (int64_t)vn0 * lj;
+#pragma unroll 1
+                        for (int k = 0; k < KC; ++k) {
+                            T wa, wb;
+                            const int ia = floor_split(fma(S0, C.u0, D0), wa);
+                            const int ib = floor_split(fma(S1, C.u1[k], D1n), wb);
+                            const T *__restrict__ q = Vn + (ia + (int64_t)vn0 * ib);
+                            const T I = lerp<T>(lerp<T>(__ldg(q), __ldg(q + 1), wa),
+                                                lerp<T>(__ldg(q + vn0), __ldg(q + vn0 + 1), wa),
+                                                wb);
+                            const T ck = KRUZ ? base[n] : fma(hlr, C.csq[k], base[n]);
+                            bn = fmin(bn, fma(P.beta, I, ck));
+                        }
+                    } else {
+#pragma unroll 1
+                        for (int k = 0; k < KC; ++k) {
+                            const T delta[3] = {fma(S0, C.u0, D0), fma(S1, C.u1[k], D1n), T(0)};
+                            const T I = interp<T, T, 2>(Vi, o, vn, P.n, P.periodic, gi, delta,
+                                                        P.v_out);
+                            const T ck = KRUZ ? base[n] : fma(hlr, C.csq[k], base[n]);
+                            bn = fmin(bn, fma(P.beta, I, ck));
+                        }
+                    }
+                    best[n] = bn;
+                }
+            }
+        }
+#pragma unroll
+        for (int n = 0; n < R; ++n) {
+            if (cls[n] == -3) continue;
+            const int lj = lj0 + n;
+            T vnew;
+            if (cls[n] == -2) {
+                vnew = P.v_out;
+            } else if (cls[n] >= 0) {
+                vnew = P.g ? P.g[(gi0) + P.n[0] * (lj + vw.o[1])] : T(0);
+            } else {
+                vnew = best[n];
+                if (P.monotone) vnew = fmin(vnew, vin[n]);
+                ++evaluated;
+            }
+            Vo[tb + n * vn0] = vnew;
+            const T dv = vnew > vin[n] ? vnew - vin[n] : vin[n] - vnew;
+            rmax = dv > rmax ? dv : rmax;
+            changed |= !same_bits(vnew, vin[n]);
+        }
+    }
+    changed_ = tile_finish(G, v, tile, it, rmax, changed, evaluated);
+    HJ_LIST_END(G, it)
+}
 
 // ---------------------------------------------------------------------------
 // Dubins car (§2 dynamics family; BASELINE config 4): the (x,y) part of
@@ -939,6 +1109,7 @@ struct SweepLaunch {
     int evals = 0;                      // brackets evaluated per interior node and sweep
                                         // (the control count unless a kernel prunes)
     bool col = false;                   // FIELD2D via k_sweep_field2d_col (shared u0)
+    bool lat = false;                   // ... via k_sweep_field2d_lat (controls one row apart)
     ColCtrl<T> colctrl;
     int seg = 0, seg_nup = 0;           // FIELD_COOP segmented control order (CoopState)
     int16_t seg_order[HJ_MAX_CONTROLS];
@@ -1070,7 +1241,7 @@ hj_status sweep_prepare(const hj_grid &g, const hj_problem &p, const hj_fields &
             if (p.A[d][e] != 0) iso = false;
     }
     const int want = p.sweep_kernel;
-    if (want < HJ_SWEEP_AUTO || want > HJ_SWEEP_FIELD_COL) {
+    if (want < HJ_SWEEP_AUTO || want > HJ_SWEEP_FIELD_LAT) {
         set_error("unknown sweep_kernel %d", want);
         return HJ_ERR_INVALID;
     }
@@ -1177,7 +1348,7 @@ hj_status sweep_prepare(const hj_grid &g, const hj_problem &p, const hj_fields &
         if (g.dim == 2 && (p.dynamics == HJ_DYN_AFFINE || p.dynamics == HJ_DYN_VANDERPOL) &&
             !g.periodic[0] && !g.periodic[1] &&
             (want == HJ_SWEEP_AUTO || want == HJ_SWEEP_FIELD2D || want == HJ_SWEEP_FIELD_COOP ||
-             want == HJ_SWEEP_FIELD_COL))
+             want == HJ_SWEEP_FIELD_COL || want == HJ_SWEEP_FIELD_LAT))
             L.kind = SWEEP_FIELD2D;
         else if (p.dynamics == HJ_DYN_DUBINS && H[2] <= 1.0 && !g.periodic[0] && !g.periodic[1] &&
                  (want == HJ_SWEEP_AUTO || want == HJ_SWEEP_DUBINS ||
@@ -1220,7 +1391,7 @@ hj_status sweep_prepare(const hj_grid &g, const hj_problem &p, const hj_fields &
         tile_dim[1] = 32;
     }
     if (L.kind == SWEEP_FIELD2D && !L.coop && p.dynamics == HJ_DYN_AFFINE && !f.speed &&
-        (want == HJ_SWEEP_AUTO || want == HJ_SWEEP_FIELD_COL)) {
+        (want == HJ_SWEEP_AUTO || want == HJ_SWEEP_FIELD_COL || want == HJ_SWEEP_FIELD_LAT)) {
         // every control moves the foot by the same amount along axis 0: one x-lerped
         // column per node (k_sweep_field2d_col)
         bool shared = true;
@@ -1276,6 +1447,28 @@ hj_status sweep_prepare(const hj_grid &g, const hj_problem &p, const hj_fields &
     // per thread sharing their column rows — 16 % fewer instructions — measured no faster:
     // the row loads' latency, not issue, then bounds it; profiles/r2/README.)
     if (L.col && p.cost == HJ_COST_DISCOUNTED) tile_dim[1] = 64;
+    if (L.col && sizeof(T) == 4 && p.cost == HJ_COST_DISCOUNTED && p.A[1][1] == 0.0 &&
+        (want == HJ_SWEEP_AUTO || want == HJ_SWEEP_FIELD_LAT) && !getenv("HJ_NO_LAT") &&
+        (p.n_controls == 17 || p.n_controls == 33 || p.n_controls == 65)) {
+        // lattice-aligned controls (k_sweep_field2d_lat): in the kernel's own arithmetic
+        // S1 (u1[k] - u1[0]) = k exactly for the sorted controls (S1 = h/dy as the kernel
+        // holds it); the products and differences are of few-bit dyadic values, so the
+        // check is done exactly in double
+        const T S1 = (T)(p.h / grid_spacing(g, 1));
+        bool unit = true;
+        for (int k = 0; k < p.n_controls; ++k) {
+            const double d = (double)S1 * ((double)L.colctrl.u1[k] - (double)L.colctrl.u1[0]);
+            if (d != (double)k) unit = false;
+        }
+        L.lat = unit && g.n[0] * g.n[1] < ((int64_t)1 << 31);   // (32-bit node offsets)
+    }
+    if (want == HJ_SWEEP_FIELD_LAT && !L.lat) {
+        set_error("sweep_kernel %d requested, but the problem does not qualify for it "
+                  "(2-D affine, discounted, no speed field, a shared axis-0 control "
+                  "component, 17/33/65 controls whose axis-1 feet are exactly one row "
+                  "apart, axis-1 drift independent of x1, fp32)", want);
+        return HJ_ERR_UNSUPPORTED;
+    }
     if (want == HJ_SWEEP_FIELD_COL && !L.col) {
         set_error("sweep_kernel %d requested, but the problem does not qualify for it "
                   "(2-D affine, no speed field, every control with the same axis-0 "
@@ -1495,7 +1688,9 @@ static hj_status launch_coop_kq(const DevProblem<T, T> &P, const SweepLaunch<T> 
                                 const CoopState &S, int64_t max_iter, double tol,
                                 cudaStream_t s) {
     constexpr int BLK = EV == 3 ? 300 : 100;
-    const size_t dyn = (size_t)CoopNW<T>::nw * 2 * BLK * sizeof(T);
+    // the staged blocks, then (segmented field class) the per-row split table
+    const size_t dyn = (size_t)CoopNW<T>::nw * 2 * BLK * sizeof(T) +
+                       (S.seg_tab ? (size_t)4 * P.n[1] : 0);
     if (S.cluster) {        // one cluster per view (at most maxc resident at a time)
         int cs = 0, maxc = 0;
         coop_cluster_shape<T, KQ, PC, EV>(dyn, cs, maxc);
@@ -1524,11 +1719,16 @@ static hj_status launch_coop_kq(const DevProblem<T, T> &P, const SweepLaunch<T> 
         }
     }
     static int grids[64] = {0};        // resident grid, per device
+    static size_t dyn_set[64] = {0};   // dynamic shared memory opted in, per device
     const int dev = current_device();
     int &grid = grids[dev];
-    if (!grid) {
+    if (dyn > dyn_set[dev]) {          // (more shared memory: re-check the occupancy)
         cudaFuncSetAttribute(k_sweep_local2d_coop<T, KQ, PC, EV>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+        dyn_set[dev] = dyn;
+        grid = 0;
+    }
+    if (!grid) {
         const int sms = device_sms();
         int per_sm = 0;
         if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sweep_local2d_coop<T, KQ, PC, EV>,
@@ -1560,6 +1760,8 @@ hj_status sweep_coop(const DevProblem<T, T> &P, const SweepLaunch<T> &L, int64_t
     S.dubins = L.kind == SWEEP_DUBINS ? 1 : 0;
     S.seg = L.seg;
     S.seg_nup = L.seg_nup;
+    // the split table (2 x n1 int16 behind the staged blocks) up to 16384 rows
+    S.seg_tab = L.seg && L.gn1 <= 16384 && !getenv("HJ_NO_SEGTAB") ? 1 : 0;
     memcpy(S.seg_order, L.seg_order, sizeof(S.seg_order));
     for (int v = 0; v < nv; ++v) {
         S.mt_base[v] = tot;
@@ -1579,6 +1781,7 @@ hj_status sweep_coop(const DevProblem<T, T> &P, const SweepLaunch<T> &L, int64_t
     // 1.25 ms: a view's work on 16 SMs outweighs the cheaper barrier), so opt-in only
     S.cluster = 0;
     if (const char *e = getenv("HJ_COOP_CLUSTER")) S.cluster = atoi(e) != 0;
+    if (S.cluster) S.seg_tab = 0;      // (cluster mode sizes its shared memory once)
     if (S.cluster) S.use_list = 0;    // (the list ring is shared by all views)
     {
         std::vector<int> ord(nv);
@@ -1658,10 +1861,38 @@ static void launch_col(const DevProblem<T, T> &P, const SweepLaunch<T> &L, int64
     }
 }
 
+template <typename T, bool KRUZ>
+static void launch_lat(const DevProblem<T, T> &P, const SweepLaunch<T> &L, int64_t it, double tol,
+                       cudaStream_t s) {
+    switch (P.K) {
+        case 17:
+            k_sweep_field2d_lat<T, KRUZ, 17>
+                <<<grid_for(k_sweep_field2d_lat<T, KRUZ, 17>, 256, 0, L.total_tiles, L.dense), 256,
+                   0, s>>>(P, L.colctrl, L.d_group, it, tol);
+            return;
+        case 33:
+            k_sweep_field2d_lat<T, KRUZ, 33>
+                <<<grid_for(k_sweep_field2d_lat<T, KRUZ, 33>, 256, 0, L.total_tiles, L.dense), 256,
+                   0, s>>>(P, L.colctrl, L.d_group, it, tol);
+            return;
+        default:
+            k_sweep_field2d_lat<T, KRUZ, 65>
+                <<<grid_for(k_sweep_field2d_lat<T, KRUZ, 65>, 256, 0, L.total_tiles, L.dense), 256,
+                   0, s>>>(P, L.colctrl, L.d_group, it, tol);
+            return;
+    }
+}
+
 template <typename T, int DYN, bool KRUZ>
 static void launch_field(const DevProblem<T, T> &P, const SweepLaunch<T> &L, int64_t it,
                          double tol, cudaStream_t s) {
     if constexpr (DYN == HJ_DYN_AFFINE) {
+        if constexpr (!KRUZ && sizeof(T) == 4) {   // (lattice kernel: fp32, discounted)
+            if (L.lat && L.dense) {
+                launch_lat<T, KRUZ>(P, L, it, tol, s);
+                return;
+            }
+        }
         if (L.col) {
             if (L.dense)
                 launch_col<T, KRUZ, 8>(P, L, it, tol, s);

@@ -53,6 +53,8 @@ struct CoopState {
     // of d1 is the control's, so the controls are kept as two groups (u1 >= 0, then
     // u1 < 0), each sorted by u0 — d0 < 0 on a prefix of each (coop_eval_field)
     int seg, seg_nup;
+    int seg_tab;                    // 1: the per-row split points are tabulated in dynamic
+                                    // shared memory once per launch (2 x n1 int16)
     int16_t seg_order[HJ_MAX_CONTROLS];
 };
 
@@ -76,6 +78,13 @@ __device__ __forceinline__ int coop_view(const CoopState &S, int64_t gid) {
     int v = 0;
     while (v + 1 < S.n_views && S.mt_base[v + 1] <= gid) ++v;
     return v;
+}
+
+// the same for a warp-uniform gid, from a shared copy of mt_base: lane v tests view v+1
+// (one shared load and a ballot instead of a serial walk over the parameter bank)
+__device__ __forceinline__ int coop_view_warp(const int32_t *__restrict__ smtb, int nv, int gid) {
+    const int lane = threadIdx.x & 31;
+    return __popc(__ballot_sync(0xffffffffu, lane + 1 < nv && smtb[lane + 1] <= gid));
 }
 
 // classes of the mini-tiles of every view: one thread per mini-tile
@@ -305,7 +314,8 @@ __device__ __forceinline__ void coop_eval_field(const DevProblem<T, T> &P, const
                                                 T &rmax_out, unsigned long long &cm_out,
                                                 int &evald_out, const SegCtl<T> *__restrict__ seg,
                                                 const T *__restrict__ seg_csq, int seg_nup,
-                                                int16_t *__restrict__ rsplit) {
+                                                int16_t *__restrict__ rsplit,
+                                                const int16_t *__restrict__ seg_tab) {
     constexpr int BP = 10;
     const int lane = threadIdx.x & 31;
     const bool mono = P.monotone != 0;
@@ -331,9 +341,14 @@ __device__ __forceinline__ void coop_eval_field(const DevProblem<T, T> &P, const
         const T D0r = P.hdx[0] * fma(P.A[0], xx0, fma(P.A[1], xx1, P.b[0]));
         const T S0r = P.hdx[0] * T(1);
         int lo = grp ? seg_nup : 0, hi = grp ? P.K : seg_nup;
-        while (lo < hi) {
-            const int mid = (lo + hi) >> 1;
-            if (fma(S0r, seg[mid].u0, D0r) < T(0)) lo = mid + 1; else hi = mid;
+        if (seg_tab) {
+            // (a mini-tile row past the grid holds no node: clamp, the value is unused)
+            lo = seg_tab[grp * (int)P.n[1] + min((int)(y0 + rr + vw.o[1]), (int)P.n[1] - 1)];
+        } else {
+            while (lo < hi) {
+                const int mid = (lo + hi) >> 1;
+                if (fma(S0r, seg[mid].u0, D0r) < T(0)) lo = mid + 1; else hi = mid;
+            }
         }
         rsplit[lane] = (int16_t)lo;
     }
@@ -689,6 +704,38 @@ __global__ void __launch_bounds__(CoopNW<T>::nw * 32,
             sseg[i].w1 = fabs(fma(P.hdx[1] * T(1), P.ctrl[k][1], T(0)));
             sseg_csq[i] = P.csq[k];
         }
+    // segmented mode: the two split points of every global row, tabulated once (behind the
+    // blocks in dynamic shared memory).  d0 = fma(S0, u0, D0) with D0 a function of the row
+    // alone (A[0][0] = 0: fma(0, x0, y) is y for every finite x0, so x0 = lo0 stands in)
+    int16_t *const segtab = reinterpret_cast<int16_t *>(coop_dyn + sizeof(T) * COOP_NW * 2 * BLK);
+    if (EV == 1 && S.seg && S.seg_tab) {
+        __syncthreads();                       // (sseg complete)
+        const int n1 = (int)P.n[1];
+        for (int e = threadIdx.x; e < 2 * n1; e += blockDim.x) {
+            const int grp = e >= n1, row = e - grp * n1;
+            const T xx0 = P.lo[0];
+            const T xx1 = fma((T)row, P.dx[1], P.lo[1]);
+            const T D0r = P.hdx[0] * fma(P.A[0], xx0, fma(P.A[1], xx1, P.b[0]));
+            const T S0r = P.hdx[0] * T(1);
+            int lo = grp ? S.seg_nup : 0, hi = grp ? P.K : S.seg_nup;
+            while (lo < hi) {
+                const int mid = (lo + hi) >> 1;
+                if (fma(S0r, sseg[mid].u0, D0r) < T(0)) lo = mid + 1; else hi = mid;
+            }
+            segtab[e] = (int16_t)lo;
+        }
+    }
+    // the views' mini-tile numbering, in shared memory (warp-uniform lookups by ballot)
+    __shared__ int32_t smtb[HJ_GROUP_VIEWS + 1], smt0[HJ_GROUP_VIEWS], smt1[HJ_GROUP_VIEWS],
+        smt2[HJ_GROUP_VIEWS];
+    if (threadIdx.x <= (unsigned)S.n_views) {
+        smtb[threadIdx.x] = (int32_t)S.mt_base[threadIdx.x];
+        if (threadIdx.x < (unsigned)S.n_views) {
+            smt0[threadIdx.x] = S.mt0[threadIdx.x];
+            smt1[threadIdx.x] = S.mt1[threadIdx.x];
+            smt2[threadIdx.x] = S.mt2[threadIdx.x];
+        }
+    }
     // Dubins: extreme |h w a_k / dth| of each sign group (coop_eval_dubins)
     __shared__ T dub_wext[4];
     if (EV == 3 && threadIdx.x == 0) {
@@ -835,11 +882,11 @@ __global__ void __launch_bounds__(CoopNW<T>::nw * 32,
 #pragma unroll
             for (int s2 = 0; s2 < 2; ++s2) {
                 const int g = gid[s2] < 0 ? gid[0] : gid[s2];
-                const int v = coop_view(S, g);
-                const int mt = g - (int)S.mt_base[v], m0 = S.mt0[v];
+                const int v = coop_view_warp(smtb, S.n_views, g);
+                const int mt = g - smtb[v], m0 = smt0[v];
                 vv[s2] = v;
                 if (EV == 3) {
-                    const int pl = m0 * S.mt1[v];
+                    const int pl = m0 * smt1[v];
                     mz[s2] = mt / pl;
                     const int r = mt - mz[s2] * pl;
                     my[s2] = r / m0;
@@ -957,7 +1004,8 @@ __global__ void __launch_bounds__(CoopNW<T>::nw * 32,
                                                lst[warp][s2], d_s, e_s, x0, y0,
                                                vw.V[(n + 1) & 1], rmax, cm, evald,
                                                EV == 1 && S.seg ? sseg : nullptr, sseg_csq,
-                                               S.seg_nup, srsplit[EV == 1 ? warp : 0]);
+                                               S.seg_nup, srsplit[EV == 1 ? warp : 0],
+                                               EV == 1 && S.seg_tab ? segtab : nullptr);
                 cm = ((unsigned long long)__reduce_or_sync(0xffffffffu, (unsigned)(cm >> 32)) << 32) |
                      (unsigned long long)__reduce_or_sync(0xffffffffu, (unsigned)cm);
 #pragma unroll
@@ -987,13 +1035,12 @@ __global__ void __launch_bounds__(CoopNW<T>::nw * 32,
                     const int dx = l9 % 3 - 1, dy = (l9 / 3) % 3 - 1, dz = l9 / 9 - 1;
                     const int nx = (s2 ? mx[1] : mx[0]) + dx, ny = (s2 ? my[1] : my[0]) + dy;
                     int nz = (s2 ? mz[1] : mz[0]) + (EV == 3 ? dz : 0);
-                    if (nz < 0) nz += S.mt2[v];
-                    if (nz >= S.mt2[v]) nz -= S.mt2[v];
-                    if (nx >= 0 && ny >= 0 && nx < S.mt0[v] && ny < S.mt1[v]) {
+                    if (nz < 0) nz += smt2[v];
+                    if (nz >= smt2[v]) nz -= smt2[v];
+                    if (nx >= 0 && ny >= 0 && nx < smt0[v] && ny < smt1[v]) {
                         const unsigned long long bits = coop_spread(cm, dx, dy);
                         if (bits) {
-                            const int64_t nid = S.mt_base[v] + nx +
-                                                (int64_t)S.mt0[v] * (ny + (int64_t)S.mt1[v] * nz);
+                            const int nid = smtb[v] + nx + smt0[v] * (ny + smt1[v] * nz);
                             if (S.use_list) {    // a mask that was empty: list the mini-tile
                                 const unsigned long long old = atomicOr(&dnext[nid], bits);
                                 if (old == 0ull)

@@ -79,7 +79,7 @@ EXPORTS = ["hj_last_error", "hj_version", "hj_solve_workspace_bytes", "hj_solve"
 # hj.h HJ_SWEEP_*
 SWEEP_KERNELS = {"auto": 0, "generic": 1, "local_scalar": 2, "local_packed": 3, "field2d": 4,
                  "dubins": 5, "local_tb": 6, "local_coop": 7,
-                 "field_coop": 8, "dubins_coop": 9, "field_col": 10}
+                 "field_coop": 8, "dubins_coop": 9, "field_col": 10, "field_lat": 11}
 
 
 def lib():

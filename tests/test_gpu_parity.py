@@ -264,6 +264,81 @@ def test_field_col_bit_identical_to_field2d(case, dtype):
     assert out["field2d"][1] == out["field_col"][1]
 
 
+def _lat_problem(case):
+    """Config 5's regulator on a dyadic 257-node grid ([-2,2], dx = 2^-6, h = 2^-4, so
+    h/dy = 4): 17/33/65 controls along axis 1, 1/4 apart — every control step moves the
+    foot by exactly one row (the class k_sweep_field2d_lat serves)."""
+    A = np.zeros((3, 3))
+    A[0, 1], A[1, 0] = 1.0, -0.5
+    K = {"k33": 33, "k65": 65}.get(case, 17)
+    ctrl = W.interval_controls(K, axis=1) * (0.25 * (K - 1) / 2)
+    kw = dict(A=A, cost=W.COST_DISCOUNTED, lam=1.0, lq=1.0, lr=0.1, tol=1e-6, h=2.0 ** -4)
+    n, hi = (257, 257), (2.0, 2.0)
+    if case == "lr":
+        kw["lr"] = 0.7
+    elif case == "shifted_u0":
+        ctrl[:, 0] = 0.25
+    elif case == "b1":            # a constant axis-1 drift (dyadic)
+        kw["b"] = np.array([0.0, 0.375, 0.0])
+    elif case == "a00":           # axis-0 drift depends on x0: i0 varies along a column
+        A[0, 0] = 0.25
+    elif case == "ragged":        # 257 x 201: ragged tiles on both axes, same spacing
+        n, hi = (257, 201), (2.0, -2.0 + 200 * 2.0 ** -6)
+    elif case == "reversed_order":
+        ctrl = ctrl[::-1].copy()
+    g = W.Grid(n, (-2.0, -2.0), hi, (False, False))
+    h = kw["h"]
+    l_max = 8.0 + 0.1 * float(np.max(np.sum(ctrl ** 2, axis=1)))
+    kw["v_out"] = h * l_max * (1.0 + h) / h      # h l_max / (1 - beta)
+    return _tiny(n, lo=(-2.0, -2.0), hi=hi, ctrl=ctrl, piece=W.sector_pieces(g, 0.3, 4), **kw)
+
+
+@pytest.mark.parametrize("case", ["k17", "k33", "k65", "lr", "shifted_u0", "b1", "a00", "ragged",
+                                  "reversed_order"])
+def test_field_lat_bit_identical_to_field2d(case):
+    """k_sweep_field2d_lat (controls one row apart: shared axis-1 weight, eight nodes of a
+    column per thread streaming the rows once) against k_sweep_field2d and the oracle: on
+    these dyadic problems every per-control foot sum is exact, so the iterates and the
+    iteration count must be identical bit for bit; the oracle within the fp32 bound."""
+    p = _lat_problem(case)
+    Vo, it_o, _ = oracle.OracleProblem(p).solve()
+    out = {}
+    for kernel in ("field2d", "field_lat"):
+        V, rep = hj.hj_solve(hj.DeviceProblem(p, "f32", sweep_kernel=kernel))
+        assert rep["converged"]
+        assert np.abs(V.double().cpu().numpy() - Vo).max() <= TOL["f32"] * 60, kernel
+        out[kernel] = (V.cpu(), rep["iterations"])
+    assert torch.equal(out["field2d"][0], out["field_lat"][0])
+    assert out["field2d"][1] == out["field_lat"][1]
+    # AUTO picks the lattice kernel for this class
+    V, rep = hj.hj_solve(hj.DeviceProblem(p, "f32"))
+    assert torch.equal(V.cpu(), out["field_lat"][0])
+
+
+def test_field_lat_refuses_off_lattice_controls():
+    p = _lat_problem("k17")
+    p.controls = p.controls * 0.9          # 0.9 rows apart
+    with pytest.raises(hj.HJError, match="does not qualify"):
+        hj.hj_solve(hj.DeviceProblem(p, "f32", sweep_kernel="field_lat"))
+    with pytest.raises(hj.HJError, match="does not qualify"):   # fp32 only
+        hj.hj_solve(hj.DeviceProblem(_lat_problem("k17"), "f64", sweep_kernel="field_lat"))
+
+
+def test_field_lat_full_size_config5_matches_field2d():
+    """Full-size config 5 (16385^2, 33 controls, h/dy = 16): the automatic choice is the
+    lattice kernel, and its first sweeps equal k_sweep_field2d's bit for bit."""
+    cfg = W.make(5)
+    Vs = {}
+    for kernel in ("field2d", "auto"):
+        dp = hj.DeviceProblem(cfg.fine, "f32", sweep_kernel=kernel)
+        V, rep = hj.hj_solve(dp, max_iter=6, allow_not_converged=True)
+        assert rep["iterations"] == 6
+        Vs[kernel] = V
+        del dp
+    assert torch.equal(Vs["field2d"], Vs["auto"])
+    assert hj.lib() is not None
+
+
 def test_local_kernel_refuses_nonlocal_problem():
     cfg = _cfg(3)                        # Zermelo drift: feet leave the 3x3 cell block
     with pytest.raises(hj.HJError, match="does not qualify"):
