@@ -20,6 +20,7 @@
 #pragma once
 
 #include <algorithm>
+#include <type_traits>
 #include <vector>
 
 #include "hj_host.cuh"
@@ -884,19 +885,34 @@ __global__ void __launch_bounds__(256, 2)
             const T D1 = P.hdx[1] * fma(P.A[3], x0, fma(P.A[4], x1r, P.b[1]));
             T w1;
             const int j0 = floor_split(fma(S1, C.u1[0], D1), w1);
-            if (fast && uni) {
-                // rows lj0 + j0 + r, r = 0 .. KC + R - 1; node n uses r = n .. n + KC
-                const T *__restrict__ p = Vi + (li + i0[0]) + (int64_t)vn0 * (lj0 + j0);
+            // the 8 rows' foot cells on axis 0: one cell (uni) or two adjacent cells (a
+            // row of the column crosses a cell boundary: three values per row, each node
+            // takes its pair — the same lerp operands)
+            int i0lo = i0[0], i0hi = i0[0];
+#pragma unroll
+            for (int n = 1; n < R; ++n) {
+                i0lo = min(i0lo, i0[n]);
+                i0hi = max(i0hi, i0[n]);
+            }
+            // rows lj0 + j0 + r, r = 0 .. KC + R - 1; node n uses r = n .. n + KC
+            auto stream_rows = [&](auto two_tag) {
+                constexpr bool TWO = decltype(two_tag)::value;
+                const T *__restrict__ p = Vi + (li + i0lo) + (int64_t)vn0 * (lj0 + j0);
+                bool up[R];
+#pragma unroll
+                for (int n = 0; n < R; ++n) up[n] = TWO && i0[n] != i0lo;
                 T xprev[R];
 #pragma unroll
                 for (int r = 0; r < KC + R; ++r) {
                     const T a = __ldg(p), b = __ldg(p + 1);
+                    const T c = TWO ? __ldg(p + 2) : b;
                     p += vn0;
 #pragma unroll
                     for (int n = 0; n < R; ++n) {
                         const int m = r - n;             // X index of node n
                         if (m < 0 || m > KC) continue;
-                        const T X = lerp<T>(a, b, w0[n]);
+                        const T X = TWO ? lerp<T>(up[n] ? b : a, up[n] ? c : b, w0[n])
+                                        : lerp<T>(a, b, w0[n]);
                         if (m >= 1) {
                             const int k = m - 1;
                             const T I = lerp<T>(xprev[n], X, w1);
@@ -906,6 +922,16 @@ __global__ void __launch_bounds__(256, 2)
                         xprev[n] = X;
                     }
                 }
+            };
+            // every value the streamed rows touch inside the view (this thread's footprint,
+            // not the tile's: edge tiles keep most threads on this path); then every foot
+            // is inside the box and the view, where interp() reads exactly these corners
+            const bool tfast = li + i0lo >= 0 && li + i0hi + 1 <= vn0 - 1 && lj0 + j0 >= 0 &&
+                               lj0 + j0 + KC + R - 1 <= vn1 - 1 && i0hi <= i0lo + 1;
+            if (tfast && uni) {
+                stream_rows(std::integral_constant<bool, false>());
+            } else if (tfast) {
+                stream_rows(std::integral_constant<bool, true>());
             } else {
                 // k_sweep_field2d's per-control loop, node by node (unrolled: the
                 // per-node arrays stay in registers)

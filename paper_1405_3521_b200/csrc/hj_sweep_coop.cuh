@@ -643,6 +643,10 @@ struct CoopBits<double> {
     static __device__ __forceinline__ double value(U b) { return __longlong_as_double((long long)b); }
 };
 
+#ifndef HJ_COOP_TRACE
+#define HJ_COOP_TRACE 0      // 1: per-sweep phase timestamps (tools/coop_trace.py, a variant build)
+#endif
+
 // warps per CTA: fp32 one 512-thread CTA per SM (fewer barrier arrivals); fp64 (its
 // staged blocks are twice the size) two 256-thread CTAs per SM
 #ifndef HJ_COOP_MINB32
@@ -775,8 +779,10 @@ __global__ void __launch_bounds__(CoopNW<T>::nw * 32,
     // would cost an L2 round trip in front of the CTA's arrival)
     unsigned long long *const tr_buf = g_tb_trace.buf;
     const long long tr_cap = g_tb_trace.cap;
-    const bool tr = tr_buf != nullptr && blockIdx.x == 0 && threadIdx.x == 0;
-    const bool tr_all = tr_buf != nullptr && threadIdx.x == 0 && gridDim.x <= 256;
+    // (compiled in only with -DHJ_COOP_TRACE=1: the timestamps would otherwise hold ~14
+    // registers live across the sweep loop)
+    const bool tr = HJ_COOP_TRACE && tr_buf != nullptr && blockIdx.x == 0 && threadIdx.x == 0;
+    const bool tr_all = HJ_COOP_TRACE && tr_buf != nullptr && threadIdx.x == 0 && gridDim.x <= 256;
     unsigned long long t_a = 0, t_b = 0, t_s = 0, t_l = 0, t_e = 0, t_m = 0, t_q = 0;
     int qitems = 0;
     for (int vs = (int)grp; vs < (CL ? S.n_views : 1); vs += (int)ngrp) {

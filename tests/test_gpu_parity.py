@@ -280,6 +280,8 @@ def _lat_problem(case):
         ctrl[:, 0] = 0.25
     elif case == "b1":            # a constant axis-1 drift (dyadic)
         kw["b"] = np.array([0.0, 0.375, 0.0])
+    elif case == "b0":            # axis-0 feet cross a cell boundary inside a thread's 8 rows
+        kw["b"] = np.array([0.03125, 0.0, 0.0])
     elif case == "a00":           # axis-0 drift depends on x0: i0 varies along a column
         A[0, 0] = 0.25
     elif case == "ragged":        # 257 x 201: ragged tiles on both axes, same spacing
@@ -293,8 +295,8 @@ def _lat_problem(case):
     return _tiny(n, lo=(-2.0, -2.0), hi=hi, ctrl=ctrl, piece=W.sector_pieces(g, 0.3, 4), **kw)
 
 
-@pytest.mark.parametrize("case", ["k17", "k33", "k65", "lr", "shifted_u0", "b1", "a00", "ragged",
-                                  "reversed_order"])
+@pytest.mark.parametrize("case", ["k17", "k33", "k65", "lr", "shifted_u0", "b1", "b0", "a00",
+                                  "ragged", "reversed_order"])
 def test_field_lat_bit_identical_to_field2d(case):
     """k_sweep_field2d_lat (controls one row apart: shared axis-1 weight, eight nodes of a
     column per thread streaming the rows once) against k_sweep_field2d and the oracle: on

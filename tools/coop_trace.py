@@ -1,4 +1,6 @@
-"""Per-sweep timeline of the cooperative local kernel (block 0's view):
+"""Per-sweep timeline of the cooperative local kernel (block 0's view) — needs a library
+built with the trace compiled in: bash tools/build_variant.sh /tmp/libhj_tr.so -DHJ_COOP_TRACE=1,
+then HJ_LIB_PATH=/tmp/libhj_tr.so;
 python tools/coop_trace.py [CONFIG] — items, block-0 item phase, barrier wait, per sweep."""
 import ctypes
 import os
