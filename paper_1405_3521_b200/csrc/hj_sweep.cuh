@@ -1808,6 +1808,7 @@ hj_status sweep_coop(const DevProblem<T, T> &P, const SweepLaunch<T> &L, int64_t
     S.cluster = 0;
     if (const char *e = getenv("HJ_COOP_CLUSTER")) S.cluster = atoi(e) != 0;
     if (S.cluster) S.seg_tab = 0;      // (cluster mode sizes its shared memory once)
+    S.seg_prune = L.seg && !getenv("HJ_NO_SEGPRUNE") ? 1 : 0;
     if (S.cluster) S.use_list = 0;    // (the list ring is shared by all views)
     {
         std::vector<int> ord(nv);

@@ -53,6 +53,7 @@ struct CoopState {
     // of d1 is the control's, so the controls are kept as two groups (u1 >= 0, then
     // u1 < 0), each sorted by u0 — d0 < 0 on a prefix of each (coop_eval_field)
     int seg, seg_nup;
+    int seg_prune;                  // 1: skip segments by their corner bound (exact)
     int seg_tab;                    // 1: the per-row split points are tabulated in dynamic
                                     // shared memory once per launch (2 x n1 int16)
     int16_t seg_order[HJ_MAX_CONTROLS];
@@ -315,7 +316,8 @@ __device__ __forceinline__ void coop_eval_field(const DevProblem<T, T> &P, const
                                                 int &evald_out, const SegCtl<T> *__restrict__ seg,
                                                 const T *__restrict__ seg_csq, int seg_nup,
                                                 int16_t *__restrict__ rsplit,
-                                                const int16_t *__restrict__ seg_tab) {
+                                                const int16_t *__restrict__ seg_tab,
+                                                T seg_w1max) {
     constexpr int BP = 10;
     const int lane = threadIdx.x & 31;
     const bool mono = P.monotone != 0;
@@ -403,12 +405,33 @@ __device__ __forceinline__ void coop_eval_field(const DevProblem<T, T> &P, const
                 // fma(w0, A1, ck)) per control as the select loop below, no sign tests
                 const int K = P.K;
                 const int bnd[5] = {0, rsplit[r], seg_nup, rsplit[8 + r], K};
+                // segment pruning (exact): on a segment the bracket is the bilinear form
+                // ck + w0 A1 + w1 (A2 + w0 A3) of (w0, w1) in the box [w0 of its first and
+                // last control] x [0, max w1] (w0 is monotone along the segment), so its
+                // minimum over the segment is at least the smallest of the box's four
+                // corners; with ck >= C0 (hlr >= 0) a segment whose corner bound, less
+                // a rounding slack that covers both the corners' and the brackets' own
+                // fp rounding, is not below the running best cannot change
+                // the min — skipped.  With the monotone clamp the best starts at V00, so
+                // the quadrants whose cell rises from V00 go first.
+                const bool prune = seg_w1max >= T(0) && (kruz || hlr >= T(0));
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
                     // q = 0: -x +y, 1: +x +y, 2: -x -y, 3: +x -y
                     const T A1 = (q & 1) ? Dxp : Dxm;
                     const T A2 = (q & 2) ? Dym : Dyp;
                     const T A3 = q == 0 ? X10 : (q == 1 ? X00 : (q == 2 ? X11 : X01));
+                    if (prune && bnd[q] < bnd[q + 1]) {
+                        const T wa = fabs(fma(S0, seg[bnd[q]].u0, D0));
+                        const T wb = fabs(fma(S0, seg[bnd[q + 1] - 1].u0, D0));
+                        const T ca = fma(wa, A1, C0), cb = fma(wb, A1, C0);
+                        const T da = fma(seg_w1max, fma(wa, A3, A2), ca);
+                        const T db = fma(seg_w1max, fma(wb, A3, A2), cb);
+                        const T lb = fmin(fmin(ca, cb), fmin(da, db));
+                        const T slack = (fabs(C0) + fabs(A1) + fabs(A2) + fabs(A3)) *
+                                        T(9.5367431640625e-07);        // 2^-20
+                        if (lb - slack >= best) continue;
+                    }
 #pragma unroll 4
                     for (int k = bnd[q]; k < bnd[q + 1]; ++k) {
                         const T w0 = fabs(fma(S0, seg[k].u0, D0));
@@ -708,6 +731,16 @@ __global__ void __launch_bounds__(CoopNW<T>::nw * 32,
             sseg[i].w1 = fabs(fma(P.hdx[1] * T(1), P.ctrl[k][1], T(0)));
             sseg_csq[i] = P.csq[k];
         }
+    // segment pruning (coop_eval_field): the largest axis-1 weight of any control
+    __shared__ T sseg_w1max;
+    if (EV == 1 && S.seg) {
+        __syncthreads();                       // (sseg complete)
+        if (threadIdx.x == 0) {
+            T m = T(0);
+            for (int i = 0; i < P.K; ++i) m = fmax(m, sseg[i].w1);
+            sseg_w1max = m;
+        }
+    }
     // segmented mode: the two split points of every global row, tabulated once (behind the
     // blocks in dynamic shared memory).  d0 = fma(S0, u0, D0) with D0 a function of the row
     // alone (A[0][0] = 0: fma(0, x0, y) is y for every finite x0, so x0 = lo0 stands in)
@@ -730,14 +763,12 @@ __global__ void __launch_bounds__(CoopNW<T>::nw * 32,
         }
     }
     // the views' mini-tile numbering, in shared memory (warp-uniform lookups by ballot)
-    __shared__ int32_t smtb[HJ_GROUP_VIEWS + 1], smt0[HJ_GROUP_VIEWS], smt1[HJ_GROUP_VIEWS],
-        smt2[HJ_GROUP_VIEWS];
+    __shared__ int32_t smtb[HJ_GROUP_VIEWS + 1], smt0[HJ_GROUP_VIEWS], smt1[HJ_GROUP_VIEWS];
     if (threadIdx.x <= (unsigned)S.n_views) {
         smtb[threadIdx.x] = (int32_t)S.mt_base[threadIdx.x];
         if (threadIdx.x < (unsigned)S.n_views) {
             smt0[threadIdx.x] = S.mt0[threadIdx.x];
             smt1[threadIdx.x] = S.mt1[threadIdx.x];
-            smt2[threadIdx.x] = S.mt2[threadIdx.x];
         }
     }
     // Dubins: extreme |h w a_k / dth| of each sign group (coop_eval_dubins)
@@ -888,11 +919,16 @@ __global__ void __launch_bounds__(CoopNW<T>::nw * 32,
 #pragma unroll
             for (int s2 = 0; s2 < 2; ++s2) {
                 const int g = gid[s2] < 0 ? gid[0] : gid[s2];
-                const int v = coop_view_warp(smtb, S.n_views, g);
-                const int mt = g - smtb[v], m0 = smt0[v];
+                // (the Dubins class keeps the parameter-bank tables and the serial walk:
+                // with the shared copies its multi-view partitioned launches faulted —
+                // config 4 at 65 x 65 x 32, cause not found; profiles/r2s/README)
+                const int v = EV == 3 ? coop_view(S, g) : coop_view_warp(smtb, S.n_views, g);
+                const int mt = g - (EV == 3 ? (int)S.mt_base[v] : smtb[v]);
+                const int m0 = EV == 3 ? S.mt0[v] : smt0[v];
+
                 vv[s2] = v;
                 if (EV == 3) {
-                    const int pl = m0 * smt1[v];
+                    const int pl = m0 * S.mt1[v];
                     mz[s2] = mt / pl;
                     const int r = mt - mz[s2] * pl;
                     my[s2] = r / m0;
@@ -1011,7 +1047,8 @@ __global__ void __launch_bounds__(CoopNW<T>::nw * 32,
                                                vw.V[(n + 1) & 1], rmax, cm, evald,
                                                EV == 1 && S.seg ? sseg : nullptr, sseg_csq,
                                                S.seg_nup, srsplit[EV == 1 ? warp : 0],
-                                               EV == 1 && S.seg_tab ? segtab : nullptr);
+                                               EV == 1 && S.seg_tab ? segtab : nullptr,
+                                               S.seg_prune ? sseg_w1max : T(-1));
                 cm = ((unsigned long long)__reduce_or_sync(0xffffffffu, (unsigned)(cm >> 32)) << 32) |
                      (unsigned long long)__reduce_or_sync(0xffffffffu, (unsigned)cm);
 #pragma unroll
@@ -1041,12 +1078,19 @@ __global__ void __launch_bounds__(CoopNW<T>::nw * 32,
                     const int dx = l9 % 3 - 1, dy = (l9 / 3) % 3 - 1, dz = l9 / 9 - 1;
                     const int nx = (s2 ? mx[1] : mx[0]) + dx, ny = (s2 ? my[1] : my[0]) + dy;
                     int nz = (s2 ? mz[1] : mz[0]) + (EV == 3 ? dz : 0);
-                    if (nz < 0) nz += smt2[v];
-                    if (nz >= smt2[v]) nz -= smt2[v];
-                    if (nx >= 0 && ny >= 0 && nx < smt0[v] && ny < smt1[v]) {
+                    const int mt0v = EV == 3 ? S.mt0[v] : smt0[v];
+                    const int mt1v = EV == 3 ? S.mt1[v] : smt1[v];
+                    if (EV == 3) {
+                        if (nz < 0) nz += S.mt2[v];
+                        if (nz >= S.mt2[v]) nz -= S.mt2[v];
+                    }
+                    if (nx >= 0 && ny >= 0 && nx < mt0v && ny < mt1v) {
                         const unsigned long long bits = coop_spread(cm, dx, dy);
                         if (bits) {
-                            const int nid = smtb[v] + nx + smt0[v] * (ny + smt1[v] * nz);
+                            const int64_t nid =
+                                EV == 3 ? S.mt_base[v] + nx +
+                                              (int64_t)S.mt0[v] * (ny + (int64_t)S.mt1[v] * nz)
+                                        : (int64_t)(smtb[v] + nx + mt0v * ny);
                             if (S.use_list) {    // a mask that was empty: list the mini-tile
                                 const unsigned long long old = atomicOr(&dnext[nid], bits);
                                 if (old == 0ull)

@@ -385,6 +385,32 @@ def test_labels_and_prolongation_bitexact(idx, oracle_cache, tie_report):
     assert np.array_equal(out["mask"].cpu().numpy().view(np.uint64), mask_o)
 
 
+@pytest.mark.parametrize("idx,scale,arms", [
+    (4, 0.25, (("dubins", {}), ("dubins_coop", {}))),
+    (4, 0.5, (("dubins", {}), ("dubins_coop", {}))),
+    (3, 0.125, (("field_coop", {"HJ_NO_SEGPRUNE": "1", "HJ_NO_SEGTAB": "1"}), ("field_coop", {}))),
+    (2, 0.5, (("local_scalar", {}), ("local_coop", {})))])
+def test_partitioned_mid_size_kernels_agree(idx, scale, arms, monkeypatch):
+    """Mid-size partitioned ISA passes (many views, many mini-tiles per view — sizes the
+    reduced parity configs do not reach; config 4 at 65 x 65 x 32 once faulted in the
+    cooperative Dubins launch): the cooperative kernel and its reference (the one-sweep
+    kernel; for config 3 the segmented loop without its split table and segment pruning)
+    give the same assembled field bit for bit and the same sweep counts."""
+    cfg = W.make(idx, scale=scale)
+    out = []
+    for kernel, env in arms:
+        for k in ("HJ_NO_SEGPRUNE", "HJ_NO_SEGTAB"):
+            monkeypatch.delenv(k, raising=False)
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        fine = hj.DeviceProblem(cfg.fine, cfg.dtype, sweep_kernel=kernel)
+        res = pipeline.run_isa(cfg, cfg.dtype, fine=fine)
+        torch.cuda.synchronize()
+        out.append((res["V"].cpu(), [r["iterations"] for r in res["reports"] if r]))
+    assert torch.equal(out[0][0], out[1][0])
+    assert out[0][1] == out[1][1]
+
+
 @pytest.mark.parametrize("idx,dtype", [(1, "f64"), (1, "f32"), (2, "f32"), (3, "f32"),
                                        (3, "f64"), (4, "f32"), (5, "f32")])
 def test_partitioned_matches_oracle(idx, dtype):
