@@ -583,13 +583,21 @@ __device__ __forceinline__ void coop_eval_dubins(const DevProblem<T, T> &P, cons
             T wx = x - fx, wy = y - fy;
             if (cx > P.n[0] - 2) { cx = P.n[0] - 2; wx = T(1); }
             if (cy > P.n[1] - 2) { cy = P.n[1] - 2; wy = T(1); }
-            const int rx = (int)(cx - gi0), ry = (int)(cy - gi1);   // in {-1, 0}
+            // cell offsets in {-1, 0, 1}: +1 when the foot offset is exactly one cell (h =
+            // dx / max|f| puts every foot of the th = 0 and th = pi/2 planes there); then
+            // the cell's far corner lies one past the staged block and enters with weight
+            // 0, where any finite value gives the same lerp — its index is clamped into
+            // the block (reading past it took other warps' data and, at the end of the
+            // shared window, faulted: the config-4 nondeterminism of round 2)
+            const int rx = (int)(cx - gi0), ry = (int)(cy - gi1);
+            const int bx0 = c + 1 + rx, by0 = r + 1 + ry;
+            const int bx1 = min(bx0 + 1, BP - 1), by1 = min(by0 + 1, BP - 1);
             T I3[3];
 #pragma unroll
             for (int s = 0; s < 3; ++s) {
-                const T *pl = b + s * BP * BP + (r + 1 + ry) * BP + (c + 1 + rx);
-                const T a = lerp<T>(pl[0], pl[1], wx);
-                const T bb = lerp<T>(pl[BP], pl[BP + 1], wx);
+                const T *pl = b + s * BP * BP;
+                const T a = lerp<T>(pl[by0 * BP + bx0], pl[by0 * BP + bx1], wx);
+                const T bb = lerp<T>(pl[by1 * BP + bx0], pl[by1 * BP + bx1], wx);
                 I3[s] = lerp<T>(a, bb, wy);
             }
             const T dM = I3[0] - I3[1], dP = I3[2] - I3[1];
@@ -666,6 +674,13 @@ struct CoopBits<double> {
     static __device__ __forceinline__ double value(U b) { return __longlong_as_double((long long)b); }
 };
 
+#ifndef HJ_COOP_DUBINS_MINB
+#define HJ_COOP_DUBINS_MINB 2   // resident 512-thread CTAs per SM asked of ptxas, Dubins class
+#endif
+#ifndef HJ_COOP_DUBINS_DYNQ
+#define HJ_COOP_DUBINS_DYNQ 1   // the Dubins class claims pairs from the CTA queue too (0: the
+                                // static split (w, w + NW), ...: config 4 99.8 vs 89.2 ms)
+#endif
 #ifndef HJ_COOP_TRACE
 #define HJ_COOP_TRACE 0      // 1: per-sweep phase timestamps (tools/coop_trace.py, a variant build)
 #endif
@@ -694,7 +709,7 @@ template <typename T, int KQ, bool PC, int EV = 0, bool CL = false>
 // (Dubins, EV 3: two 512-thread CTAs per SM at 64 registers measured 10 % faster on
 // config 4; the 2-D classes spill and lose at 64 registers — profiles/r2/occupancy_r2j.txt)
 __global__ void __launch_bounds__(CoopNW<T>::nw * 32,
-                                  EV == 3 && CoopNW<T>::nw <= 16 ? 2 : CoopNW<T>::minb)
+                                  EV == 3 && CoopNW<T>::nw <= 16 ? HJ_COOP_DUBINS_MINB : CoopNW<T>::minb)
     k_sweep_local2d_coop(const DevProblem<T, T> P, const LocalCtrl<T> C,
                          const SweepGroup<T> *__restrict__ G, const CoopState S,
                          int64_t max_iter, double tol) {
@@ -763,12 +778,14 @@ __global__ void __launch_bounds__(CoopNW<T>::nw * 32,
         }
     }
     // the views' mini-tile numbering, in shared memory (warp-uniform lookups by ballot)
-    __shared__ int32_t smtb[HJ_GROUP_VIEWS + 1], smt0[HJ_GROUP_VIEWS], smt1[HJ_GROUP_VIEWS];
+    __shared__ int32_t smtb[HJ_GROUP_VIEWS + 1], smt0[HJ_GROUP_VIEWS], smt1[HJ_GROUP_VIEWS],
+        smt2[HJ_GROUP_VIEWS];
     if (threadIdx.x <= (unsigned)S.n_views) {
         smtb[threadIdx.x] = (int32_t)S.mt_base[threadIdx.x];
         if (threadIdx.x < (unsigned)S.n_views) {
             smt0[threadIdx.x] = S.mt0[threadIdx.x];
             smt1[threadIdx.x] = S.mt1[threadIdx.x];
+            smt2[threadIdx.x] = S.mt2[threadIdx.x];
         }
     }
     // Dubins: extreme |h w a_k / dth| of each sign group (coop_eval_dubins)
@@ -894,8 +911,9 @@ __global__ void __launch_bounds__(CoopNW<T>::nw * 32,
         // updates of both go out together
         // the warps claim two queued mini-tiles at a time from a shared counter: a warp that
         // finishes early takes the next pair instead of waiting at the CTA barrier
-        // (the Dubins class keeps the static split: (warp, warp + NW), (warp + 2 NW, ...))
-        constexpr bool DYNQ = EV != 3;
+        // (HJ_COOP_DUBINS_DYNQ=0: the Dubins class takes the static split (warp, warp + NW),
+        // (warp + 2 NW, ...) instead)
+        constexpr bool DYNQ = EV != 3 || HJ_COOP_DUBINS_DYNQ;
         for (int itw = warp;; itw += 2 * COOP_NW) {
             int it = itw;
             if (DYNQ) {
@@ -919,16 +937,12 @@ __global__ void __launch_bounds__(CoopNW<T>::nw * 32,
 #pragma unroll
             for (int s2 = 0; s2 < 2; ++s2) {
                 const int g = gid[s2] < 0 ? gid[0] : gid[s2];
-                // (the Dubins class keeps the parameter-bank tables and the serial walk:
-                // with the shared copies its multi-view partitioned launches faulted —
-                // config 4 at 65 x 65 x 32, cause not found; profiles/r2s/README)
-                const int v = EV == 3 ? coop_view(S, g) : coop_view_warp(smtb, S.n_views, g);
-                const int mt = g - (EV == 3 ? (int)S.mt_base[v] : smtb[v]);
-                const int m0 = EV == 3 ? S.mt0[v] : smt0[v];
+                const int v = coop_view_warp(smtb, S.n_views, g);
+                const int mt = g - smtb[v], m0 = smt0[v];
 
                 vv[s2] = v;
                 if (EV == 3) {
-                    const int pl = m0 * S.mt1[v];
+                    const int pl = m0 * smt1[v];
                     mz[s2] = mt / pl;
                     const int r = mt - mz[s2] * pl;
                     my[s2] = r / m0;
@@ -1078,19 +1092,14 @@ __global__ void __launch_bounds__(CoopNW<T>::nw * 32,
                     const int dx = l9 % 3 - 1, dy = (l9 / 3) % 3 - 1, dz = l9 / 9 - 1;
                     const int nx = (s2 ? mx[1] : mx[0]) + dx, ny = (s2 ? my[1] : my[0]) + dy;
                     int nz = (s2 ? mz[1] : mz[0]) + (EV == 3 ? dz : 0);
-                    const int mt0v = EV == 3 ? S.mt0[v] : smt0[v];
-                    const int mt1v = EV == 3 ? S.mt1[v] : smt1[v];
                     if (EV == 3) {
-                        if (nz < 0) nz += S.mt2[v];
-                        if (nz >= S.mt2[v]) nz -= S.mt2[v];
+                        if (nz < 0) nz += smt2[v];
+                        if (nz >= smt2[v]) nz -= smt2[v];
                     }
-                    if (nx >= 0 && ny >= 0 && nx < mt0v && ny < mt1v) {
+                    if (nx >= 0 && ny >= 0 && nx < smt0[v] && ny < smt1[v]) {
                         const unsigned long long bits = coop_spread(cm, dx, dy);
                         if (bits) {
-                            const int64_t nid =
-                                EV == 3 ? S.mt_base[v] + nx +
-                                              (int64_t)S.mt0[v] * (ny + (int64_t)S.mt1[v] * nz)
-                                        : (int64_t)(smtb[v] + nx + mt0v * ny);
+                            const int nid = smtb[v] + nx + smt0[v] * (ny + smt1[v] * nz);
                             if (S.use_list) {    // a mask that was empty: list the mini-tile
                                 const unsigned long long old = atomicOr(&dnext[nid], bits);
                                 if (old == 0ull)

@@ -23,11 +23,12 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_sw
 python tools/ncu_roofline.py gpurun_out/$TAG/ncu_c3_fine.ncu-rep c3_zermelo_4097 gpurun_out/$TAG/ncu_roofline_c3_zermelo_4097.json k_sweep_local2d_coop 2>&1 | grep -E "duration|issue|warp_inst|threads_per|fma_pipe|l2_gbs|barrier|wait"
 python tools/ncu_source.py gpurun_out/$TAG/ncu_c3_fine.ncu-rep 40 > gpurun_out/$TAG/ncu_c3_fine_hotspots.txt 2>&1
 python tools/ncu_summary.py gpurun_out/$TAG/ncu_c3_fine.ncu-rep > gpurun_out/$TAG/ncu_c3_fine_summary.txt 2>&1
+python tools/ncu_sass_dump.py gpurun_out/$TAG/ncu_c3_fine.ncu-rep gpurun_out/$TAG/sass_c3.txt
 mv gpurun_out/$TAG/ncu_c3_fine.ncu-rep /tmp/   # (reports stay on the box: gpurun_out is capped at 64 MiB)
-python tools/prof_solve.py 5 f32 field_col fine 1 20 > /dev/null 2>&1 && \
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_sweep_field2d_col --launch-skip 10 --launch-count 1 \
-    -o gpurun_out/$TAG/ncu_c5_col python tools/prof_solve.py 5 f32 field_col fine 1 20 > gpurun_out/$TAG/ncu5.log 2>&1; echo "ncu c5 rc=$?"
-python tools/ncu_roofline.py gpurun_out/$TAG/ncu_c5_col.ncu-rep c5_regulator_16385 gpurun_out/$TAG/ncu_roofline_c5_regulator_16385.json k_sweep_field2d_col > /dev/null 2>&1
+python tools/prof_solve.py 5 f32 auto fine 1 20 > /dev/null 2>&1 && \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_sweep_field2d_lat --launch-skip 10 --launch-count 1 \
+    -o gpurun_out/$TAG/ncu_c5_col python tools/prof_solve.py 5 f32 auto fine 1 20 > gpurun_out/$TAG/ncu5.log 2>&1; echo "ncu c5 rc=$?"
+python tools/ncu_roofline.py gpurun_out/$TAG/ncu_c5_col.ncu-rep c5_regulator_16385 gpurun_out/$TAG/ncu_roofline_c5_regulator_16385.json k_sweep_field2d_lat > /dev/null 2>&1
 python tools/ncu_source.py gpurun_out/$TAG/ncu_c5_col.ncu-rep 40 > gpurun_out/$TAG/ncu_c5_col_hotspots.txt 2>&1
 mv gpurun_out/$TAG/ncu_c5_col.ncu-rep /tmp/
 du -sh gpurun_out/$TAG
