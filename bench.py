@@ -394,8 +394,10 @@ def main():
                        "parallelism": f"sub-domains over {world} GPU(s), one MIN all-reduce",
                        "labeller": args.labeller,
                        "l2": "flushed (256 MiB write) between timed steps"},
-            "value_note": "evaluated node x control updates (work the kernels performed; "
-                          "exactly skipped nodes not counted) / time-to-solution",
+            "value_note": "evaluated node x control updates: the brackets the kernels "
+                          "computed (exactly skipped nodes, and control segments the "
+                          "cooperative field kernel prunes by their exact corner bound, are "
+                          "not counted) / time-to-solution",
             "time_to_solution_ms": total_ms / args.steps,
             "step_ms": [round(x, 3) for x in step_ms],
             "nominal_updates_per_s": nominal / (total_ms / 1e3),

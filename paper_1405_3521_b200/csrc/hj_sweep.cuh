@@ -1389,6 +1389,9 @@ hj_status sweep_prepare(const hj_grid &g, const hj_problem &p, const hj_fields &
         (want == HJ_SWEEP_AUTO || want == HJ_SWEEP_DUBINS_COOP))
         L.coop = true;         // (x, y) feet within one cell: the cooperative kernel
     L.evals = p.n_controls;
+    // the cooperative field class counts the brackets it computes itself (its segment
+    // pruning skips some): the work counter is already node x control
+    if (L.kind == SWEEP_FIELD2D && L.coop) L.evals = 1;
     if (L.kind == SWEEP_DUBINS && L.coop && p.cost == HJ_COST_KRUZKOV) {
         // coop_eval_dubins evaluates only each heading-sign group's extreme |d_k|
         double e[4] = {INFINITY, -INFINITY, INFINITY, -INFINITY};

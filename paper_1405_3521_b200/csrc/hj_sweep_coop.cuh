@@ -387,6 +387,7 @@ __device__ __forceinline__ void coop_eval_field(const DevProblem<T, T> &P, const
             base = P.h * cost_state(P, x);
         }
         T best = mono ? V00 : (T)INFINITY;
+        int nb = P.K;            // brackets computed for this node (segment pruning: fewer)
         if ((di >> loc) & 1ull) {
             // one-sided and cross differences, prescaled by beta
             const T Vp0 = q0[1], Vm0 = q0[-1], V0p = q0[BP], V0m = q0[-BP];
@@ -430,7 +431,10 @@ __device__ __forceinline__ void coop_eval_field(const DevProblem<T, T> &P, const
                         const T lb = fmin(fmin(ca, cb), fmin(da, db));
                         const T slack = (fabs(C0) + fabs(A1) + fabs(A2) + fabs(A3)) *
                                         T(9.5367431640625e-07);        // 2^-20
-                        if (lb - slack >= best) continue;
+                        if (lb - slack >= best) {
+                            nb -= bnd[q + 1] - bnd[q];
+                            continue;
+                        }
                     }
 #pragma unroll 4
                     for (int k = bnd[q]; k < bnd[q + 1]; ++k) {
@@ -507,7 +511,7 @@ __device__ __forceinline__ void coop_eval_field(const DevProblem<T, T> &P, const
             best = mono ? fmin(eb, V00) : eb;
         }
         Vo[(x0 + c) + vn0 * (y0 + r)] = best;
-        ++evald;
+        evald += nb;
         if (!same_bits(best, V00)) {
             cm |= 1ull << loc;
             const T dv = best > V00 ? best - V00 : V00 - best;
