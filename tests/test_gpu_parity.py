@@ -341,6 +341,34 @@ def test_field_lat_full_size_config5_matches_field2d():
     assert hj.lib() is not None
 
 
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+@pytest.mark.parametrize("case", ["k96_lr", "one_sided"])
+def test_local_coop_many_controls_and_empty_quadrants(case, dtype):
+    """The cooperative local kernel with 24 controls per quadrant and per-control costs
+    (the fp64 CTA has 256 threads, fewer than the 12 KQ = 288 table entries: the table is
+    filled by a strided loop), and with a one-sided control set (two quadrants empty: the
+    +inf padding needs the per-control cost table) — against the one-sweep scalar kernel
+    bit for bit and the oracle."""
+    if case == "k96_lr":
+        ctrl = W.unit_circle_controls(96)
+    else:                               # the upper half plane only
+        th = np.pi * (np.arange(40) + 0.5) / 40
+        ctrl = np.stack([np.cos(th), np.sin(th), np.zeros_like(th)], axis=1)
+    g = W.Grid((65, 65), (-1.0, -1.0), (1.0, 1.0), (False, False))
+    h = g.spacing(0)
+    p = _tiny((65, 65), ctrl=ctrl, cost=W.COST_DISCOUNTED, lam=1.0, lq=1.0, lr=0.5,
+              v_out=2.5 * (1.0 + h), h=h, tol=1e-10 if dtype == "f64" else 1e-6)
+    Vo, it_o, _ = oracle.OracleProblem(p).solve()
+    out = {}
+    for kernel in ("local_scalar", "local_coop"):
+        V, rep = hj.hj_solve(hj.DeviceProblem(p, dtype, sweep_kernel=kernel))
+        assert rep["converged"]
+        assert np.abs(V.double().cpu().numpy() - Vo).max() <= TOL[dtype] * 10, kernel
+        out[kernel] = (V.cpu(), rep["iterations"])
+    assert torch.equal(out["local_scalar"][0], out["local_coop"][0])
+    assert out["local_scalar"][1] == out["local_coop"][1]
+
+
 def test_local_kernel_refuses_nonlocal_problem():
     cfg = _cfg(3)                        # Zermelo drift: feet leave the 3x3 cell block
     with pytest.raises(hj.HJError, match="does not qualify"):
