@@ -54,9 +54,10 @@ def load_peaks():
 
 def ncu_evidence(workload):
     """The newest committed ncu summary of this workload's dominant kernel
-    (profiles/<round>/ncu_roofline_<workload>.json, tools/ncu_roofline.py)."""
-    paths = sorted(glob.glob(os.path.join(ROOT, "profiles", "*", f"ncu_roofline_{workload}.json")),
-                   key=os.path.getmtime)
+    (profiles/<round>/ncu_roofline_<workload>.json, tools/ncu_roofline.py).  Newest = the
+    last session directory in name order (r01 < ... < r13 < r2 < r2s < r2u): file mtimes
+    are all equal in a fresh checkout."""
+    paths = sorted(glob.glob(os.path.join(ROOT, "profiles", "*", f"ncu_roofline_{workload}.json")))
     if not paths:
         return None
     with open(paths[-1]) as f:

@@ -287,7 +287,9 @@ def config5(seed: int = 5, scale: float = 1.0, ratio=None) -> Config:
     """2D discounted regulator: f = (x2, a - 0.5 x1), 33 controls in [-1,1],
     l = |x|^2 + 0.1 a^2, lambda = 1, [-2,2]^2, 16385^2 fp32, 32 sub-domains from
     a 513^2 coarse feedback, tol 1e-6.  Reading R12: target B(0,0.2) cut in 32
-    sectors (paper §4.1 "slices of a cake"); reading R5b: h = dx^(2/3)."""
+    sectors (paper §4.1 "slices of a cake"); reading R5b: h = dx^(2/3).  Reading R13b: the
+    band (unstated) is two coarse cells, 2 x ratio fine cells — the coarse feedback's
+    trajectories leave thinner sets (measured at full size, R13b)."""
     ratio = 32 if ratio is None else int(ratio)
     n = _scaled(16385, scale, ratio)
     g = Grid((n, n), (-2.0, -2.0), (2.0, 2.0), (False, False))
@@ -305,7 +307,7 @@ def config5(seed: int = 5, scale: float = 1.0, ratio=None) -> Config:
                        piece=sector_pieces(grid, 0.2, 32), n_pieces=32, A=A,
                        lq=1.0, lr=0.1, v_out=h * l_max / (1.0 - beta), name="regulator32")
     cg = coarse_grid(g, (ratio, ratio))
-    return Config("c5_regulator_16385", mk(g), mk(cg), m=32, band=4, ratio=(ratio, ratio),
+    return Config("c5_regulator_16385", mk(g), mk(cg), m=32, band=2 * ratio, ratio=(ratio, ratio),
                   dtype="f32", n_max_steps=int(40.0 / mk(cg).h))
 
 
