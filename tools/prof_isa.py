@@ -34,3 +34,17 @@ for r in range(reps):
         print(f"  sets {n}, labels -1: {int((lab['label'] == -1).sum())}, exit set (-2): "
               f"{int((lab['label'] == -2).sum())}, sum|S_k|/N = {sum(cover) / fine.N:.3f}, "
               f"sum box/N = {sum(p.box_nodes for p in res['plan']) / fine.N:.3f}", flush=True)
+    if "--shares" in sys.argv:
+        # per-set work actually done (evaluated updates) and the LPT split over 2/4/8 ranks
+        # (hj_assign_subdomains' own assignment): the largest rank's share of the work bounds
+        # the partitioned solve's parallel efficiency
+        work = [x["evaluated_updates"] if x else 0 for x in res["reports"]]
+        tot = float(sum(work))
+        print("  per set: " + ", ".join(f"{k}:{x['iterations']}sw/{p.n_nodes / fine.N:.3f}N/"
+                                         f"{w / tot:.3f}" for k, (x, p, w) in
+                                         enumerate(zip(res["reports"], res["plan"], work)) if x))
+        for world in (2, 4, 8):
+            owners = hj.hj_assign_subdomains(res["plan"], world)
+            per = [sum(w for w, o in zip(work, owners) if o == r) for r in range(world)]
+            print(f"  world {world}: rank work shares {[round(p / tot, 3) for p in per]}; "
+                  f"max-rank bound on efficiency {tot / (world * max(per)):.3f}", flush=True)
