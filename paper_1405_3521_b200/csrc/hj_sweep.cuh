@@ -1813,6 +1813,14 @@ hj_status sweep_coop(const DevProblem<T, T> &P, const SweepLaunch<T> &L, int64_t
     if (S.cluster) S.seg_tab = 0;      // (cluster mode sizes its shared memory once)
     S.seg_prune = L.seg && !getenv("HJ_NO_SEGPRUNE") ? 1 : 0;
     if (S.cluster) S.use_list = 0;    // (the list ring is shared by all views)
+    // inter-CTA dynamic tail and single-item claims at the end of a CTA's queue
+    // (CoopState::tail16 / tch / qsingle; defaults measured on config 3)
+    S.tail16 = 0;
+    S.tch = 32;
+    S.qsingle = 0;
+    if (const char *e = getenv("HJ_COOP_TAIL")) S.tail16 = std::max(0, std::min(16, atoi(e)));
+    if (const char *e = getenv("HJ_COOP_TCH")) S.tch = std::max(2, std::min(512, atoi(e)));
+    if (const char *e = getenv("HJ_COOP_QSINGLE")) S.qsingle = std::max(0, atoi(e));
     {
         std::vector<int> ord(nv);
         for (int v = 0; v < nv; ++v) ord[v] = v;

@@ -41,7 +41,8 @@ struct CoopState {
     unsigned long long *dmask[2];   // [total] nodes to evaluate in sweep n (parity n)
     int32_t *items[2];              // [total] mini-tiles with a nonzero mask (parity n)
     int32_t *count;                 // [3] ring: sweep n reads count[n % 3]; [3] the grid
-                                    // barrier
+                                    // barrier; [4..6] ring: claimed items of the sweep's
+                                    // dynamic tail (tail16)
     int64_t *stop;                  // [n_views] iterations performed (output)
     int use_list;                   // 1: walk items/count (many mini-tiles); 0: scan all
     int dubins;                     // 3-D Dubins views: 8 x 8 mini-tiles per heading plane
@@ -56,6 +57,11 @@ struct CoopState {
     int seg_prune;                  // 1: skip segments by their corner bound (exact)
     int seg_tab;                    // 1: the per-row split points are tabulated in dynamic
                                     // shared memory once per launch (2 x n1 int16)
+    // load balance (list mode): the last tail16/16 of a sweep's list is not pre-assigned;
+    // CTAs that finish their strided share claim it in chunks of tch mini-tiles from the
+    // ring counter count[4 + n % 3] (one atomic per chunk, not per item); and the last
+    // qsingle items of a CTA's queue are claimed one at a time instead of in pairs
+    int tail16, tch, qsingle;
     int16_t seg_order[HJ_MAX_CONTROLS];
 };
 
@@ -730,6 +736,7 @@ __global__ void __launch_bounds__(CoopNW<T>::nw * 32,
     __shared__ unsigned long long qmask[COOP_NW * 32], qemask[COOP_NW * 32];
     __shared__ int wcnt[COOP_NW];
     __shared__ int qnext;          // the next unclaimed queue position (warps claim pairs)
+    __shared__ int qbase;          // the dynamic tail chunk this CTA claimed (CoopState::tail16)
     // per-CTA max of the sweep's |V^{n+1} - V^n| as the bits of a T >= 0 (monotone as
     // unsigned: native shared atomicMax, no CAS loop), evaluated-node count
     __shared__ typename CoopBits<T>::U cres[HJ_GROUP_VIEWS];
@@ -868,17 +875,42 @@ __global__ void __launch_bounds__(CoopNW<T>::nw * 32,
         const int64_t ncand =
             S.use_list ? (int64_t)*(volatile const int32_t *)&S.count[n % 3] : ctot;
         const int32_t *litems = S.items[n & 1];
-        const int64_t per_cta = ncand > grank ? (ncand - grank + gsize - 1) / gsize : 0;
-        for (int64_t ch = 0; ch < per_cta; ch += COOP_NW * 32) {
+        // dynamic tail (list mode): the list's last `tail` items are claimed in chunks by
+        // whichever CTA has finished its strided share of the first `nstat`
+        const int64_t tail = !CL && S.use_list && S.tail16 > 0 ? (ncand * S.tail16) >> 4 : 0;
+        const int64_t nstat = ncand - tail;
+        const int tch = min(S.tch, COOP_NW * 32);     // a chunk is one queue fill
+        const int64_t per_cta = nstat > grank ? (nstat - grank + gsize - 1) / gsize : 0;
+        int64_t ch = 0;
+        bool dyn = false;
+        for (;;) {
+        bool have;
+        int64_t idx;
+        if (!dyn) {
+            if (ch >= per_cta) {
+                if (tail <= 0) break;
+                dyn = true;
+                continue;
+            }
+            const int64_t k = ch + threadIdx.x;
+            have = k < per_cta;
+            idx = grank + k * (int64_t)gsize;
+            ch += COOP_NW * 32;
+        } else {
+            if (threadIdx.x == 0) qbase = atomicAdd(&S.count[4 + n % 3], tch);
+            __syncthreads();
+            const int tb = qbase;
+            if (tb >= tail) break;                  // (every thread: the same value)
+            have = (int)threadIdx.x < tch && tb + (int64_t)threadIdx.x < tail;
+            idx = nstat + tb + threadIdx.x;
+        }
         int chunk_n;
         {
-            const int64_t k = ch + threadIdx.x;
-            const int64_t idx = grank + k * (int64_t)gsize;
-            const int64_t g = k < per_cta ? (S.use_list ? (int64_t)litems[idx] : cbase + idx) : 0;
-            const unsigned long long m = k < per_cta ? dcur[g] : 0ull;
+            const int64_t g = have ? (S.use_list ? (int64_t)litems[idx] : cbase + idx) : 0;
+            const unsigned long long m = have ? dcur[g] : 0ull;
             // the class masks ride along with the dirty mask (one round trip for all three)
-            const unsigned long long cim = k < per_cta ? S.imask[g] : 0ull;
-            const unsigned long long cem = k < per_cta ? S.emask[g] : 0ull;
+            const unsigned long long cim = have ? S.imask[g] : 0ull;
+            const unsigned long long cem = have ? S.emask[g] : 0ull;
             const unsigned bal = __ballot_sync(0xffffffffu, m != 0ull);
             if (lane == 0) wcnt[warp] = __popc(bal);
             __syncthreads();
@@ -918,18 +950,28 @@ __global__ void __launch_bounds__(CoopNW<T>::nw * 32,
         // (HJ_COOP_DUBINS_DYNQ=0: the Dubins class takes the static split (warp, warp + NW),
         // (warp + 2 NW, ...) instead)
         constexpr bool DYNQ = EV != 3 || HJ_COOP_DUBINS_DYNQ;
+        // (the queue's last qsingle items go one per claim: a finer tail for the CTA barrier)
+        const int pz = DYNQ ? cnt - min(cnt, S.qsingle) : cnt;     // items claimed in pairs
+        const int npair = (pz + 1) >> 1;
         for (int itw = warp;; itw += 2 * COOP_NW) {
-            int it = itw;
+            int it = itw, lim2 = cnt;
             if (DYNQ) {
-                if (lane == 0) it = atomicAdd(&qnext, 2);
+                if (lane == 0) it = atomicAdd(&qnext, 1);
                 it = __shfl_sync(0xffffffffu, it, 0);
+                if (it < npair) {
+                    it *= 2;
+                    lim2 = pz;
+                } else {
+                    it = pz + (it - npair);
+                    lim2 = 0;                                      // a single item
+                }
             }
             if (it >= cnt) break;
             const int it2 = DYNQ ? it + 1 : it + COOP_NW;    // the pair's second item
             // 32-bit mini-tile arithmetic (ids are int32; a 2-D view's nodes < 2^31)
             int gid[2];
             gid[0] = qgid[it];
-            gid[1] = it2 < cnt ? qgid[it2] : -1;
+            gid[1] = it2 < lim2 ? qgid[it2] : -1;
             int vv[2], mx[2], my[2], mz[2];
             unsigned long long dd[2], em[2];
 #ifdef HJ_DEBUG_BOUNDS
@@ -1140,7 +1182,10 @@ __global__ void __launch_bounds__(CoopNW<T>::nw * 32,
             if (m > 0.0) atomic_max_nonneg(&sview[v].res[n], m);
             if (w) atomicAdd(sview[v].work, w);
         }
-        if (S.use_list && blockIdx.x == 0 && threadIdx.x == 0) S.count[(n + 2) % 3] = 0;
+        if (S.use_list && blockIdx.x == 0 && threadIdx.x == 0) {
+            S.count[(n + 2) % 3] = 0;
+            S.count[4 + (n + 2) % 3] = 0;
+        }
         if (tr) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_b));
         if (tr_all && n < tr_cap) {
             unsigned long long t_arr;              // every CTA's arrival (load balance)
