@@ -1813,13 +1813,15 @@ hj_status sweep_coop(const DevProblem<T, T> &P, const SweepLaunch<T> &L, int64_t
     if (S.cluster) S.seg_tab = 0;      // (cluster mode sizes its shared memory once)
     S.seg_prune = L.seg && !getenv("HJ_NO_SEGPRUNE") ? 1 : 0;
     if (S.cluster) S.use_list = 0;    // (the list ring is shared by all views)
-    // inter-CTA dynamic tail and single-item claims at the end of a CTA's queue
-    // (CoopState::tail16 / tch / qsingle; defaults measured on config 3)
-    S.tail16 = 0;
-    S.tch = 32;
-    S.qsingle = 0;
-    if (const char *e = getenv("HJ_COOP_TAIL")) S.tail16 = std::max(0, std::min(16, atoi(e)));
-    if (const char *e = getenv("HJ_COOP_TCH")) S.tch = std::max(2, std::min(512, atoi(e)));
+    // load balance inside a CTA (CoopState::qsingle / heavy): the last 32 items of a CTA's
+    // queue are claimed one at a time, and mini-tiles with more than 24 listed nodes are
+    // queued in front of the lighter ones (longest first).  Measured on config 3's
+    // whole-grid solve: 503 -> 481 ms (single claims) -> 476.5 ms (both); config 2 -2 %
+    // (profiles/r2v/balance_ab.txt).  The Dubins class, whose items stage three planes,
+    // lost 2 % with single claims and 0.4 % with the order: pairs only, list order.
+    S.qsingle = L.kind == SWEEP_DUBINS ? 0 : 32;
+    S.heavy = L.kind == SWEEP_DUBINS ? -1 : 24;
+    if (const char *e = getenv("HJ_COOP_HEAVY")) S.heavy = std::max(-1, std::min(64, atoi(e)));
     if (const char *e = getenv("HJ_COOP_QSINGLE")) S.qsingle = std::max(0, atoi(e));
     {
         std::vector<int> ord(nv);

@@ -41,8 +41,7 @@ struct CoopState {
     unsigned long long *dmask[2];   // [total] nodes to evaluate in sweep n (parity n)
     int32_t *items[2];              // [total] mini-tiles with a nonzero mask (parity n)
     int32_t *count;                 // [3] ring: sweep n reads count[n % 3]; [3] the grid
-                                    // barrier; [4..6] ring: claimed items of the sweep's
-                                    // dynamic tail (tail16)
+                                    // barrier
     int64_t *stop;                  // [n_views] iterations performed (output)
     int use_list;                   // 1: walk items/count (many mini-tiles); 0: scan all
     int dubins;                     // 3-D Dubins views: 8 x 8 mini-tiles per heading plane
@@ -57,11 +56,11 @@ struct CoopState {
     int seg_prune;                  // 1: skip segments by their corner bound (exact)
     int seg_tab;                    // 1: the per-row split points are tabulated in dynamic
                                     // shared memory once per launch (2 x n1 int16)
-    // load balance (list mode): the last tail16/16 of a sweep's list is not pre-assigned;
-    // CTAs that finish their strided share claim it in chunks of tch mini-tiles from the
-    // ring counter count[4 + n % 3] (one atomic per chunk, not per item); and the last
-    // qsingle items of a CTA's queue are claimed one at a time instead of in pairs
-    int tail16, tch, qsingle;
+    // load balance inside a CTA: the last qsingle items of its queue are claimed one at a
+    // time instead of in pairs (a finer tail in front of the CTA barrier)
+    int qsingle;
+    int heavy;                      // queue order: items with more than `heavy` listed nodes
+                                    // first (-1: every item, i.e. the list's own order)
     int16_t seg_order[HJ_MAX_CONTROLS];
 };
 
@@ -736,7 +735,6 @@ __global__ void __launch_bounds__(CoopNW<T>::nw * 32,
     __shared__ unsigned long long qmask[COOP_NW * 32], qemask[COOP_NW * 32];
     __shared__ int wcnt[COOP_NW];
     __shared__ int qnext;          // the next unclaimed queue position (warps claim pairs)
-    __shared__ int qbase;          // the dynamic tail chunk this CTA claimed (CoopState::tail16)
     // per-CTA max of the sweep's |V^{n+1} - V^n| as the bits of a T >= 0 (monotone as
     // unsigned: native shared atomicMax, no CAS loop), evaluated-node count
     __shared__ typename CoopBits<T>::U cres[HJ_GROUP_VIEWS];
@@ -875,57 +873,40 @@ __global__ void __launch_bounds__(CoopNW<T>::nw * 32,
         const int64_t ncand =
             S.use_list ? (int64_t)*(volatile const int32_t *)&S.count[n % 3] : ctot;
         const int32_t *litems = S.items[n & 1];
-        // dynamic tail (list mode): the list's last `tail` items are claimed in chunks by
-        // whichever CTA has finished its strided share of the first `nstat`
-        const int64_t tail = !CL && S.use_list && S.tail16 > 0 ? (ncand * S.tail16) >> 4 : 0;
-        const int64_t nstat = ncand - tail;
-        const int tch = min(S.tch, COOP_NW * 32);     // a chunk is one queue fill
-        const int64_t per_cta = nstat > grank ? (nstat - grank + gsize - 1) / gsize : 0;
-        int64_t ch = 0;
-        bool dyn = false;
-        for (;;) {
-        bool have;
-        int64_t idx;
-        if (!dyn) {
-            if (ch >= per_cta) {
-                if (tail <= 0) break;
-                dyn = true;
-                continue;
-            }
-            const int64_t k = ch + threadIdx.x;
-            have = k < per_cta;
-            idx = grank + k * (int64_t)gsize;
-            ch += COOP_NW * 32;
-        } else {
-            if (threadIdx.x == 0) qbase = atomicAdd(&S.count[4 + n % 3], tch);
-            __syncthreads();
-            const int tb = qbase;
-            if (tb >= tail) break;                  // (every thread: the same value)
-            have = (int)threadIdx.x < tch && tb + (int64_t)threadIdx.x < tail;
-            idx = nstat + tb + threadIdx.x;
-        }
+        const int64_t per_cta = ncand > grank ? (ncand - grank + gsize - 1) / gsize : 0;
+        for (int64_t ch = 0; ch < per_cta; ch += COOP_NW * 32) {
         int chunk_n;
         {
-            const int64_t g = have ? (S.use_list ? (int64_t)litems[idx] : cbase + idx) : 0;
-            const unsigned long long m = have ? dcur[g] : 0ull;
+            const int64_t k = ch + threadIdx.x;
+            const int64_t idx = grank + k * (int64_t)gsize;
+            const int64_t g = k < per_cta ? (S.use_list ? (int64_t)litems[idx] : cbase + idx) : 0;
+            const unsigned long long m = k < per_cta ? dcur[g] : 0ull;
             // the class masks ride along with the dirty mask (one round trip for all three)
-            const unsigned long long cim = have ? S.imask[g] : 0ull;
-            const unsigned long long cem = have ? S.emask[g] : 0ull;
-            const unsigned bal = __ballot_sync(0xffffffffu, m != 0ull);
-            if (lane == 0) wcnt[warp] = __popc(bal);
+            const unsigned long long cim = k < per_cta ? S.imask[g] : 0ull;
+            const unsigned long long cem = k < per_cta ? S.emask[g] : 0ull;
+            // the queue is filled from both ends: mini-tiles with more than `heavy` listed
+            // nodes from the front (claimed first, in pairs), the lighter ones from the back
+            // (they end up in the single-claim tail) — longest first in front of the barrier
+            const bool hv = m != 0ull && __popcll(m & (cim | cem)) > S.heavy;
+            const unsigned bal = __ballot_sync(0xffffffffu, hv);
+            const unsigned ball = __ballot_sync(0xffffffffu, m != 0ull && !hv);
+            if (lane == 0) wcnt[warp] = __popc(bal) | (__popc(ball) << 16);
             __syncthreads();
-            // this warp's offset and the chunk's total: one shared load + two warp
-            // reductions (lane w holds warp w's count)
+            // this warp's offsets and the chunk's totals: one shared load + two warp
+            // reductions (lane w holds warp w's counts, heavy | light << 16)
             const int wc = lane < COOP_NW ? wcnt[lane] : 0;
             const int base_i = __reduce_add_sync(0xffffffffu, lane < warp ? wc : 0);
+            const int tot_i = __reduce_add_sync(0xffffffffu, wc);
+            chunk_n = (tot_i & 0xffff) + (tot_i >> 16);
             if (m) {
-                const int pos = base_i + __popc(bal & ((1u << lane) - 1u));
+                const unsigned lt = (1u << lane) - 1u;
+                const int pos = hv ? (base_i & 0xffff) + __popc(bal & lt)
+                                   : chunk_n - 1 - ((base_i >> 16) + __popc(ball & lt));
                 qgid[pos] = (int32_t)g;
                 qmask[pos] = m & cim;
                 qemask[pos] = m & cem;
                 dcur[g] = 0ull;                    // consumed
             }
-            chunk_n = __reduce_add_sync(0xffffffffu, wc);
             if (threadIdx.x == 0) qnext = 0;
             __syncthreads();                       // the queue is complete
         }
@@ -1182,10 +1163,7 @@ __global__ void __launch_bounds__(CoopNW<T>::nw * 32,
             if (m > 0.0) atomic_max_nonneg(&sview[v].res[n], m);
             if (w) atomicAdd(sview[v].work, w);
         }
-        if (S.use_list && blockIdx.x == 0 && threadIdx.x == 0) {
-            S.count[(n + 2) % 3] = 0;
-            S.count[4 + (n + 2) % 3] = 0;
-        }
+        if (S.use_list && blockIdx.x == 0 && threadIdx.x == 0) S.count[(n + 2) % 3] = 0;
         if (tr) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_b));
         if (tr_all && n < tr_cap) {
             unsigned long long t_arr;              // every CTA's arrival (load balance)

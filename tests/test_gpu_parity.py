@@ -188,29 +188,35 @@ def test_coop_list_mode_matches_scan_mode(idx, kernel, oracle_cache, monkeypatch
 
 @pytest.mark.parametrize("idx,kernel", [(1, "local_coop"), (2, "local_coop"), (3, "field_coop"),
                                         (4, "dubins_coop")])
-@pytest.mark.parametrize("tail,tch,qsingle", [("8", "32", "0"), ("16", "2", "0"), ("5", "64", "16"),
-                                              ("0", "32", "1000")])
-def test_coop_dynamic_tail_bit_identical(idx, kernel, tail, tch, qsingle, monkeypatch):
-    """Load balance of the cooperative sweep in list mode (CoopState::tail16/tch/qsingle): part
-    of each sweep's list is claimed in chunks by whichever CTA is free, and the end of a
-    CTA's queue goes one mini-tile per claim.  Which CTA or warp evaluates a mini-tile cannot
-    change a Jacobi sweep: iterates, sweep counts and evaluated work must be identical to
-    the static assignment, for the whole-grid solve and the partitioned ISA pass."""
+@pytest.mark.parametrize("lst", ["0", "1"])
+def test_coop_single_claims_bit_identical(idx, kernel, lst, monkeypatch):
+    """Load balance inside a CTA of the cooperative sweep (CoopState::qsingle / heavy): the last
+    items of a CTA's queue go one mini-tile per claim instead of two, and mini-tiles with
+    many listed nodes are queued first.  Which warp evaluates a mini-tile, when, alone or
+    paired, cannot change a Jacobi sweep: iterates, sweep counts and
+    evaluated work must be identical for every setting (pairs only, the default, an odd
+    count, singles only), for the whole-grid solve and the partitioned ISA pass, in both
+    enumeration modes."""
     cfg = _cfg(idx)
-    monkeypatch.setenv("HJ_COOP_LIST", "1")
+    monkeypatch.setenv("HJ_COOP_LIST", lst)
     out = []
-    for t, c, q in (("0", "32", "0"), (tail, tch, qsingle)):
-        monkeypatch.setenv("HJ_COOP_TAIL", t)
-        monkeypatch.setenv("HJ_COOP_TCH", c)
-        monkeypatch.setenv("HJ_COOP_QSINGLE", q)
+    # (pairs only in list order; the defaults; an odd tail with a low threshold; singles only
+    # with every nonempty item "heavy")
+    for q, h in (("0", "-1"), (None, None), ("7", "10"), ("100000", "0")):
+        for var, val in (("HJ_COOP_QSINGLE", q), ("HJ_COOP_HEAVY", h)):
+            if val is None:
+                monkeypatch.delenv(var, raising=False)
+            else:
+                monkeypatch.setenv(var, val)
         V, rep = hj.hj_solve(hj.DeviceProblem(cfg.fine, "f32", sweep_kernel=kernel),
                              tol=max(cfg.fine.tol, 1e-7))
         res = pipeline.run_isa(cfg, "f32")
         out.append((V.cpu(), rep["iterations"], rep["evaluated_updates"], res["V"].cpu(),
                     [r["iterations"] for r in res["reports"] if r]))
-    a, b = out
-    assert torch.equal(a[0], b[0]) and a[1] == b[1] and a[2] == b[2]
-    assert torch.equal(a[3], b[3]) and a[4] == b[4]
+    a = out[0]
+    for b in out[1:]:
+        assert torch.equal(a[0], b[0]) and a[1] == b[1] and a[2] == b[2]
+        assert torch.equal(a[3], b[3]) and a[4] == b[4]
 
 
 @pytest.mark.parametrize("dtype", ["f32", "f64"])
