@@ -902,6 +902,11 @@ __global__ void __launch_bounds__(CoopNW<T>::nw * 32,
                 const unsigned lt = (1u << lane) - 1u;
                 const int pos = hv ? (base_i & 0xffff) + __popc(bal & lt)
                                    : chunk_n - 1 - ((base_i >> 16) + __popc(ball & lt));
+#ifdef HJ_DEBUG_BOUNDS
+                if (pos < 0 || pos >= chunk_n || chunk_n > COOP_NW * 32)
+                    printf("HJ_DEBUG queue: n %lld pos %d chunk_n %d\n", (long long)n, pos, chunk_n),
+                        __trap();
+#endif
                 qgid[pos] = (int32_t)g;
                 qmask[pos] = m & cim;
                 qemask[pos] = m & cem;
