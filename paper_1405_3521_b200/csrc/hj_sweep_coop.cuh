@@ -26,7 +26,12 @@
 
 #include <cooperative_groups.h>
 
+#ifndef HJ_SEG_UNROLL
+#define HJ_SEG_UNROLL 4      // the segmented control loop (2: +1.6 %, 8: +6 %; balance_ab.txt)
+#endif
+
 namespace hj {
+constexpr int kSegUnroll = HJ_SEG_UNROLL;
 
 // keep a value in a register as computed (stops the compiler from re-deriving it from
 // its inputs inside a loop, which it otherwise does under register pressure)
@@ -441,7 +446,7 @@ __device__ __forceinline__ void coop_eval_field(const DevProblem<T, T> &P, const
                             continue;
                         }
                     }
-#pragma unroll 4
+#pragma unroll(kSegUnroll)
                     for (int k = bnd[q]; k < bnd[q + 1]; ++k) {
                         const T w0 = fabs(fma(S0, seg[k].u0, D0));
                         const T ck = kruz ? C0 : C0 + hlr * seg_csq[k];
