@@ -704,6 +704,9 @@ struct CoopBits<double> {
 #ifndef HJ_COOP_MINB32
 #define HJ_COOP_MINB32 1     // resident 512-thread CTAs per SM asked of ptxas for fp32
 #endif
+#ifndef HJ_COOP_NP
+#define HJ_COOP_NP 2
+#endif
 #ifndef HJ_COOP_NW32
 #define HJ_COOP_NW32 16      // warps per CTA for fp32
 #endif
@@ -941,8 +944,11 @@ __global__ void __launch_bounds__(CoopNW<T>::nw * 32,
         // (HJ_COOP_DUBINS_DYNQ=0: the Dubins class takes the static split (warp, warp + NW),
         // (warp + 2 NW, ...) instead)
         constexpr bool DYNQ = EV != 3 || HJ_COOP_DUBINS_DYNQ;
+        // items per claim at the front of the queue (HJ_COOP_NP=1, a build switch: one item
+        // per claim throughout — no pair state in registers; measured with two CTAs per SM)
+        constexpr int NP = EV == 3 ? 2 : HJ_COOP_NP;
         // (the queue's last qsingle items go one per claim: a finer tail for the CTA barrier)
-        const int pz = DYNQ ? cnt - min(cnt, S.qsingle) : cnt;     // items claimed in pairs
+        const int pz = DYNQ ? (NP == 1 ? 0 : cnt - min(cnt, S.qsingle)) : cnt;   // items claimed in pairs
         const int npair = (pz + 1) >> 1;
         for (int itw = warp;; itw += 2 * COOP_NW) {
             int it = itw, lim2 = cnt;
@@ -963,8 +969,8 @@ __global__ void __launch_bounds__(CoopNW<T>::nw * 32,
             int gid[2];
             gid[0] = qgid[it];
             gid[1] = it2 < lim2 ? qgid[it2] : -1;
-            int vv[2], mx[2], my[2], mz[2];
-            unsigned long long dd[2], em[2];
+            int vv[2] = {0, 0}, mx[2] = {0, 0}, my[2] = {0, 0}, mz[2] = {0, 0};
+            unsigned long long dd[2] = {0ull, 0ull}, em[2] = {0ull, 0ull};
 #ifdef HJ_DEBUG_BOUNDS
             if (it < 0 || it >= COOP_NW * 32 || gid[0] < 0 || gid[0] >= S.total ||
                 gid[1] >= S.total)
@@ -972,7 +978,7 @@ __global__ void __launch_bounds__(CoopNW<T>::nw * 32,
                        it, cnt, gid[0], gid[1], (long long)S.total), __trap();
 #endif
 #pragma unroll
-            for (int s2 = 0; s2 < 2; ++s2) {
+            for (int s2 = 0; s2 < NP; ++s2) {
                 const int g = gid[s2] < 0 ? gid[0] : gid[s2];
                 const int v = coop_view_warp(smtb, S.n_views, g);
                 const int mt = g - smtb[v], m0 = smt0[v];
@@ -997,7 +1003,7 @@ __global__ void __launch_bounds__(CoopNW<T>::nw * 32,
             constexpr int NLD = (BLK + 31) / 32;
             T ld[2][NLD], lsp[2][2];
 #pragma unroll
-            for (int s2 = 0; s2 < 2; ++s2) {
+            for (int s2 = 0; s2 < NP; ++s2) {
                 const SweepView<T> &vw = sview[vv[s2]];
                 const int vn0 = (int)vw.vn[0], vn1 = (int)vw.vn[1], vn2 = (int)vw.vn[2];
                 const T *__restrict__ Vi = vw.V[n & 1];
@@ -1055,7 +1061,7 @@ __global__ void __launch_bounds__(CoopNW<T>::nw * 32,
                 }
             }
 #pragma unroll
-            for (int s2 = 0; s2 < 2; ++s2) {
+            for (int s2 = 0; s2 < NP; ++s2) {
 #pragma unroll
                 for (int k = 0; k < NLD; ++k)
                     if (lane + 32 * k < BLK) blk[warp][s2][lane + 32 * k] = ld[s2][k];
@@ -1068,7 +1074,7 @@ __global__ void __launch_bounds__(CoopNW<T>::nw * 32,
             if (tr && t_l == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_l));
             unsigned long long cmv[2] = {0ull, 0ull};
 #pragma unroll 1
-            for (int s2 = 0; s2 < 2; ++s2) {
+            for (int s2 = 0; s2 < NP; ++s2) {
                 // (selects, not indexing: a runtime index would put the arrays in local memory)
                 const int v = s2 ? vv[1] : vv[0];
                 if ((s2 ? gid[1] : gid[0]) < 0 || ((stopped >> v) & 1u)) continue;
