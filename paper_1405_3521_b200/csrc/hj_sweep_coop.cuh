@@ -705,7 +705,10 @@ struct CoopBits<double> {
 #define HJ_COOP_MINB32 1     // resident 512-thread CTAs per SM asked of ptxas for fp32
 #endif
 #ifndef HJ_COOP_NP
-#define HJ_COOP_NP 2
+#define HJ_COOP_NP 2           // items per claim at the front of a CTA's queue, field class
+#endif
+#ifndef HJ_COOP_NP_LOCAL
+#define HJ_COOP_NP_LOCAL 1     // the same for the local class
 #endif
 #ifndef HJ_COOP_NW32
 #define HJ_COOP_NW32 16      // warps per CTA for fp32
@@ -946,7 +949,11 @@ __global__ void __launch_bounds__(CoopNW<T>::nw * 32,
         constexpr bool DYNQ = EV != 3 || HJ_COOP_DUBINS_DYNQ;
         // items per claim at the front of the queue (HJ_COOP_NP=1, a build switch: one item
         // per claim throughout — no pair state in registers; measured with two CTAs per SM)
-        constexpr int NP = EV == 3 ? 2 : HJ_COOP_NP;
+        // The local class takes one item per claim throughout: its sweeps hold few items per
+        // CTA, where the finer claims win (config 2 whole grid 8.28 -> 7.48 ms, ISA step
+        // 11.96 -> 11.31 ms); the field class keeps pairs + a single tail (config 3: 478 vs
+        // 514 ms singles only) — profiles/r2v/balance_ab.txt.
+        constexpr int NP = EV == 3 ? 2 : (EV == 0 ? HJ_COOP_NP_LOCAL : HJ_COOP_NP);
         // (the queue's last qsingle items go one per claim: a finer tail for the CTA barrier)
         const int pz = DYNQ ? (NP == 1 ? 0 : cnt - min(cnt, S.qsingle)) : cnt;   // items claimed in pairs
         const int npair = (pz + 1) >> 1;
